@@ -1,0 +1,153 @@
+"""ctypes binding of libadaptra.so (include/adaptra.h).  Argument marshalling
+only: every step of the path runs in the library's kernels / host code.
+
+The product path fails loudly when the library is missing: there is no CPU or
+PyTorch fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libadaptra.so")
+
+OK = 0
+EINVAL, EPLAN, EDEADLOCK, ECUDA, ENOMEM, ELINK, ETOOBIG = -1, -2, -3, -4, -5, -6, -7
+
+OP_F, OP_B, OP_W = 0, 1, 2
+SEL_PAPER, SEL_CAP, MERGE_W = 0, 1, 2
+F32, BF16 = 0, 1
+BLOCK_MLP, BLOCK_GPT = 0, 1
+
+EPI_STORE, EPI_GELU, EPI_RESID, EPI_DGELU, EPI_ACC_F32, EPI_STORE_F32, EPI_DSOFTMAX = range(7)
+CAUSAL_NONE, CAUSAL_TILE, CAUSAL_KEND, CAUSAL_KSTART = range(4)
+
+LINK_DIRECT, LINK_P2P, LINK_HOST = 0, 1, 2
+DIR_FWD, DIR_BWD = 0, 1
+LINK_DOWN = (1 << 63) - 1
+
+_i32, _i64, _u32, _f32, _vp = C.c_int32, C.c_int64, C.c_uint32, C.c_float, C.c_void_p
+
+
+class AdaptraError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"adaptra error {code}: {msg}")
+        self.code = code
+
+
+class Op(C.Structure):
+    _fields_ = [("kind", _i32), ("mb", _i32), ("start", _i64), ("end", _i64)]
+
+
+class GemmDesc(C.Structure):
+    _fields_ = [
+        ("dtype", _i32), ("M", _i32), ("N", _i32), ("K", _i32), ("Z", _i32), ("zdiv", _i32),
+        ("A", _vp), ("lda", _i64), ("a_rows", _i64), ("a_cols", _i64),
+        ("a_row1", _i64), ("a_row2", _i64), ("a_col1", _i64), ("a_col2", _i64),
+        ("a_mn", _i32), ("b_mn", _i32),
+        ("B", _vp), ("ldb", _i64), ("b_rows", _i64), ("b_cols", _i64),
+        ("b_row1", _i64), ("b_row2", _i64), ("b_col1", _i64), ("b_col2", _i64),
+        ("epi", _i32), ("causal", _i32), ("alpha", _f32), ("pad0", _i32),
+        ("C", _vp), ("ldc", _i64), ("c_1", _i64), ("c_2", _i64),
+        ("aux", _vp), ("ldaux", _i64), ("aux_1", _i64), ("aux_2", _i64),
+        ("R", _vp), ("ldr", _i64), ("bias", _vp), ("rowv", _vp), ("rowv_1", _i64), ("rowv_2", _i64),
+    ]
+
+
+class StageDesc(C.Structure):
+    _fields_ = [
+        ("block", _i32), ("dtype", _i32), ("n_layers", _i32), ("d", _i32), ("d_ff", _i32), ("n_heads", _i32),
+        ("b", _i32), ("T", _i32), ("is_first", _i32), ("is_last", _i32), ("n_microbatches", _i32),
+        ("n_slots", _i32), ("wts", _vp), ("vecs", _vp), ("gwts", _vp), ("gvecs", _vp),
+        ("stash", _vp), ("work", _vp),
+    ]
+
+
+class LinkDesc(C.Structure):
+    _fields_ = [
+        ("mode", _i32), ("n_mb", _i32), ("bytes", _i64), ("dev_up", _i32), ("dev_down", _i32),
+        ("fwd_mbox", _vp), ("bwd_mbox", _vp), ("fwd_flags", _vp), ("bwd_flags", _vp),
+        ("host_fwd", _vp), ("host_bwd", _vp),
+    ]
+
+
+class ExecDesc(C.Structure):
+    _fields_ = [
+        ("stage", _vp), ("stage_index", _i32), ("n_stages", _i32), ("n_microbatches", _i32),
+        ("link_up", _vp), ("link_down", _vp), ("compute_stream", _vp),
+        ("inputs", C.POINTER(_vp)), ("targets", C.POINTER(_vp)), ("loss_acc", _vp), ("merge_w", _u32),
+    ]
+
+
+class IterStats(C.Structure):
+    _fields_ = [("n_ops", _i64), ("busy_ns", _i64), ("first_start_ns", _i64), ("last_end_ns", _i64),
+                ("op_ns", _i64 * 3), ("op_cnt", _i64 * 3)]
+
+
+_P = C.POINTER
+_SIGS = {
+    "adaptra_last_error": (C.c_char_p, []),
+    "adaptra_version": (C.c_char_p, []),
+    "adaptra_plan_init": (_i32, [_i32, _i32, _i64, _i64, _P(_i32)]),
+    "adaptra_plan_adapt": (_i32, [_i32, _i32, _P(_i64), _P(_i64), _P(_i64), _P(_i32)]),
+    "adaptra_eq1_holds": (_i32, [_i32, _P(_i64), _P(_i64), _P(_i64), _P(_i32), _P(C.c_uint8)]),
+    "adaptra_schedule": (_i32, [_i32, _i32, _P(_i64), _P(_i64), _P(_i64), _P(_i64), _P(_i32), _i64, _u32,
+                                _P(Op), _P(_i32), _P(_i64), _P(_i64)]),
+    "adaptra_replay": (_i32, [_i32, _i32, _P(_i64), _P(_i64), _P(_i64), _P(_i64), _P(Op), _P(_i32), _u32,
+                              _P(Op), _P(_i64)]),
+    "adaptra_validate": (_i32, [_i32, _i32, _P(_i64), _P(_i64), _P(_i64), _P(_i64), _P(Op), _P(_i32), _u32,
+                                _P(_i32)]),
+    "adaptra_gemm": (_i32, [_P(GemmDesc), _vp]),
+    "adaptra_stage_slot_bytes": (_i64, [_P(StageDesc)]),
+    "adaptra_stage_work_bytes": (_i64, [_P(StageDesc)]),
+    "adaptra_stage_wts_elems": (_i64, [_P(StageDesc)]),
+    "adaptra_stage_vecs_elems": (_i64, [_P(StageDesc)]),
+    "adaptra_stage_create": (_i32, [_P(StageDesc), _P(_vp)]),
+    "adaptra_stage_destroy": (_i32, [_vp]),
+    "adaptra_stage_F": (_i32, [_vp, _i32, _vp, _vp, _vp, _vp, _vp]),
+    "adaptra_stage_B": (_i32, [_vp, _i32, _vp, _vp, _vp]),
+    "adaptra_stage_W": (_i32, [_vp, _i32, _vp]),
+    "adaptra_stage_zero_grads": (_i32, [_vp, _vp]),
+    "adaptra_link_open": (_i32, [_P(LinkDesc), _P(_vp)]),
+    "adaptra_link_close": (_i32, [_vp]),
+    "adaptra_set_link_latency": (_i32, [_vp, _i64]),
+    "adaptra_send": (_i32, [_vp, _i32, _i32, _vp, _vp, _u32]),
+    "adaptra_recv": (_i32, [_vp, _i32, _i32, _vp, _u32, _P(_vp)]),
+    "adaptra_link_stats": (_i32, [_vp, _P(_i64), _P(_i64), _P(_i64)]),
+    "adaptra_exec_create": (_i32, [_P(ExecDesc), _P(_vp)]),
+    "adaptra_exec_destroy": (_i32, [_vp]),
+    "adaptra_run_iteration": (_i32, [_vp, _P(Op), _i32, _u32, _vp]),
+    "adaptra_exec_wait": (_i32, [_vp, _P(IterStats)]),
+}
+
+_lib = None
+
+
+def declared_symbols():
+    """Every entry point include/adaptra.h declares (the binding binds all)."""
+    return list(_SIGS)
+
+
+def lib():
+    """Load libadaptra.so (in-tree).  Raises if it is missing: no fallback."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name, None)
+            if fn is None:
+                continue
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(rc):
+    if rc != OK:
+        msg = lib().adaptra_last_error()
+        raise AdaptraError(rc, msg.decode() if msg else "")
+    return rc

@@ -1,0 +1,88 @@
+"""Build libadaptra.so in-tree with nvcc for sm_100a (no JIT, no torch ext).
+
+Every .cu / .cpp under csrc/ is compiled with
+  nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -O3
+and linked into paper_2504_19232_b200/libadaptra.so (the file the tests and
+bench load).  Incremental: objects are rebuilt only when a source or header is
+newer.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import glob
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+BUILD = os.path.join(HERE, "_build")
+LIB = os.path.join(HERE, "libadaptra.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
+          "-I", CSRC]
+
+
+def _sources():
+    s = sorted(glob.glob(os.path.join(CSRC, "**", "*.cu"), recursive=True))
+    s += sorted(glob.glob(os.path.join(CSRC, "**", "*.cpp"), recursive=True))
+    return s
+
+
+def _headers():
+    h = glob.glob(os.path.join(CSRC, "**", "*.h"), recursive=True)
+    h += glob.glob(os.path.join(CSRC, "**", "*.cuh"), recursive=True)
+    h += glob.glob(os.path.join(ROOT, "include", "*.h"))
+    return h
+
+
+def _obj(src):
+    rel = os.path.relpath(src, CSRC).replace(os.sep, "_")
+    return os.path.join(BUILD, rel + ".o")
+
+
+def _compile(src, verbose=False):
+    obj = _obj(src)
+    cmd = [NVCC] + ARCH + COMMON + ["-c", src, "-o", obj]
+    if src.endswith(".cu"):
+        cmd += ["-Xptxas", "-v"] if verbose else []
+        cmd += ["--expt-relaxed-constexpr"]
+    else:
+        cmd += ["-x", "cu"] if False else []
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
+    return obj, r.stderr
+
+
+def build(force=False, verbose=False, jobs=None):
+    os.makedirs(BUILD, exist_ok=True)
+    srcs = _sources()
+    hdr_t = max((os.path.getmtime(h) for h in _headers()), default=0)
+    todo = []
+    for s in srcs:
+        o = _obj(s)
+        if force or not os.path.exists(o) or os.path.getmtime(o) < max(os.path.getmtime(s), hdr_t):
+            todo.append(s)
+    logs = []
+    with cf.ThreadPoolExecutor(max_workers=jobs or os.cpu_count() or 4) as ex:
+        for obj, log in ex.map(lambda s: _compile(s, verbose), todo):
+            logs.append(log)
+    objs = [_obj(s) for s in srcs]
+    if todo or not os.path.exists(LIB):
+        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart", "-lpthread"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    if verbose:
+        for lg in logs:
+            if lg.strip():
+                print(lg, file=sys.stderr)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(LIB)

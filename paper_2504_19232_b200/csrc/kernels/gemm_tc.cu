@@ -1,0 +1,351 @@
+// tcgen05 / TMEM / TMA bf16 GEMM for sm_100a (stage F, B = dX and W = dW
+// contractions, and the batched attention products).
+//
+// Persistent warp-specialised kernel, one CTA per SM:
+//   warp 0      TMA producer (one elected lane) -> smem ring of kStages stages
+//   warp 1      TMEM allocator + MMA issuer (one elected lane, tcgen05.mma
+//               kind::f16, 128 x BN x 16 per instruction, fp32 accumulate)
+//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> fused epilogue -> HBM
+// Two TMEM accumulators (2 x BN columns) let the epilogue of tile t overlap
+// the main loop of tile t+1.  Operands may be K-major or MN-major (SWIZZLE_128B
+// canonical layouts, selected by the instruction descriptor's major bits), so
+// dX = dY W and dW = dY^T X read the stored activations without transposes.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <string>
+
+#include "../../../include/adaptra.h"
+#include "../util.h"
+#include "common.cuh"
+#include "epilogue.cuh"
+
+namespace adaptra {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // 64 bf16 = 128 B = one SWIZZLE_128B row
+constexpr int kThreads = 192;
+
+template <int BN>
+struct TcCfg {
+  static constexpr int kStages = (BN == 256) ? 4 : 6;
+  static constexpr int kABytes = BM * BK * 2;  // 16 KB
+  static constexpr int kBBytes = BN * BK * 2;  // 32 / 16 KB
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kTmemCols = 2 * BN;     // two accumulators
+  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+struct TileInfo {
+  int m_blocks, n_blocks, Z;
+  int k_blocks;  // full K range in BK blocks
+};
+
+__device__ __forceinline__ void tile_coords(int t, const TileInfo& ti, int& mb, int& nb, int& z) {
+  mb = t % ti.m_blocks;
+  int r = t / ti.m_blocks;
+  nb = r % ti.n_blocks;
+  z = r / ti.n_blocks;
+}
+
+// K-block range of a tile (causal variants restrict it), and whether it is skipped.
+template <int BN>
+__device__ __forceinline__ bool tile_range(const adaptra_gemm_desc_t& g, const TileInfo& ti, int mb, int nb,
+                                           int& kb0, int& kb1) {
+  kb0 = 0;
+  kb1 = ti.k_blocks;
+  if (g.causal == ADAPTRA_CAUSAL_TILE) {
+    if (nb * BN > mb * BM + BM - 1) return false;
+  } else if (g.causal == ADAPTRA_CAUSAL_KEND) {
+    int kend = min(g.K, mb * BM + BM);
+    kb1 = (kend + BK - 1) / BK;
+  } else if (g.causal == ADAPTRA_CAUSAL_KSTART) {
+    kb0 = (mb * BM) / BK;
+  }
+  return kb1 > kb0;
+}
+
+template <int BN, int AMN, int BMN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const adaptra_gemm_desc_t g, const TileInfo ti, int vec_ok) {
+  using Cfg = TcCfg<BN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + Cfg::kStages * Cfg::kABytes;
+  uint64_t* full = (uint64_t*)(smem + Cfg::kStages * Cfg::kStageBytes);
+  uint64_t* empty = full + Cfg::kStages;
+  uint64_t* tfull = empty + Cfg::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int n_tiles = ti.m_blocks * ti.n_blocks * ti.Z;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < Cfg::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, Cfg::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        int mb, nb, z, kb0, kb1;
+        tile_coords(t, ti, mb, nb, z);
+        if (!tile_range<BN>(g, ti, mb, nb, kb0, kb1)) continue;
+        const int z1 = z / g.zdiv, z2 = z % g.zdiv;
+        const int a_r = (int)(z1 * g.a_row1 + z2 * g.a_row2), a_c = (int)(z1 * g.a_col1 + z2 * g.a_col2);
+        const int b_r = (int)(z1 * g.b_row1 + z2 * g.b_row2), b_c = (int)(z1 * g.b_col1 + z2 * g.b_col2);
+        const int m0 = mb * BM, n0 = nb * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
+          uint8_t* a_dst = sA + stage * Cfg::kABytes;
+          uint8_t* b_dst = sB + stage * Cfg::kBBytes;
+          const int k0 = kb * BK;
+          if (AMN == 0) {
+            tma_load_2d(a_dst, &tmA, &full[stage], a_c + k0, a_r + m0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_2d(a_dst + j * (BK * 128), &tmA, &full[stage], a_c + m0 + 64 * j, a_r + k0);
+          }
+          if (BMN == 0) {
+            tma_load_2d(b_dst, &tmB, &full[stage], b_c + k0, b_r + n0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_2d(b_dst + j * (BK * 128), &tmB, &full[stage], b_c + n0 + 64 * j, b_r + k0);
+          }
+          if (++stage == Cfg::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    // Instruction descriptor, kind::f16: D f32 (bit 4), A bf16 (bits 7-9 = 1),
+    // B bf16 (bits 10-12 = 1), A/B major (bits 15/16), N>>3 (17-22), M>>4 (24-28).
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)AMN << 15) | ((uint32_t)BMN << 16) |
+                           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      int mb, nb, z, kb0, kb1;
+      tile_coords(t, ti, mb, nb, z);
+      if (!tile_range<BN>(g, ti, mb, nb, kb0, kb1)) continue;
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a_addr = smem_u32(sA + stage * Cfg::kABytes);
+          const uint32_t b_addr = smem_u32(sB + stage * Cfg::kBBytes);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // K-major: advance 16 elements = 32 B inside the swizzled row; SBO = 8 rows x 128 B.
+            // MN-major: advance 16 K-rows = 2 KB; LBO = one 64-wide MN chunk (BK x 128 B), SBO = 8 rows.
+            uint64_t ad = AMN == 0 ? umma_desc_sw128(a_addr + k * 32, 16, 1024)
+                                   : umma_desc_sw128(a_addr + k * 2048, BK * 128, 1024);
+            uint64_t bd = BMN == 0 ? umma_desc_sw128(b_addr + k * 32, 16, 1024)
+                                   : umma_desc_sw128(b_addr + k * 2048, BK * 128, 1024);
+            tc_mma_f16(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          tc_commit(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == Cfg::kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (lane == 0) tc_commit(&tfull[acc]);
+      __syncwarp();
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ===================== epilogue (warps 2..5) =====================
+    const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      int mb, nb, z, kb0, kb1;
+      tile_coords(t, ti, mb, nb, z);
+      if (!tile_range<BN>(g, ti, mb, nb, kb0, kb1)) continue;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      EpiCtx e = make_epi<bf16>(g, z);
+      const int m = mb * BM + quad * 32 + lane;
+      const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tbase + c * 32, r);
+        tmem_ld_wait();
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        const int n0 = nb * BN + c * 32;
+        if (n0 >= e.N) break;
+        if (vec_ok && m < e.M && n0 + 32 <= e.N)
+          epi_row32_bf16_fast(e, m, n0, v);
+        else
+          epi_row<bf16, 32>(e, m, n0, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem_base, Cfg::kTmemCols);
+}
+
+// ------------------------------------------------------------------ host side
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_encodeTiled)p;
+  });
+  return fn;
+}
+
+// 2-D bf16 map over a [rows, cols] row-major matrix with leading dimension ld.
+static int make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_c,
+                    int box_r) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return set_error(ADAPTRA_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)box_c, (cuuint32_t)box_r};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(ADAPTRA_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return ADAPTRA_OK;
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int BN, int AMN, int BMN>
+static int launch_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
+  using Cfg = TcCfg<BN>;
+  CUtensorMap ma, mbm;
+  int rc;
+  if (AMN == 0)
+    rc = make_map(&ma, g.A, g.a_rows, g.a_cols, g.lda, BK, BM);
+  else
+    rc = make_map(&ma, g.A, g.a_rows, g.a_cols, g.lda, 64, BK);
+  if (rc) return rc;
+  if (BMN == 0)
+    rc = make_map(&mbm, g.B, g.b_rows, g.b_cols, g.ldb, BK, BN);
+  else
+    rc = make_map(&mbm, g.B, g.b_rows, g.b_cols, g.ldb, 64, BK);
+  if (rc) return rc;
+  TileInfo ti;
+  ti.m_blocks = (g.M + BM - 1) / BM;
+  ti.n_blocks = (g.N + BN - 1) / BN;
+  ti.Z = g.Z;
+  ti.k_blocks = (g.K + BK - 1) / BK;
+  const int n_tiles = ti.m_blocks * ti.n_blocks * ti.Z;
+  auto kern = gemm_tc_kernel<BN, AMN, BMN>;
+  static unsigned attr_mask = 0;  // per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(attr_mask & (1u << dev))) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+    attr_mask |= 1u << dev;
+  }
+  bool f32out = (g.epi == ADAPTRA_EPI_ACC_F32 || g.epi == ADAPTRA_EPI_STORE_F32);
+  int vec_ok = (g.ldc % (f32out ? 4 : 8) == 0) && ((uintptr_t)g.C % 16 == 0) &&
+               (!g.aux || (g.ldaux % 8 == 0 && (uintptr_t)g.aux % 16 == 0)) &&
+               (!g.R || (g.ldr % 8 == 0 && (uintptr_t)g.R % 16 == 0)) && ((uintptr_t)g.bias % 16 == 0) &&
+               (g.c_1 % 8 == 0) && (g.c_2 % 8 == 0) && (g.aux_1 % 8 == 0) && (g.aux_2 % 8 == 0);
+  int grid = n_tiles < num_sms() ? n_tiles : num_sms();
+  if (grid < 1) return ADAPTRA_OK;
+  kern<<<grid, kThreads, Cfg::kSmem, st>>>(ma, mbm, g, ti, vec_ok);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(ADAPTRA_ECUDA, std::string("gemm_tc launch: ") + cudaGetErrorString(e));
+  return ADAPTRA_OK;
+}
+
+int gemm_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
+  // BN = 256 for large unbatched N, else 128 (batched attention tiles must not
+  // cross a batch boundary: require tile-aligned extents when Z > 1).
+  if (g.Z > 1 && (g.M % BM || g.K % BK)) return set_error(ADAPTRA_EINVAL, "batched tc gemm needs M%128==0, K%64==0");
+  if ((g.lda * 2) % 16 || (g.ldb * 2) % 16) return set_error(ADAPTRA_EINVAL, "tc gemm needs 16B-aligned rows");
+  bool big = (g.Z == 1 && g.N >= 2048 && g.causal == ADAPTRA_CAUSAL_NONE);
+  if (g.Z > 1 && g.N % 128) return set_error(ADAPTRA_EINVAL, "batched tc gemm needs N%128==0");
+  const int key = g.a_mn * 2 + g.b_mn;
+  if (big) {
+    switch (key) {
+      case 0: return launch_tc<256, 0, 0>(g, st);
+      case 1: return launch_tc<256, 0, 1>(g, st);
+      case 2: return launch_tc<256, 1, 0>(g, st);
+      default: return launch_tc<256, 1, 1>(g, st);
+    }
+  }
+  switch (key) {
+    case 0: return launch_tc<128, 0, 0>(g, st);
+    case 1: return launch_tc<128, 0, 1>(g, st);
+    case 2: return launch_tc<128, 1, 0>(g, st);
+    default: return launch_tc<128, 1, 1>(g, st);
+  }
+}
+
+}  // namespace adaptra

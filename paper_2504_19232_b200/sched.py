@@ -1,0 +1,99 @@
+"""Python binding of the host scheduling core (csrc/sched/sched.cpp).
+
+Marshalling only; the planning and simulation run in libadaptra.so.
+Ops are returned as per-stage lists of (kind, mb, start, end) with kind in
+"F"/"B"/"W" and 1-based microbatches.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+from . import _lib as L
+
+KIND = {L.OP_F: "F", L.OP_B: "B", L.OP_W: "W"}
+KIND_ID = {"F": L.OP_F, "B": L.OP_B, "W": L.OP_W}
+
+
+def _arr(t, vals):
+    return (t * len(vals))(*vals)
+
+
+def plan_init(S, N, mem, mem_per_act):
+    x = (C.c_int32 * S)()
+    L.check(L.lib().adaptra_plan_init(S, N, mem, mem_per_act, x))
+    return list(x)
+
+
+def plan_adapt(S, N, tF, tB, c):
+    x = (C.c_int32 * S)()
+    L.check(L.lib().adaptra_plan_adapt(S, N, _arr(C.c_int64, tF), _arr(C.c_int64, tB),
+                                       _arr(C.c_int64, list(c) or [0]), x))
+    return list(x)
+
+
+def eq1_holds(tF, tB, c, x):
+    S = len(x)
+    ok = (C.c_uint8 * max(1, S - 1))()
+    L.check(L.lib().adaptra_eq1_holds(S, _arr(C.c_int64, tF), _arr(C.c_int64, tB),
+                                      _arr(C.c_int64, list(c) or [0]), _arr(C.c_int32, x), ok))
+    return [bool(v) for v in ok[:S - 1]]
+
+
+def _flags(mode, merge_w):
+    return (L.SEL_CAP if mode == "cap" else L.SEL_PAPER) | (L.MERGE_W if merge_w else 0)
+
+
+def schedule(S, N, tF, tB, tW, c, x, delta, mode="paper", merge_w=False):
+    """Alg. 4 Schedule.  Returns (X, T, steps), X[i] = [(kind, mb, start, end)]."""
+    per = 3 * N
+    ops = (L.Op * (S * per))()
+    n = (C.c_int32 * S)()
+    T = C.c_int64()
+    steps = C.c_int64()
+    L.check(L.lib().adaptra_schedule(S, N, _arr(C.c_int64, tF), _arr(C.c_int64, tB), _arr(C.c_int64, tW),
+                                      _arr(C.c_int64, list(c) or [0]), _arr(C.c_int32, x), delta,
+                                      _flags(mode, merge_w), ops, n, C.byref(T), C.byref(steps)))
+    X = [[(KIND[ops[i * per + q].kind], ops[i * per + q].mb, ops[i * per + q].start, ops[i * per + q].end)
+          for q in range(n[i])] for i in range(S)]
+    return X, T.value, steps.value
+
+
+def _pack(S, N, order):
+    per = 3 * N
+    arr = (L.Op * (S * per))()
+    n = (C.c_int32 * S)()
+    for i in range(S):
+        n[i] = len(order[i])
+        for q, o in enumerate(order[i]):
+            arr[i * per + q].kind = KIND_ID[o[0]]
+            arr[i * per + q].mb = o[1]
+            if len(o) >= 4:
+                arr[i * per + q].start = o[2]
+                arr[i * per + q].end = o[3]
+    return arr, n
+
+
+def replay(S, N, tF, tB, tW, c, order, merge_w=False):
+    per = 3 * N
+    arr, n = _pack(S, N, order)
+    out = (L.Op * (S * per))()
+    T = C.c_int64()
+    L.check(L.lib().adaptra_replay(S, N, _arr(C.c_int64, tF), _arr(C.c_int64, tB), _arr(C.c_int64, tW),
+                                   _arr(C.c_int64, list(c) or [0]), arr, n, _flags("paper", merge_w), out,
+                                   C.byref(T)))
+    X = [[(KIND[out[i * per + q].kind], out[i * per + q].mb, out[i * per + q].start, out[i * per + q].end)
+          for q in range(n[i])] for i in range(S)]
+    return X, T.value
+
+
+def validate(S, N, tF, tB, tW, c, X, merge_w=False):
+    arr, n = _pack(S, N, X)
+    v = C.c_int32()
+    L.check(L.lib().adaptra_validate(S, N, _arr(C.c_int64, tF), _arr(C.c_int64, tB), _arr(C.c_int64, tW),
+                                     _arr(C.c_int64, list(c) or [0]), arr, n, _flags("paper", merge_w),
+                                     C.byref(v)))
+    return v.value
+
+
+def order_of(X):
+    return [[(o[0], o[1]) for o in ops] for ops in X]
