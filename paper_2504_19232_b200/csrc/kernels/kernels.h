@@ -1,0 +1,31 @@
+// Launch wrappers of the stage kernels (csrc/kernels/*.cu).  Host-callable.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "../../../include/adaptra.h"
+
+namespace adaptra {
+typedef __nv_bfloat16 bf16;
+
+int gemm_tc(const adaptra_gemm_desc_t& g, cudaStream_t st);
+int gemm_simt(const adaptra_gemm_desc_t& g, cudaStream_t st);
+
+template <typename T>
+int ln_fwd(const T* x, const float* g, const float* b, T* h, float* mean, float* rstd, int R, int d, cudaStream_t st);
+template <typename T>
+int ln_bwd(const T* dh, const T* x, const float* mean, const float* rstd, const float* g, const T* dres, T* dx, int R,
+           int d, cudaStream_t st);
+template <typename T>
+int ln_param_grad(const T* dh, const T* x, const float* mean, const float* rstd, float* dg, float* db, int R, int d,
+                  cudaStream_t st);
+template <typename T>
+int col_sum(const T* y, float* out, int R, int N, cudaStream_t st);
+template <typename T>
+int softmax_causal(const float* S, T* P, int Z, int Tn, cudaStream_t st);
+template <typename T>
+int attn_rowdot(const T* dO, const T* O, float* D, int b, int H, int Tn, int dh, int ld, cudaStream_t st);
+template <typename T>
+int mse_loss(const T* y, const float* tgt, T* dy, float* loss_acc, long n, int n_mb, cudaStream_t st);
+int copy_async(void* dst, const void* src, long bytes, cudaStream_t st);
+}  // namespace adaptra
