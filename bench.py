@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""Benchmark of the zero-bubble pipeline-parallel training step (Adaptra,
+arXiv 2504.19232) on B200: tokens/s and bubble rate under the injected
+straggler trace, for the adaptive schedule and the fixed 1F1B / ZB arms on the
+same kernels.  Prints ONE JSON line (rank 0).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun (one process per GPU, stages spread contiguously).
+A "step" is one pipelined training iteration (all S stages x N microbatches,
+F/B/W, transfers, schedule generation) on synthetic GPT-2-shaped data.
+Workload: config C1 of BASELINE.json -- GPT-style 1.3B-shaped
+stack (24 pre-LN blocks, d=2048, 16 heads, d_ff=8192), S=4 stages, N=16
+microbatches of one 2048-token sequence, bf16 (8 GPUs: S=8 stages, N=32).
+The straggler trace is the paper's appendix table compressed to
+one event per step and scaled to the measured op time (R22, R27).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--layers", type=int, default=24)
+    ap.add_argument("--d", type=int, default=2048)
+    ap.add_argument("--heads", type=int, default=16)
+    ap.add_argument("--T", type=int, default=2048)
+    ap.add_argument("--S", type=int, default=0, help="stages (default 4, or 8 on 8 GPUs)")
+    ap.add_argument("--N", type=int, default=0, help="microbatches (default 16, or 32 with S=8)")
+    ap.add_argument("--arms", default="adaptive,zb,1f1b")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--link-mode", default="direct", choices=["direct", "p2p"])
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- clocks
+class Clocks:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.samples = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._th = threading.Thread(target=self._run, daemon=True)
+        self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._th.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if len(s) > 2 + k and
+                          s[2 + k].lower().startswith("active")})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- helpers
+def trace_links(links, S):
+    """R27: the paper's trace names links 0..6 of an 8-stage pipeline; for S < 8
+    link a maps to floor(a (S-1) / 7)."""
+    if S == 8:
+        return list(links)
+    return sorted({(a * (S - 1)) // 7 for a in links})
+
+
+def trace_c(event, S, t_ref_ns, host_c_ns):
+    """Per-link latency (ns) of one trace event.  R22: latency_ms is in units of
+    the paper's simulated op time t = 10 ms, i.e. c = (lat/10) * t_ref."""
+    c = [0] * (S - 1)
+    down = []
+    for a in trace_links(event["links"], S):
+        if event["latency_ms"] == float("inf"):
+            down.append(a)
+            c[a] = host_c_ns
+        else:
+            c[a] = int(event["latency_ms"] / 10.0 * t_ref_ns)
+    return c, down
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_19232_b200  # noqa: F401  (sets CUDA_DEVICE_MAX_CONNECTIONS)
+    from paper_2504_19232_b200 import _lib as L
+    from paper_2504_19232_b200.pipeline import Arm, ModelCfg, Pipeline
+    import synthetic as sy
+
+    torch.cuda.set_device(local_rank)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        group = dist.new_group(backend="gloo")
+    S = args.S or (8 if world >= 8 else 4)
+    N = args.N or (32 if S == 8 else 16)
+    model = ModelCfg(block="gpt", n_layers=args.layers, d=args.d, d_ff=4 * args.d, n_heads=args.heads,
+                     b=1, T=args.T, dtype=L.BF16)
+    mode = L.LINK_DIRECT if args.link_mode == "direct" else L.LINK_P2P
+    pipe = Pipeline(model, S, N, rank=rank, world=world, device=local_rank, group=group, link_mode=mode,
+                    host_links=True, seed=0)
+
+    def gather(obj):
+        if world == 1:
+            return [obj]
+        out = [None] * world
+        dist.all_gather_object(out, obj, group=group)
+        return out
+
+    # -------- profile t^F, t^B, t^W per stage (ZB order at c = 0), quantised to 1 us
+    zero = [0] * (S - 1)
+    prof_arm = Arm("zb", S, N, [1000] * S, [1000] * S, [1000] * S)
+    for _ in range(2):
+        r = pipe.run(prof_arm.orders)
+    loc = {i: [st["op_ns"][k] // max(1, st["op_cnt"][k]) for k in range(3)] for i, st in r.stats.items()}
+    allp = {}
+    for d in gather(loc):
+        allp.update(d)
+    tF = [max(1, allp[i][0] // 1000) * 1000 for i in range(S)]
+    tB = [max(1, allp[i][1] // 1000) * 1000 for i in range(S)]
+    tW = [max(1, allp[i][2] // 1000) * 1000 for i in range(S)]
+    t_ref = sum(tF) // S
+    # delegated-path latency used for planning when a link is down: measured
+    host_c = measure_host_path(pipe, torch) if rank == 0 else 0
+    host_c = max(gather(host_c))
+    # Alg. 1 memory input: F->B stash capacity of stage 0 (M / M^F, R12)
+    cap_fb = {i: st.n_slots_fb for i, st in pipe.stages.items()}
+    caps = {}
+    for d in gather(cap_fb):
+        caps.update(d)
+    x_cap = [caps[i] for i in range(S)]
+    from paper_2504_19232_b200 import sched as cs
+    x_init = cs.plan_init(S, N, x_cap[0], 1)
+    x_init = [min(v, c) for v, c in zip(x_init, x_cap)]
+    for i in range(S - 2, -1, -1):
+        x_init[i] = max(x_init[i], x_init[i + 1])
+
+    events = sy.PAPER_TRACE
+    arms = [a for a in args.arms.split(",") if a]
+    results = {}
+    lib = L.lib()
+    timer = torch.cuda.Stream(device=local_rank)
+
+    def run_arm(name, with_trace, steps, warmup, e2e=False, prof=False):
+        arm = Arm(name, S, N, tF, tB, tW, x_init=x_init if name == "adaptive" else None, x_cap=x_cap)
+        host_in = None
+        if e2e and 0 in pipe.stages:
+            host_in = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in pipe.inputs]
+            for h, t in zip(host_in, pipe.inputs):
+                h.copy_(t)
+        busy_tot, span_tot, n_it, losses = 0, 0, 0, []
+        dev_busy = 0
+
+        def one_step(k):
+            ev = events[k % len(events)] if with_trace else None
+            c, down = trace_c(ev, S, t_ref, host_c) if ev else (list(zero), [])
+            for l in range(S - 1):
+                want = L.LINK_DOWN if l in down else c[l]
+                if pipe.latency[l] != want:
+                    pipe.set_latency(l, want)
+            orders = arm.plan(c)
+            if host_in is not None:
+                for h, t in zip(host_in, pipe.inputs):
+                    t.copy_(h, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+            res = pipe.run(orders, merge_w=arm.merge_w, want_times=True)
+            return res
+
+        for k in range(warmup):
+            one_step(k)
+        if world > 1:
+            dist.barrier(group=group)
+        torch.cuda.synchronize()
+        if prof:
+            lib.adaptra_prof_enable(1)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(timer)
+        for k in range(steps):
+            res = one_step(warmup + k)
+            if res.loss is not None:
+                losses.append(res.loss)   # D2H read of the step's result
+            span = max(st["last_end_ns"] for st in res.stats.values())
+            busy = sum(st["busy_ns"] for st in res.stats.values())
+            # device-level busy: union of this rank's op intervals
+            iv = sorted(t for st in res.stats.values() for t in st["op_times"])
+            u, cur_s, cur_e = 0, None, None
+            for s0, e0_ in iv:
+                if cur_e is None or s0 > cur_e:
+                    if cur_e is not None:
+                        u += cur_e - cur_s
+                    cur_s, cur_e = s0, e0_
+                else:
+                    cur_e = max(cur_e, e0_)
+            if cur_e is not None:
+                u += cur_e - cur_s
+            busy_tot += busy
+            dev_busy += u
+            span_tot += span
+            n_it += 1
+        e1.record(timer)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if prof:
+            lib.adaptra_prof_enable(0)
+        g = gather({"ms": ms, "busy": busy_tot, "span": span_tot, "dev_busy": dev_busy,
+                    "links": {str(k): v for k, v in pipe.link_stats().items()}})
+        ms_max = max(x["ms"] for x in g)
+        busy = sum(x["busy"] for x in g)
+        dbusy = sum(x["dev_busy"] for x in g)
+        span = max(x["span"] for x in g)
+        toks = steps * N * model.tokens_per_mb
+        out = {"tokens_per_s": toks / (ms_max / 1e3), "ms_per_step": ms_max / steps,
+               # R15: utilisation bubble 1 - sum busy / (S T) with T the step time
+               "bubble": 1.0 - busy / (S * ms_max * 1e6),
+               "device_bubble": 1.0 - dbusy / (world * ms_max * 1e6),
+               "replans": arm.replans, "x_final": arm.x}
+        if losses:
+            out["loss_last"] = losses[-1]
+        return out
+
+    # -------- timed arms: headline = adaptive under the trace
+    for name in arms:
+        results[(name, "trace")] = run_arm(name, True, args.steps, args.warmup, prof=(name == "adaptive"))
+        if name == "adaptive":
+            n, ms, fl, by = (__import__("ctypes").c_int64(), __import__("ctypes").c_double(),
+                             __import__("ctypes").c_double(), __import__("ctypes").c_double())
+            lib.adaptra_prof_collect(0, n, ms, fl, by)
+            gem = gather((n.value, ms.value, fl.value, by.value))
+        results[(name, "nominal")] = run_arm(name, False, max(3, args.steps // 2), 1)
+    e2e = None
+    if not args.no_e2e and "adaptive" in arms:
+        e2e_r = run_arm("adaptive", True, max(3, args.steps // 2), 1, e2e=True)
+        bi = N * model.tokens_per_mb * model.d * 2
+        e2e = {"value": e2e_r["tokens_per_s"], "unit": "tokens/s", "h2d_bytes_per_step": bi,
+               "d2h_bytes_per_step": 4}
+
+    with Clocks(local_rank) as clk:
+        clocked = run_arm("adaptive", True, max(3, args.steps // 2), 1)
+    clocks = clk.summary()
+
+    if rank == 0:
+        head = results[("adaptive", "trace")] if "adaptive" in arms else results[(arms[0], "trace")]
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+            os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+        peak = peaks.get("bf16_tflops_sustained", 1400.0)
+        n_l = sum(x[0] for x in gem)
+        ms_l = sum(x[1] for x in gem)
+        fl_l = sum(x[2] for x in gem)
+        avg_ms = ms_l / max(1, n_l)
+        achieved = (fl_l / max(1, n_l)) / (avg_ms / 1e3) / 1e12 if n_l else None
+        line = {
+            "metric": "tokens/sec and bubble rate at 8 stages under injected straggler trace",
+            "value": round(head["tokens_per_s"], 1), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(head["ms_per_step"], 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded N(0,1) inputs/targets, GPT-2 init weights)",
+            "bubble_rate": round(head["bubble"], 4), "device_bubble_rate": round(head["device_bubble"], 4),
+            "config": {"workload": f"C1: GPT-style {args.layers}x(d={args.d},h={args.heads},ff={4 * args.d}) "
+                                   f"S={S} N={N} seq={args.T} bf16, paper trace compressed 1 event/step",
+                       "stages": S, "microbatches": N, "tokens_per_step": N * model.tokens_per_mb,
+                       "stage_map": [i * world // S for i in range(S)],
+                       "l2": "inputs > L2 (per-step working set >> 126 MB)",
+                       "t_ref_us": t_ref / 1e3, "host_path_c_us": host_c / 1e3},
+            "arms": {f"{a}/{w}": {k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()}
+                     for (a, w), r in results.items()},
+            "roofline": {"bound": "tensor", "achieved": round(achieved, 1) if achieved else None,
+                         "peak": peak, "unit": "TFLOP/s",
+                         "frac": round(achieved / peak, 4) if achieved else None, "traffic": None,
+                         "kernel": "gemm_tc_kernel (tcgen05)", "launches": n_l,
+                         "avg_launch_us": round(avg_ms * 1e3, 2),
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"},
+            "clocks": clocks,
+            "e2e": e2e,
+            "gpu_launches": None,
+        }
+        if not args.no_cpu:
+            line["cpu_baseline"] = cpu_baseline(model, S, N)
+        print(json.dumps(line), flush=True)
+    pipe.close()
+    if world > 1:
+        dist.barrier(group=group)
+        dist.destroy_process_group()
+
+
+def measure_host_path(pipe, torch):
+    """One message's D2H + H2D time through pinned memory (the delegated path)."""
+    n = pipe.msg_bytes
+    a = torch.empty(n, dtype=torch.uint8, device=f"cuda:{pipe.dev}")
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    for _ in range(2):
+        h.copy_(a, non_blocking=True)
+        a.copy_(h, non_blocking=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(5):
+        h.copy_(a, non_blocking=True)
+        torch.cuda.synchronize()
+        a.copy_(h, non_blocking=True)
+        torch.cuda.synchronize()
+    return int((time.perf_counter() - t0) / 5 * 1e9)
+
+
+def cpu_baseline(model, S, N, budget_s=15.0):
+    """The oracle as it stands (float64 numpy) on the host cores: a bounded sample
+    = F+B+W of one GPT block on one microbatch (scaled to tokens/s of the whole
+    n_layers-deep model), plus Schedule() of the oracle."""
+    import numpy as np
+    from oracle import numerics as nu
+    import synthetic as sy
+    d, T = model.d, model.T
+    p = sy.gpt_params(0, 1, 1, d, 4 * d, perturb=False)[0][0]
+    x = sy.microbatches(1, 1, 1, T, d)[0]
+    t0 = time.perf_counter()
+    y, cache = nu.block_F("gpt", p, x.astype(np.float64), model.n_heads)
+    dx, gc = nu.block_B("gpt", {k: v.astype(np.float64) for k, v in p.items()}, cache, np.ones_like(y) / y.size,
+                        model.n_heads)
+    nu.block_W("gpt", cache, gc)
+    dt = time.perf_counter() - t0
+    per_token_s = dt * model.n_layers / T
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        cores = os.cpu_count()
+    return {"value": round(1.0 / per_token_s, 3), "unit": "tokens/s", "cores": cores, "kind": "oracle",
+            "sample": f"oracle F+B+W of 1 of {model.n_layers} GPT blocks on 1 microbatch "
+                      f"(T={T}, d={d}), float64 numpy, {dt:.1f}s; tokens/s scaled to the full stack"}
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: the CPU oracle as it stands, on this box's host cores,
+    same metric/unit; each step a bounded sample of the workload."""
+    if rank != 0:
+        return 0
+    import numpy as np
+    from oracle import numerics as nu
+    from oracle import sched as osc
+    import synthetic as sy
+    S = args.S or (8 if world >= 8 else 4)
+    N = args.N or (32 if S == 8 else 16)
+    d, T, H, nl = args.d, args.T, args.heads, args.layers
+    p = {k: v.astype(np.float64) for k, v in sy.gpt_params(0, 1, 1, d, 4 * d, perturb=False)[0][0].items()}
+    x = sy.microbatches(1, 1, 1, T, d)[0].astype(np.float64)
+    times = []
+    for k in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        y, cache = nu.block_F("gpt", p, x, H)
+        dx, gc = nu.block_B("gpt", p, cache, np.ones_like(y) / y.size, H)
+        nu.block_W("gpt", cache, gc)
+        t = [10] * S
+        osc.schedule(S, N, t, t, t, [0] * (S - 1), osc.get_adapted_warmup_fwds(S, N, t, t, [0] * (S - 1)), 1)
+        if k >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    per_step = sum(times) / len(times)
+    value = T / (per_step * nl)
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        cores = os.cpu_count()
+    sample = f"per step: oracle F+B+W of 1 of {nl} GPT blocks on 1 microbatch (T={T}, d={d}) + Schedule(); scaled"
+    line = {"metric": "tokens/sec and bubble rate at 8 stages under injected straggler trace", "value": value,
+            "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"C1 (oracle sample) S={S} N={N} seq={T} d={d}"},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main() or 0)

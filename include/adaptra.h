@@ -14,10 +14,12 @@
  *    oracle on the same inputs.
  *  - Memory ownership: the caller allocates every output array (host arrays
  *    for planning calls; device buffers for stage calls).  Weights, gradients,
- *    stash arenas, workspaces and pinned host rings are caller-owned (the
- *    Python binding allocates them with torch); the library only borrows raw
- *    pointers.  Only opaque handles (stage, link) are library-allocated and
- *    are freed by the matching *_destroy / *_close call.
+ *    stash arenas and workspaces are caller-owned (the Python binding
+ *    allocates them with torch); the library only borrows raw pointers.
+ *    Library-allocated: opaque handles (stage, inbox, outbox, exec) and the
+ *    inbox mailboxes/flags/host rings (whole cudaMalloc / shm allocations so
+ *    they can be exported across processes); all are freed by the matching
+ *    *_destroy / *_close call.
  *  - Device work is enqueued on caller-supplied cudaStream_t (passed as void*).
  *    Asynchronous CUDA faults surface as ADAPTRA_ECUDA from a later call.
  *  - Planning calls are pure and reentrant.  A stage or link handle must be
@@ -160,6 +162,14 @@ typedef struct adaptra_gemm_desc {
 
 int adaptra_gemm(const adaptra_gemm_desc_t* g, void* stream);
 
+/* Live kernel timing (bench roofline): when enabled, every tcgen05 GEMM launch
+ * (kind 0) is bracketed by CUDA events on its own stream.  collect() waits for
+ * the recorded launches of `kind`, returns their count, summed duration (ms),
+ * algorithmic FLOPs (2MNK per batch, causal products counted at 1/2, R28) and
+ * operand/result bytes, and forgets them. */
+int adaptra_prof_enable(int32_t on);
+int adaptra_prof_collect(int32_t kind, int64_t* n_launches, double* sum_ms, double* flops, double* bytes);
+
 /* ================================================================ stage compute
  * One pipeline stage = n_layers identical blocks (R24/R19: uniform stages).
  * block MLP: y = x + gelu(x W1^T + b1) W2^T + b2                (config C0)
@@ -175,9 +185,13 @@ int adaptra_gemm(const adaptra_gemm_desc_t* g, void* stream);
  *        MLP: b1[dff], b2[d]
  *  gwts, gvecs (fp32): gradients, same layouts as wts / vecs; W ops accumulate
  *        into them (deferred weight gradients).
- *  stash (bytes = n_slots * adaptra_stage_slot_bytes): saved activations of
- *        one in-flight microbatch per slot; F fills slot s, B reads it and adds
- *        output gradients, W consumes and frees it.
+ *  stash (bytes = n_slots * adaptra_stage_slot_bytes): what W needs of one
+ *        in-flight microbatch (GEMM inputs and output gradients); taken at F,
+ *        freed at W (slot index chosen by the caller).
+ *  stash_fb (bytes = n_slots_fb * adaptra_stage_slot_fb_bytes): what only B
+ *        needs (qkv, attention probabilities, FC1 pre-activation); taken at F
+ *        and freed at the end of B by the stage itself, in issue order
+ *        ("B ... immediately free activation memory").
  *  work  (bytes = adaptra_stage_work_bytes): per-stage scratch (attention
  *        scores), reused by every op issued on the stage's stream.
  */
@@ -190,18 +204,21 @@ typedef struct adaptra_stage_desc {
   int32_t b, T;            /* microbatch = b sequences of T tokens            */
   int32_t is_first, is_last;
   int32_t n_microbatches;  /* N: loss is L = (1/N) sum_j L_j (R19)           */
-  int32_t n_slots;
+  int32_t n_slots;          /* F->W slots (caller-indexed)                    */
+  int32_t n_slots_fb;       /* F->B slots (stage-managed free list)           */
   void* wts;
   float* vecs;
   float* gwts;
   float* gvecs;
   void* stash;
+  void* stash_fb;
   void* work;
 } adaptra_stage_desc_t;
 
 typedef struct adaptra_stage* adaptra_stage_t;
 
 int64_t adaptra_stage_slot_bytes(const adaptra_stage_desc_t* d);
+int64_t adaptra_stage_slot_fb_bytes(const adaptra_stage_desc_t* d);
 int64_t adaptra_stage_work_bytes(const adaptra_stage_desc_t* d);
 int64_t adaptra_stage_wts_elems(const adaptra_stage_desc_t* d);
 int64_t adaptra_stage_vecs_elems(const adaptra_stage_desc_t* d);
@@ -225,108 +242,120 @@ int adaptra_stage_W(adaptra_stage_t s, int32_t slot, void* stream);
 int adaptra_stage_zero_grads(adaptra_stage_t s, void* stream);
 
 /* ================================================================ transport
- * A link carries stage i's F output to stage i+1 (dir FWD) and stage i+1's B
- * output to stage i (dir BWD), one message of `bytes` per microbatch.
- * Receiver-side mailboxes: one slot per microbatch per direction.  Readiness
- * is a per-(dir, mb) 32-bit flag equal to the iteration epoch.
+ * One direction of one link (stage i -> i+1 for forward activations, i+1 -> i
+ * for input gradients) is an inbox on the receiving stage and an
+ * outbox on the sending stage.  One message of `bytes` per microbatch.
  *
- * Modes:
- *  ADAPTRA_LINK_DIRECT  producer epilogue writes straight into the receiver
- *                       mailbox (same device or NVLink peer pointer); send
- *                       only posts the flag.
- *  ADAPTRA_LINK_P2P     send runs the P2P copy kernel (src -> peer mailbox
- *                       over NVLink), then posts the flag.
- *  ADAPTRA_LINK_HOST    delegated path: D2H copy engine into a
- *                       pinned host slot on a side stream, then H2D into the
- *                       receiver mailbox, then the flag.  Also the path taken
- *                       while the link is down (latency ADAPTRA_LINK_DOWN).
- * Latency injection: adaptra_set_link_latency(l, c) delays the flag of every
- * later message by c ns after the producing op completes (a pure per-message
- * latency, R16), applied by a host gate thread with no SM use.
+ * Inbox (library-allocated so it can be exported over CUDA IPC):
+ *   mailbox  [n_mb * bytes] device memory of the receiver, one slot per mb;
+ *   flags    uint32[n_mb] device memory; message (mb) of iteration `epoch` is
+ *            ready when flags[mb] >= epoch (epochs start at 1, increase);
+ *   host ring (optional, POSIX shm `host_name`, pinned with cudaHostRegister):
+ *            [n_mb * bytes] data + uint32[n_mb] host flags: the delegated path
+ *            (P:2270-2350).  A process-wide delegate thread copies arrived host
+ *            slots into the mailbox (H2D, copy engine) and posts the device flag.
+ * Outbox (sender side):
+ *   dst(mb)  where the producing kernel writes: the peer mailbox slot itself
+ *            (DIRECT: the last GEMM epilogue stores over NVLink, no extra copy)
+ *            or a local staging slot (P2P: a copy kernel moves it afterwards;
+ *            HOST: D2H into the host ring).
+ *   send     enqueues the transfer on the outbox's own stream after the
+ *            producing op (never on the compute stream) and posts the flag.
+ * Latency injection (R16): with latency c > 0 the flag of each message is
+ * posted c ns after its data is in place, by a process-wide gate thread that
+ * polls the completion event (no SM use, messages pipeline).  Latency
+ * ADAPTRA_LINK_DOWN marks the GPU path failed: the outbox switches to the
+ * HOST path (the inbox must be told with adaptra_inbox_set_host); the
+ * delegated path's own latency then applies.
  */
 #define ADAPTRA_LINK_DIRECT 0
 #define ADAPTRA_LINK_P2P 1
 #define ADAPTRA_LINK_HOST 2
-#define ADAPTRA_DIR_FWD 0
-#define ADAPTRA_DIR_BWD 1
 #define ADAPTRA_LINK_DOWN INT64_MAX
+#define ADAPTRA_IPC_BYTES 128
 
-typedef struct adaptra_link_desc {
-  int32_t mode;
-  int32_t n_mb;            /* mailbox slots per direction                     */
-  int64_t bytes;           /* message size                                    */
-  int32_t dev_up, dev_down;/* CUDA device of stage i and of stage i+1         */
-  /* Receiver mailboxes, [n_mb * bytes] each, on the receiving device (caller
-   * owned; may be IPC-mapped peer pointers).  fwd_mbox lives on dev_down,
-   * bwd_mbox on dev_up. */
-  void* fwd_mbox;
-  void* bwd_mbox;
-  /* Flags: uint32[n_mb] each, device memory of the receiver (fwd_flags on
-   * dev_down, bwd_flags on dev_up), zero-initialised by the caller. */
-  uint32_t* fwd_flags;
-  uint32_t* bwd_flags;
-  /* Delegated path: pinned host staging [n_mb * bytes] per direction (may be NULL
-   * unless mode == HOST or the link can go down). */
-  void* host_fwd;
-  void* host_bwd;
-} adaptra_link_desc_t;
+typedef struct adaptra_inbox* adaptra_inbox_t;
+typedef struct adaptra_outbox* adaptra_outbox_t;
 
-typedef struct adaptra_link* adaptra_link_t;
+/* host_name: NULL = no delegated path for this inbox. */
+int adaptra_inbox_create(int32_t dev, int32_t n_mb, int64_t bytes, const char* host_name, adaptra_inbox_t* out);
+int adaptra_inbox_destroy(adaptra_inbox_t ib);
+/* 128 bytes: CUDA IPC handles of the mailbox and the flags. */
+int adaptra_inbox_export(adaptra_inbox_t ib, uint8_t* handle_out);
+void* adaptra_inbox_slot(adaptra_inbox_t ib, int32_t mb);
+/* Enqueue on `consumer` a GPU-side wait (stream memory op, no host blocking,
+ * no SM) until message mb of iteration epoch is in the mailbox; the slot
+ * address is returned in slot_out. */
+int adaptra_recv(adaptra_inbox_t ib, int32_t mb, uint32_t epoch, void* consumer, void** slot_out);
+/* Abort path: set every flag to 0xFFFFFFFF so that all waiters proceed
+ * (after a failed or timed-out iteration); adaptra_inbox_reset clears flags
+ * (and host flags) back to 0 before epochs restart at 1. */
+int adaptra_inbox_poison(adaptra_inbox_t ib);
+int adaptra_inbox_reset(adaptra_inbox_t ib);
+/* Receiver side of the delegated path on (1) / off (0). */
+int adaptra_inbox_set_host(adaptra_inbox_t ib, int32_t on);
 
-int adaptra_link_open(const adaptra_link_desc_t* d, adaptra_link_t* out);
-int adaptra_link_close(adaptra_link_t l);
-/* Injected latency in ns (>= 0), or ADAPTRA_LINK_DOWN: the link's GPU path has
- * failed and traffic moves to the delegated host path. */
-int adaptra_set_link_latency(adaptra_link_t l, int64_t latency_ns);
-/* Send message (dir, mb) of iteration `epoch`: src is the producer's buffer
- * (NULL in DIRECT mode: data already in the mailbox).  `produced` is a
- * cudaEvent_t recorded after the producing op on the producer stream; the
- * send is enqueued on the link's own streams, never on the compute stream. */
-int adaptra_send(adaptra_link_t l, int32_t dir, int32_t mb, const void* src, void* produced, uint32_t epoch);
-/* Make `consumer` stream wait (on the GPU, no host blocking) until message
- * (dir, mb) of iteration `epoch` is in the mailbox; returns its address. */
-int adaptra_recv(adaptra_link_t l, int32_t dir, int32_t mb, void* consumer, uint32_t epoch, void** slot_out);
-/* Achieved per-message latency statistics since open (ns). */
-int adaptra_link_stats(adaptra_link_t l, int64_t* n_msgs, int64_t* sum_latency_ns, int64_t* max_latency_ns);
+/* Same-process outbox (stages co-located in one process; devices may differ). */
+int adaptra_outbox_open_local(int32_t dev, adaptra_inbox_t peer, int32_t mode, adaptra_outbox_t* out);
+/* Cross-process outbox from an exported inbox handle (IPC over NVLink). */
+int adaptra_outbox_open_ipc(int32_t dev, const uint8_t* handle, int32_t n_mb, int64_t bytes, const char* host_name,
+                            int32_t mode, adaptra_outbox_t* out);
+int adaptra_outbox_close(adaptra_outbox_t ob);
+void* adaptra_outbox_dst(adaptra_outbox_t ob, int32_t mb);
+/* Injected latency in ns (>= 0), or ADAPTRA_LINK_DOWN (delegated host path). */
+int adaptra_set_link_latency(adaptra_outbox_t ob, int64_t latency_ns);
+/* Send message mb of iteration epoch once the work already enqueued on
+ * `producer` (the producing op) has completed. */
+int adaptra_send(adaptra_outbox_t ob, int32_t mb, void* producer, uint32_t epoch);
+/* Gate statistics since open: messages, sum/max of (flag post - data ready) in ns. */
+int adaptra_link_stats(adaptra_outbox_t ob, int64_t* n_msgs, int64_t* sum_delay_ns, int64_t* max_delay_ns);
 
 /* ================================================================ executor
- * Interprets one iteration of a stage's op list (from adaptra_schedule) on the
- * stage's compute stream: per op, wait for its input message on the GPU
- * (never blocking the host, so no HOL stall: P:1801-1828), launch the F/B/W
- * kernels, record CUDA events, and hand the output to the link.
+ * Interprets one iteration of a stage's op order (from adaptra_schedule) on
+ * the stage's compute stream from a dedicated host thread: per op, a GPU-side
+ * wait for its input message (so a late message never blocks the host from
+ * launching later work: no HOL stall), the F/B/W kernels, CUDA
+ * events around the op, and the send of its output.  Stash slots are taken
+ * at F and released at W (in op order, on the one compute stream).
  */
 typedef struct adaptra_exec_desc {
   adaptra_stage_t stage;
   int32_t stage_index, n_stages, n_microbatches;
-  adaptra_link_t link_up;     /* link to stage i-1 (NULL on the first stage)  */
-  adaptra_link_t link_down;   /* link to stage i+1 (NULL on the last stage)   */
+  adaptra_inbox_t in_fwd;     /* activations from stage i-1 (NULL on stage 0)   */
+  adaptra_inbox_t in_bwd;     /* gradients from stage i+1 (NULL on stage S-1)   */
+  adaptra_outbox_t out_fwd;   /* to stage i+1 (NULL on stage S-1)               */
+  adaptra_outbox_t out_bwd;   /* to stage i-1 (NULL on stage 0)                 */
   void* compute_stream;
-  /* first stage: microbatch inputs, n_mb pointers [b*T,d] dtype (device) */
-  const void* const* inputs;
-  /* last stage: targets, n_mb pointers [b*T,d] fp32 (device) */
-  const float* const* targets;
-  float* loss_acc;            /* device fp32 scalar                            */
-  uint32_t merge_w;           /* 1F1B: run W right after B                     */
+  const void* const* inputs;   /* stage 0: n_mb device pointers [b*T, d]        */
+  const float* const* targets; /* stage S-1: n_mb device pointers [b*T, d] fp32 */
+  float* loss_acc;             /* stage S-1: device fp32 scalar                 */
 } adaptra_exec_desc_t;
 
 typedef struct adaptra_exec* adaptra_exec_t;
 
 typedef struct adaptra_iter_stats {
   int64_t n_ops;
-  int64_t busy_ns;           /* sum of op durations on the compute stream (CUDA events) */
-  int64_t first_start_ns;    /* relative to the iteration's time base         */
+  int64_t busy_ns;          /* sum of op durations (CUDA events, compute stream) */
+  int64_t first_start_ns;   /* relative to the iteration start event             */
   int64_t last_end_ns;
-  int64_t op_ns[3];          /* summed duration per kind F, B, W              */
+  int64_t op_ns[3];         /* summed duration per kind F, B, W                  */
   int64_t op_cnt[3];
+  int64_t host_enqueue_ns;  /* host time spent enqueueing the iteration          */
 } adaptra_iter_stats_t;
 
 int adaptra_exec_create(const adaptra_exec_desc_t* d, adaptra_exec_t* out);
 int adaptra_exec_destroy(adaptra_exec_t e);
-/* Enqueue one iteration: ops[n] in order (kind, mb); slots are assigned from
- * the stage's stash pool in op order (F takes, W frees).  Non-blocking. */
-int adaptra_run_iteration(adaptra_exec_t e, const adaptra_op_t* ops, int32_t n, uint32_t epoch, void* t0_event);
-/* Block until the iteration's work on this stage is done; fill stats. */
-int adaptra_exec_wait(adaptra_exec_t e, adaptra_iter_stats_t* stats_out);
+/* Post one iteration: ops[n] (kind, mb) in order; flags: ADAPTRA_MERGE_W runs W
+ * right after each B (1F1B).  Non-blocking (the stage thread enqueues). */
+int adaptra_run_iteration(adaptra_exec_t e, const adaptra_op_t* ops, int32_t n, uint32_t epoch, uint32_t flags);
+/* Wait until the stage thread has enqueued the whole iteration; returns its
+ * error, if any (call on every stage before adaptra_exec_wait so that a
+ * failed stage can be detected and the others released). */
+int adaptra_exec_join(adaptra_exec_t e);
+/* Wait until the iteration's GPU work on this stage is complete (bounded by
+ * $ADAPTRA_TIMEOUT_MS, default 120000: ELINK on timeout); fill stats.
+ * op_times_out (optional, n x 2 int64: start, end ns) gets per-op times. */
+int adaptra_exec_wait(adaptra_exec_t e, adaptra_iter_stats_t* stats_out, int64_t* op_times_out);
 
 #ifdef __cplusplus
 }

@@ -4,6 +4,12 @@ The compute path is libadaptra.so (csrc/, C-ABI in include/adaptra.h); this
 package is the thin Python binding and the torch-side driver (device memory,
 streams, process groups).
 """
-from . import _lib  # noqa: F401
+import os
+
+# Streams that block on stream memory waits must not share a hardware channel
+# with the streams that release them: give every stream its own connection.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
+from . import _lib  # noqa: E402,F401
 
 __all__ = ["_lib"]

@@ -24,7 +24,7 @@ EPI_STORE, EPI_GELU, EPI_RESID, EPI_DGELU, EPI_ACC_F32, EPI_STORE_F32, EPI_DSOFT
 CAUSAL_NONE, CAUSAL_TILE, CAUSAL_KEND, CAUSAL_KSTART = range(4)
 
 LINK_DIRECT, LINK_P2P, LINK_HOST = 0, 1, 2
-DIR_FWD, DIR_BWD = 0, 1
+IPC_BYTES = 128
 LINK_DOWN = (1 << 63) - 1
 
 _i32, _i64, _u32, _f32, _vp = C.c_int32, C.c_int64, C.c_uint32, C.c_float, C.c_void_p
@@ -59,30 +59,22 @@ class StageDesc(C.Structure):
     _fields_ = [
         ("block", _i32), ("dtype", _i32), ("n_layers", _i32), ("d", _i32), ("d_ff", _i32), ("n_heads", _i32),
         ("b", _i32), ("T", _i32), ("is_first", _i32), ("is_last", _i32), ("n_microbatches", _i32),
-        ("n_slots", _i32), ("wts", _vp), ("vecs", _vp), ("gwts", _vp), ("gvecs", _vp),
-        ("stash", _vp), ("work", _vp),
-    ]
-
-
-class LinkDesc(C.Structure):
-    _fields_ = [
-        ("mode", _i32), ("n_mb", _i32), ("bytes", _i64), ("dev_up", _i32), ("dev_down", _i32),
-        ("fwd_mbox", _vp), ("bwd_mbox", _vp), ("fwd_flags", _vp), ("bwd_flags", _vp),
-        ("host_fwd", _vp), ("host_bwd", _vp),
+        ("n_slots", _i32), ("n_slots_fb", _i32), ("wts", _vp), ("vecs", _vp), ("gwts", _vp), ("gvecs", _vp),
+        ("stash", _vp), ("stash_fb", _vp), ("work", _vp),
     ]
 
 
 class ExecDesc(C.Structure):
     _fields_ = [
         ("stage", _vp), ("stage_index", _i32), ("n_stages", _i32), ("n_microbatches", _i32),
-        ("link_up", _vp), ("link_down", _vp), ("compute_stream", _vp),
-        ("inputs", C.POINTER(_vp)), ("targets", C.POINTER(_vp)), ("loss_acc", _vp), ("merge_w", _u32),
+        ("in_fwd", _vp), ("in_bwd", _vp), ("out_fwd", _vp), ("out_bwd", _vp), ("compute_stream", _vp),
+        ("inputs", C.POINTER(_vp)), ("targets", C.POINTER(_vp)), ("loss_acc", _vp),
     ]
 
 
 class IterStats(C.Structure):
     _fields_ = [("n_ops", _i64), ("busy_ns", _i64), ("first_start_ns", _i64), ("last_end_ns", _i64),
-                ("op_ns", _i64 * 3), ("op_cnt", _i64 * 3)]
+                ("op_ns", _i64 * 3), ("op_cnt", _i64 * 3), ("host_enqueue_ns", _i64)]
 
 
 _P = C.POINTER
@@ -99,7 +91,10 @@ _SIGS = {
     "adaptra_validate": (_i32, [_i32, _i32, _P(_i64), _P(_i64), _P(_i64), _P(_i64), _P(Op), _P(_i32), _u32,
                                 _P(_i32)]),
     "adaptra_gemm": (_i32, [_P(GemmDesc), _vp]),
+    "adaptra_prof_enable": (_i32, [_i32]),
+    "adaptra_prof_collect": (_i32, [_i32, _P(_i64), _P(C.c_double), _P(C.c_double), _P(C.c_double)]),
     "adaptra_stage_slot_bytes": (_i64, [_P(StageDesc)]),
+    "adaptra_stage_slot_fb_bytes": (_i64, [_P(StageDesc)]),
     "adaptra_stage_work_bytes": (_i64, [_P(StageDesc)]),
     "adaptra_stage_wts_elems": (_i64, [_P(StageDesc)]),
     "adaptra_stage_vecs_elems": (_i64, [_P(StageDesc)]),
@@ -109,16 +104,26 @@ _SIGS = {
     "adaptra_stage_B": (_i32, [_vp, _i32, _vp, _vp, _vp]),
     "adaptra_stage_W": (_i32, [_vp, _i32, _vp]),
     "adaptra_stage_zero_grads": (_i32, [_vp, _vp]),
-    "adaptra_link_open": (_i32, [_P(LinkDesc), _P(_vp)]),
-    "adaptra_link_close": (_i32, [_vp]),
+    "adaptra_inbox_create": (_i32, [_i32, _i32, _i64, C.c_char_p, _P(_vp)]),
+    "adaptra_inbox_destroy": (_i32, [_vp]),
+    "adaptra_inbox_export": (_i32, [_vp, _P(C.c_uint8)]),
+    "adaptra_inbox_slot": (_vp, [_vp, _i32]),
+    "adaptra_recv": (_i32, [_vp, _i32, _u32, _vp, _P(_vp)]),
+    "adaptra_inbox_set_host": (_i32, [_vp, _i32]),
+    "adaptra_inbox_poison": (_i32, [_vp]),
+    "adaptra_inbox_reset": (_i32, [_vp]),
+    "adaptra_outbox_open_local": (_i32, [_i32, _vp, _i32, _P(_vp)]),
+    "adaptra_outbox_open_ipc": (_i32, [_i32, _P(C.c_uint8), _i32, _i64, C.c_char_p, _i32, _P(_vp)]),
+    "adaptra_outbox_close": (_i32, [_vp]),
+    "adaptra_outbox_dst": (_vp, [_vp, _i32]),
     "adaptra_set_link_latency": (_i32, [_vp, _i64]),
-    "adaptra_send": (_i32, [_vp, _i32, _i32, _vp, _vp, _u32]),
-    "adaptra_recv": (_i32, [_vp, _i32, _i32, _vp, _u32, _P(_vp)]),
+    "adaptra_send": (_i32, [_vp, _i32, _vp, _u32]),
     "adaptra_link_stats": (_i32, [_vp, _P(_i64), _P(_i64), _P(_i64)]),
     "adaptra_exec_create": (_i32, [_P(ExecDesc), _P(_vp)]),
     "adaptra_exec_destroy": (_i32, [_vp]),
-    "adaptra_run_iteration": (_i32, [_vp, _P(Op), _i32, _u32, _vp]),
-    "adaptra_exec_wait": (_i32, [_vp, _P(IterStats)]),
+    "adaptra_run_iteration": (_i32, [_vp, _P(Op), _i32, _u32, _u32]),
+    "adaptra_exec_join": (_i32, [_vp]),
+    "adaptra_exec_wait": (_i32, [_vp, _P(IterStats), _P(_i64)]),
 }
 
 _lib = None

@@ -1,0 +1,11 @@
+// Internal helpers shared by the executor and the transport.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace adaptra {
+int stream_wait_geq(cudaStream_t st, const uint32_t* addr, uint32_t v);
+int stream_write(cudaStream_t st, uint32_t* addr, uint32_t v);
+int64_t now_ns();
+cudaStream_t signal_stream(int dev);
+}  // namespace adaptra

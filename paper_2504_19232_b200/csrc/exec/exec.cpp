@@ -1,0 +1,244 @@
+// Per-stage schedule executor: one host thread per stage interprets the
+// stage's op order for one iteration.  Inputs are awaited on the GPU
+// (adaptra_recv enqueues a stream memory wait), so the thread enqueues the
+// whole iteration without ever blocking on communication: a late message
+// delays only the ops that depend on it, never the launch of later kernels
+// (no head-of-line blocking).  Outputs are handed to the outbox
+// right after the producing op (adaptra_send, own stream).
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <condition_variable>
+#include <cstdlib>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../../include/adaptra.h"
+#include "../comm/transport.h"
+#include "../util.h"
+
+namespace adaptra {
+int stage_n_slots(adaptra_stage_t s);
+int stage_device(adaptra_stage_t s);
+}  // namespace adaptra
+
+using namespace adaptra;
+
+struct adaptra_exec {
+  adaptra_exec_desc_t d{};
+  int dev = 0;
+  cudaStream_t cs = nullptr;
+  std::thread th;
+  std::mutex mu;
+  std::condition_variable cv;
+  bool stop = false, has_job = false, busy = false;
+  std::vector<adaptra_op_t> ops;
+  uint32_t epoch = 0, flags = 0;
+  int rc = ADAPTRA_OK;
+  std::string err;
+  int64_t host_ns = 0;
+  cudaEvent_t ev_t0 = nullptr;
+  std::vector<cudaEvent_t> ev_s, ev_e;
+  std::vector<int> slot_of_mb;
+
+  int run_one() {
+    cudaSetDevice(dev);
+    const int S = d.n_stages, i = d.stage_index, N = d.n_microbatches;
+    const bool merge = flags & ADAPTRA_MERGE_W;
+    const int64_t t_start = now_ns();
+    std::vector<int> free_slots;
+    for (int k = stage_n_slots(d.stage) - 1; k >= 0; --k) free_slots.push_back(k);
+    slot_of_mb.assign(N + 1, -1);
+    ADAPTRA_CUDA_TRY(cudaEventRecord(ev_t0, cs));
+    if (i == S - 1 && d.loss_acc) ADAPTRA_CUDA_TRY(cudaMemsetAsync(d.loss_acc, 0, sizeof(float), cs));
+    int rc;
+    if ((rc = adaptra_stage_zero_grads(d.stage, cs))) return rc;  // gradients of this iteration only
+    for (size_t q = 0; q < ops.size(); ++q) {
+      const adaptra_op_t& o = ops[q];
+      const int mb = o.mb;
+      if (mb < 1 || mb > N) return set_error(ADAPTRA_EINVAL, "exec: bad microbatch");
+      if (o.kind == ADAPTRA_OP_F) {
+        if (free_slots.empty()) return set_error(ADAPTRA_ENOMEM, "exec: stash slots exhausted (plan needs more)");
+        int slot = free_slots.back();
+        free_slots.pop_back();
+        slot_of_mb[mb] = slot;
+        const void* x = nullptr;
+        if (i == 0) {
+          x = d.inputs[mb - 1];
+        } else {
+          void* p = nullptr;
+          if ((rc = adaptra_recv(d.in_fwd, mb - 1, epoch, cs, &p))) return rc;
+          x = p;
+        }
+        void* y = (i < S - 1) ? adaptra_outbox_dst(d.out_fwd, mb - 1) : nullptr;
+        ADAPTRA_CUDA_TRY(cudaEventRecord(ev_s[q], cs));
+        if ((rc = adaptra_stage_F(d.stage, slot, x, y, i == S - 1 ? d.targets[mb - 1] : nullptr,
+                                  i == S - 1 ? d.loss_acc : nullptr, cs)))
+          return rc;
+        ADAPTRA_CUDA_TRY(cudaEventRecord(ev_e[q], cs));
+        if (i < S - 1 && (rc = adaptra_send(d.out_fwd, mb - 1, cs, epoch))) return rc;
+      } else if (o.kind == ADAPTRA_OP_B) {
+        int slot = slot_of_mb[mb];
+        if (slot < 0) return set_error(ADAPTRA_EINVAL, "exec: B before F");
+        void* dy = nullptr;
+        if (i < S - 1 && (rc = adaptra_recv(d.in_bwd, mb - 1, epoch, cs, &dy))) return rc;
+        void* dx = (i > 0) ? adaptra_outbox_dst(d.out_bwd, mb - 1) : nullptr;
+        ADAPTRA_CUDA_TRY(cudaEventRecord(ev_s[q], cs));
+        if ((rc = adaptra_stage_B(d.stage, slot, dy, dx, cs))) return rc;
+        if (merge) {
+          if ((rc = adaptra_stage_W(d.stage, slot, cs))) return rc;
+          free_slots.push_back(slot);
+          slot_of_mb[mb] = -1;
+        }
+        ADAPTRA_CUDA_TRY(cudaEventRecord(ev_e[q], cs));
+        if (i > 0 && (rc = adaptra_send(d.out_bwd, mb - 1, cs, epoch))) return rc;
+      } else if (o.kind == ADAPTRA_OP_W) {
+        int slot = slot_of_mb[mb];
+        if (slot < 0) return set_error(ADAPTRA_EINVAL, "exec: W before F");
+        ADAPTRA_CUDA_TRY(cudaEventRecord(ev_s[q], cs));
+        if ((rc = adaptra_stage_W(d.stage, slot, cs))) return rc;
+        ADAPTRA_CUDA_TRY(cudaEventRecord(ev_e[q], cs));
+        free_slots.push_back(slot);
+        slot_of_mb[mb] = -1;
+      } else {
+        return set_error(ADAPTRA_EINVAL, "exec: bad op kind");
+      }
+    }
+    host_ns = now_ns() - t_start;
+    return ADAPTRA_OK;
+  }
+
+  void loop() {
+    for (;;) {
+      std::unique_lock<std::mutex> lk(mu);
+      cv.wait(lk, [&] { return stop || has_job; });
+      if (stop) return;
+      has_job = false;
+      lk.unlock();
+      int r = run_one();
+      std::string e = r ? last_error() : "";
+      lk.lock();
+      rc = r;
+      err = e;
+      busy = false;
+      cv.notify_all();
+    }
+  }
+};
+
+extern "C" int adaptra_exec_create(const adaptra_exec_desc_t* d, adaptra_exec_t* out) {
+  if (!d || !out || !d->stage || d->n_stages < 1 || d->stage_index < 0 || d->stage_index >= d->n_stages ||
+      d->n_microbatches < 1 || !d->compute_stream)
+    return set_error(ADAPTRA_EINVAL, "exec_create: bad args");
+  const int i = d->stage_index, S = d->n_stages;
+  if ((i > 0 && (!d->in_fwd || !d->out_bwd)) || (i < S - 1 && (!d->in_bwd || !d->out_fwd)) ||
+      (i == 0 && !d->inputs) || (i == S - 1 && (!d->targets || !d->loss_acc)))
+    return set_error(ADAPTRA_EINVAL, "exec_create: missing link or io buffers");
+  auto* e = new adaptra_exec();
+  e->d = *d;
+  e->cs = (cudaStream_t)d->compute_stream;
+  e->dev = stage_device(d->stage);
+  cudaSetDevice(e->dev);
+  int cap = 3 * d->n_microbatches;
+  e->ev_s.resize(cap);
+  e->ev_e.resize(cap);
+  cudaEventCreate(&e->ev_t0);
+  for (int k = 0; k < cap; ++k) {
+    cudaEventCreate(&e->ev_s[k]);
+    cudaEventCreate(&e->ev_e[k]);
+  }
+  e->th = std::thread([e] { e->loop(); });
+  *out = e;
+  return ADAPTRA_OK;
+}
+
+extern "C" int adaptra_exec_destroy(adaptra_exec_t e) {
+  if (!e) return ADAPTRA_OK;
+  {
+    std::unique_lock<std::mutex> lk(e->mu);
+    e->cv.wait(lk, [&] { return !e->busy; });
+    e->stop = true;
+  }
+  e->cv.notify_all();
+  e->th.join();
+  cudaSetDevice(e->dev);
+  cudaEventDestroy(e->ev_t0);
+  for (auto ev : e->ev_s) cudaEventDestroy(ev);
+  for (auto ev : e->ev_e) cudaEventDestroy(ev);
+  delete e;
+  return ADAPTRA_OK;
+}
+
+extern "C" int adaptra_run_iteration(adaptra_exec_t e, const adaptra_op_t* ops, int32_t n, uint32_t epoch,
+                                     uint32_t flags) {
+  if (!e || !ops || n < 0 || n > (int)e->ev_s.size()) return set_error(ADAPTRA_EINVAL, "run_iteration: bad args");
+  std::unique_lock<std::mutex> lk(e->mu);
+  if (e->busy) return set_error(ADAPTRA_EINVAL, "run_iteration: previous iteration still running");
+  e->ops.assign(ops, ops + n);
+  e->epoch = epoch;
+  e->flags = flags;
+  e->has_job = true;
+  e->busy = true;
+  e->rc = ADAPTRA_OK;
+  e->cv.notify_all();
+  return ADAPTRA_OK;
+}
+
+extern "C" int adaptra_exec_join(adaptra_exec_t e) {
+  if (!e) return set_error(ADAPTRA_EINVAL, "exec_join: null");
+  std::unique_lock<std::mutex> lk(e->mu);
+  e->cv.wait(lk, [&] { return !e->busy; });
+  if (e->rc) return set_error(e->rc, e->err);
+  return ADAPTRA_OK;
+}
+
+extern "C" int adaptra_exec_wait(adaptra_exec_t e, adaptra_iter_stats_t* st, int64_t* op_times) {
+  if (!e) return set_error(ADAPTRA_EINVAL, "exec_wait: null");
+  {
+    std::unique_lock<std::mutex> lk(e->mu);
+    e->cv.wait(lk, [&] { return !e->busy; });
+    if (e->rc) return set_error(e->rc, e->err);
+  }
+  cudaSetDevice(e->dev);
+  // bounded wait: a message that never arrives must not hang the process
+  static const int64_t timeout_ns = [] {
+    const char* v = getenv("ADAPTRA_TIMEOUT_MS");
+    return (v ? atoll(v) : 120000) * 1000000LL;
+  }();
+  const int64_t t0 = now_ns();
+  for (;;) {
+    cudaError_t q = cudaStreamQuery(e->cs);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) return set_error(ADAPTRA_ECUDA, std::string("exec_wait: ") + cudaGetErrorString(q));
+    if (now_ns() - t0 > timeout_ns) return set_error(ADAPTRA_ELINK, "exec_wait: iteration timed out (message lost?)");
+    std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+  adaptra_iter_stats_t s{};
+  s.n_ops = (int64_t)e->ops.size();
+  s.first_start_ns = INT64_MAX;
+  s.last_end_ns = 0;
+  for (size_t q = 0; q < e->ops.size(); ++q) {
+    float a = 0.f, b = 0.f;
+    ADAPTRA_CUDA_TRY(cudaEventElapsedTime(&a, e->ev_t0, e->ev_s[q]));
+    ADAPTRA_CUDA_TRY(cudaEventElapsedTime(&b, e->ev_t0, e->ev_e[q]));
+    int64_t s0 = (int64_t)(a * 1e6), e0 = (int64_t)(b * 1e6);
+    if (op_times) {
+      op_times[2 * q] = s0;
+      op_times[2 * q + 1] = e0;
+    }
+    s.busy_ns += e0 - s0;
+    int k = e->ops[q].kind;
+    if (k >= 0 && k < 3) {
+      s.op_ns[k] += e0 - s0;
+      s.op_cnt[k] += 1;
+    }
+    if (s0 < s.first_start_ns) s.first_start_ns = s0;
+    if (e0 > s.last_end_ns) s.last_end_ns = e0;
+  }
+  if (s.n_ops == 0) s.first_start_ns = 0;
+  s.host_enqueue_ns = e->host_ns;
+  if (st) *st = s;
+  return ADAPTRA_OK;
+}

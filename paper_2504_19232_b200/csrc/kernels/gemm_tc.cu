@@ -17,6 +17,7 @@
 #include <string>
 
 #include "../../../include/adaptra.h"
+#include "../prof.h"
 #include "../util.h"
 #include "common.cuh"
 #include "epilogue.cuh"
@@ -318,7 +319,15 @@ static int launch_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
                (g.c_1 % 8 == 0) && (g.c_2 % 8 == 0) && (g.aux_1 % 8 == 0) && (g.aux_2 % 8 == 0);
   int grid = n_tiles < num_sms() ? n_tiles : num_sms();
   if (grid < 1) return ADAPTRA_OK;
+  void* pb = prof_on() ? prof_begin(st) : nullptr;
   kern<<<grid, kThreads, Cfg::kSmem, st>>>(ma, mbm, g, ti, vec_ok);
+  if (pb) {
+    // algorithmic FLOPs: 2MNK per batch; causal variants count the lower half (R28)
+    double fl = 2.0 * g.M * (double)g.N * g.K * g.Z * (g.causal ? 0.5 : 1.0);
+    bool f32o = (g.epi == ADAPTRA_EPI_ACC_F32 || g.epi == ADAPTRA_EPI_STORE_F32);
+    double by = 2.0 * ((double)g.M * g.K + (double)g.N * g.K) * g.Z + (f32o ? 4.0 : 2.0) * g.M * (double)g.N * g.Z;
+    prof_end(pb, st, PROF_GEMM_TC, fl, by);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(ADAPTRA_ECUDA, std::string("gemm_tc launch: ") + cudaGetErrorString(e));
   return ADAPTRA_OK;

@@ -1,0 +1,9 @@
+#pragma once
+#include <cuda_runtime.h>
+
+namespace adaptra {
+enum { PROF_GEMM_TC = 0, PROF_GEMM_SIMT = 1 };
+bool prof_on();
+void* prof_begin(cudaStream_t st);
+void prof_end(void* begin, cudaStream_t st, int kind, double flops, double bytes);
+}  // namespace adaptra

@@ -65,7 +65,7 @@ struct SlotLayout {
   // per layer (GPT): xl h1 qkv P o y1 h2 a g dqkv dy1 da dyl dh2 dh1 | f32: mean1 rstd1 mean2 rstd2
   // per layer (MLP): xl a g da dyl
   long xl, h1, qkv, P, o, y1, h2, a, g, dqkv, dy1, da, dyl, dh2, dh1, mean1, rstd1, mean2, rstd2;
-  long layer_bytes;
+  long layer_bytes, fb_layer_bytes, fb_slot_bytes;
   long yL, seed;  // stage-level (after the per-layer block)
   long slot_bytes;
   // work area
@@ -78,10 +78,13 @@ struct adaptra_stage_impl;
 
 struct adaptra_stage {
   adaptra_stage_desc_t d;
+  int dev = 0;
   adaptra::SlotLayout L;
   long R;  // rows = b*T
   std::vector<const void*> x_in;  // per slot: layer-0 input pointer (mailbox), kept until W
   std::vector<const void*> dy_in;  // per slot: top-layer output gradient pointer
+  std::vector<int> fb_of;          // per slot: F->B pool index (-1 if none)
+  std::vector<int> fb_free;        // free F->B pool indices (issue order)
 };
 
 namespace adaptra {
@@ -110,12 +113,9 @@ static int compute_layout(const adaptra_stage_desc_t& d, SlotLayout& L) {
     long PT = (long)d.b * d.n_heads * d.T * d.T;
     L.xl = put(R * D * e);
     L.h1 = put(R * D * e);
-    L.qkv = put(R * 3 * D * e);
-    L.P = put(PT * e);
     L.o = put(R * D * e);
     L.y1 = put(R * D * e);
     L.h2 = put(R * D * e);
-    L.a = put(R * F * e);
     L.g = put(R * F * e);
     L.dqkv = put(R * 3 * D * e);
     L.dy1 = put(R * D * e);
@@ -127,12 +127,24 @@ static int compute_layout(const adaptra_stage_desc_t& d, SlotLayout& L) {
     L.rstd1 = put(R * 4);
     L.mean2 = put(R * 4);
     L.rstd2 = put(R * 4);
+    // F->B pool (freed when B ends)
+    long off_w = off;
+    off = 0;
+    L.qkv = put(R * 3 * D * e);
+    L.P = put(PT * e);
+    L.a = put(R * F * e);
+    L.fb_layer_bytes = off;
+    off = off_w;
   } else if (d.block == ADAPTRA_BLOCK_MLP) {
     L.xl = put(R * D * e);
-    L.a = put(R * F * e);
     L.g = put(R * F * e);
     L.da = put(R * F * e);
     L.dyl = put(R * D * e);
+    long off_w = off;
+    off = 0;
+    L.a = put(R * F * e);
+    L.fb_layer_bytes = off;
+    off = off_w;
   } else {
     return set_error(ADAPTRA_EINVAL, "stage: bad block kind");
   }
@@ -141,6 +153,7 @@ static int compute_layout(const adaptra_stage_desc_t& d, SlotLayout& L) {
   L.yL = tail;
   L.seed = align256(L.yL + R * D * e);
   L.slot_bytes = d.is_last ? align256(L.seed + R * D * e) : tail;
+  L.fb_slot_bytes = L.fb_layer_bytes * d.n_layers;
   long w = 0;
   if (d.block == ADAPTRA_BLOCK_GPT) {
     long PT = (long)d.b * d.n_heads * d.T * d.T;
@@ -201,6 +214,9 @@ struct StageOps {
   char* slot_base(int slot) const { return (char*)s->d.stash + (long)slot * s->L.slot_bytes; }
   char* lay(int slot, int l) const { return slot_base(slot) + (long)l * s->L.layer_bytes; }
   T* buf(int slot, int l, long off) const { return (T*)(lay(slot, l) + off); }
+  T* fbb(int slot, int l, long off) const {
+    return (T*)((char*)s->d.stash_fb + (long)s->fb_of[slot] * s->L.fb_slot_bytes + (long)l * s->L.fb_layer_bytes + off);
+  }
   float* fbuf(int slot, int l, long off) const { return (float*)(lay(slot, l) + off); }
   const T* W(long off) const { return (const T*)s->d.wts + off; }
   const float* V(long off) const { return s->d.vecs + off; }
@@ -236,7 +252,7 @@ struct StageOps {
       T* y = layer_out(slot, l, y_out);
       if (!y) return set_error(ADAPTRA_EINVAL, "stage_F: y_out is null on a non-last stage");
       if (D.block == ADAPTRA_BLOCK_MLP) {
-        T* a = buf(slot, l, s->L.a);
+        T* a = fbb(slot, l, s->L.a);
         T* g = buf(slot, l, s->L.g);
         TRY(GB(dt()).shape(R, Ff, Dm).A(x, Dm, R, Dm).B(W(p.W1), Dm, Ff, Dm).C(g, Ff).aux(a, Ff)
                 .epi(ADAPTRA_EPI_GELU).bias(V(p.b1)).run(st));
@@ -247,12 +263,12 @@ struct StageOps {
       const int H = D.n_heads, Tn = D.T, b = D.b;
       const long dh = Dm / H;
       T* h1 = buf(slot, l, s->L.h1);
-      T* qkv = buf(slot, l, s->L.qkv);
-      T* P = buf(slot, l, s->L.P);
+      T* qkv = fbb(slot, l, s->L.qkv);
+      T* P = fbb(slot, l, s->L.P);
       T* o = buf(slot, l, s->L.o);
       T* y1 = buf(slot, l, s->L.y1);
       T* h2 = buf(slot, l, s->L.h2);
-      T* a = buf(slot, l, s->L.a);
+      T* a = fbb(slot, l, s->L.a);
       T* g = buf(slot, l, s->L.g);
       float* S = (float*)((char*)D.work + s->L.w_S);
       TRY(ln_fwd<T>(x, V(p.ln1_g), V(p.ln1_b), h1, fbuf(slot, l, s->L.mean1), fbuf(slot, l, s->L.rstd1), R, Dm, st));
@@ -297,7 +313,7 @@ struct StageOps {
       const T* dy = layer_dy(slot, l);
       T* dx = layer_dx(slot, l, dx_out);
       const T* x = layer_in(slot, l);
-      T* a = buf(slot, l, s->L.a);
+      T* a = fbb(slot, l, s->L.a);
       T* da = buf(slot, l, s->L.da);
       // da = (dy W2) * gelu'(a)     (W2 [d, dff] read MN-major)
       TRY(GB(dt()).shape(R, Ff, Dm).A(dy, Dm, R, Dm).B(W(p.W2), Ff, Dm, Ff, 1).C(da, Ff)
@@ -310,8 +326,8 @@ struct StageOps {
       }
       const int H = D.n_heads, Tn = D.T, b = D.b;
       const long dh = Dm / H;
-      T* qkv = buf(slot, l, s->L.qkv);
-      T* P = buf(slot, l, s->L.P);
+      T* qkv = fbb(slot, l, s->L.qkv);
+      T* P = fbb(slot, l, s->L.P);
       T* o = buf(slot, l, s->L.o);
       T* y1 = buf(slot, l, s->L.y1);
       T* dqkv = buf(slot, l, s->L.dqkv);
@@ -408,10 +424,20 @@ struct StageOps {
 
 using namespace adaptra;
 
+namespace adaptra {
+int stage_n_slots(adaptra_stage_t s) { return s->d.n_slots; }
+int stage_device(adaptra_stage_t s) { return s->dev; }
+}  // namespace adaptra
+
 extern "C" int64_t adaptra_stage_slot_bytes(const adaptra_stage_desc_t* d) {
   SlotLayout L;
   if (!d || compute_layout(*d, L)) return -1;
   return L.slot_bytes;
+}
+extern "C" int64_t adaptra_stage_slot_fb_bytes(const adaptra_stage_desc_t* d) {
+  SlotLayout L;
+  if (!d || compute_layout(*d, L)) return -1;
+  return L.fb_slot_bytes;
 }
 extern "C" int64_t adaptra_stage_work_bytes(const adaptra_stage_desc_t* d) {
   SlotLayout L;
@@ -434,14 +460,20 @@ extern "C" int adaptra_stage_create(const adaptra_stage_desc_t* d, adaptra_stage
     delete s;
     return rc;
   }
-  if (!d->wts || !d->vecs || !d->gwts || !d->gvecs || !d->stash || d->n_slots < 1 ||
+  if (!d->wts || !d->vecs || !d->gwts || !d->gvecs || !d->stash || d->n_slots < 1 || !d->stash_fb ||
+      d->n_slots_fb < 1 ||
       (s->L.work_bytes > 0 && !d->work)) {
     delete s;
     return set_error(ADAPTRA_EINVAL, "stage_create: missing buffers");
   }
   s->R = (long)d->b * d->T;
+  cudaPointerAttributes pa;
+  if (cudaPointerGetAttributes(&pa, d->wts) == cudaSuccess && pa.type == cudaMemoryTypeDevice) s->dev = pa.device;
+  else cudaGetDevice(&s->dev);
   s->x_in.assign(d->n_slots, nullptr);
   s->dy_in.assign(d->n_slots, nullptr);
+  s->fb_of.assign(d->n_slots, -1);
+  for (int k = d->n_slots_fb - 1; k >= 0; --k) s->fb_free.push_back(k);
   *out = s;
   return ADAPTRA_OK;
 }
@@ -454,6 +486,10 @@ extern "C" int adaptra_stage_destroy(adaptra_stage_t s) {
 extern "C" int adaptra_stage_F(adaptra_stage_t s, int32_t slot, const void* x_in, void* y_out, const float* target,
                                float* loss_acc, void* stream) {
   if (!s || slot < 0 || slot >= s->d.n_slots || !x_in) return set_error(ADAPTRA_EINVAL, "stage_F: bad args");
+  if (s->fb_of[slot] >= 0) return set_error(ADAPTRA_EINVAL, "stage_F: slot still holds an un-consumed F");
+  if (s->fb_free.empty()) return set_error(ADAPTRA_ENOMEM, "stage_F: F->B stash pool exhausted");
+  s->fb_of[slot] = s->fb_free.back();
+  s->fb_free.pop_back();
   s->x_in[slot] = x_in;
   s->dy_in[slot] = nullptr;
   if (s->d.dtype == ADAPTRA_BF16) return StageOps<bf16>{s, (cudaStream_t)stream}.F(slot, y_out, target, loss_acc);
@@ -469,8 +505,14 @@ extern "C" int adaptra_stage_B(adaptra_stage_t s, int32_t slot, const void* dy_i
     return set_error(ADAPTRA_EINVAL, "stage_B: F was not run for this slot");
   }
   if (!s->d.is_first && !dx_out) return set_error(ADAPTRA_EINVAL, "stage_B: dx_out required on a non-first stage");
-  if (s->d.dtype == ADAPTRA_BF16) return StageOps<bf16>{s, (cudaStream_t)stream}.B(slot, s->d.is_first ? nullptr : dx_out);
-  return StageOps<float>{s, (cudaStream_t)stream}.B(slot, s->d.is_first ? nullptr : dx_out);
+  if (s->fb_of[slot] < 0) return set_error(ADAPTRA_EINVAL, "stage_B: no F for this slot");
+  int rc = s->d.dtype == ADAPTRA_BF16
+               ? StageOps<bf16>{s, (cudaStream_t)stream}.B(slot, s->d.is_first ? nullptr : dx_out)
+               : StageOps<float>{s, (cudaStream_t)stream}.B(slot, s->d.is_first ? nullptr : dx_out);
+  // the F->B buffers are free once B's kernels are enqueued (stream order)
+  s->fb_free.push_back(s->fb_of[slot]);
+  s->fb_of[slot] = -1;
+  return rc;
 }
 
 extern "C" int adaptra_stage_W(adaptra_stage_t s, int32_t slot, void* stream) {

@@ -1,0 +1,369 @@
+"""Pipeline driver: builds stages, links and executors through the C-ABI and
+runs iterations under a schedule arm (1F1B / ZB / adaptive) with injected
+link latencies.  Control plane only (torch for memory and streams,
+torch.distributed gloo for handle exchange / schedule broadcast / barriers);
+every F/B/W, transfer and the schedule itself run in libadaptra.so.
+
+Stage -> rank placement: contiguous, stage i on rank floor(i * world / S);
+one process per GPU (rank r uses cuda:local_rank).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import secrets
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from . import sched as cs
+from .stage import Stage
+
+
+@dataclass
+class ModelCfg:
+    block: str = "gpt"          # "gpt" | "mlp"
+    n_layers: int = 24          # total blocks, split evenly over stages
+    d: int = 2048
+    d_ff: int = 8192
+    n_heads: int = 16
+    b: int = 1                  # sequences per microbatch
+    T: int = 2048               # tokens per sequence
+    dtype: int = L.BF16
+
+    @property
+    def tokens_per_mb(self):
+        return self.b * self.T
+
+
+@dataclass
+class IterResult:
+    epoch: int
+    stats: dict                  # stage -> IterStats fields (+ op_times)
+    loss: float | None = None
+
+
+def _op_array(ops):
+    arr = (L.Op * max(1, len(ops)))()
+    for q, (k, mb) in enumerate(ops):
+        arr[q].kind = cs.KIND_ID[k]
+        arr[q].mb = mb
+    return arr
+
+
+class Pipeline:
+    def __init__(self, model: ModelCfg, S: int, N: int, *, params=None, inputs=None, targets=None,
+                 rank: int = 0, world: int = 1, device: int = 0, group=None, link_mode: int = L.LINK_DIRECT,
+                 host_links: bool = True, n_slots=None, n_slots_fb=None, seed: int = 0):
+        if model.n_layers % S:
+            raise ValueError("n_layers must divide evenly over stages")
+        self.model, self.S, self.N = model, S, N
+        self.rank, self.world, self.group = rank, world, group
+        self.dev = device
+        torch.cuda.set_device(device)
+        self.Ls = model.n_layers // S
+        self.stage_rank = [i * world // S for i in range(S)]
+        self.local = [i for i in range(S) if self.stage_rank[i] == rank]
+        self.msg_bytes = model.tokens_per_mb * model.d * (2 if model.dtype == L.BF16 else 4)
+        lib = L.lib()
+        block = L.BLOCK_GPT if model.block == "gpt" else L.BLOCK_MLP
+        # ---------------- stages
+        self.stages = {}
+        for i in self.local:
+            ns = n_slots[i] if isinstance(n_slots, (list, tuple)) else (n_slots or N)
+            nf = n_slots_fb[i] if isinstance(n_slots_fb, (list, tuple)) else (n_slots_fb or ns)
+            st = Stage(block, model.dtype, self.Ls, model.d, model.d_ff, model.n_heads, model.b, model.T,
+                       i == 0, i == S - 1, N, ns, f"cuda:{device}", n_slots_fb=nf)
+            if params is not None:
+                st.load_params(params[i])
+            else:
+                self._init_params(st, i, seed)
+            self.stages[i] = st
+        # ---------------- io
+        tdt = self.stages[self.local[0]].tdt
+        R = model.tokens_per_mb
+        self.inputs, self.targets = [], []
+        if 0 in self.stages:
+            if inputs is not None:
+                self.inputs = [torch.from_numpy(np.asarray(x, np.float32).reshape(R, model.d)).to(
+                    f"cuda:{device}", tdt) for x in inputs]
+            else:
+                g = torch.Generator(device=f"cuda:{device}").manual_seed(seed + 1)
+                self.inputs = [torch.randn(R, model.d, device=f"cuda:{device}", generator=g).to(tdt)
+                               for _ in range(N)]
+        if S - 1 in self.stages:
+            if targets is not None:
+                self.targets = [torch.from_numpy(np.asarray(t, np.float32).reshape(R, model.d)).to(
+                    f"cuda:{device}") for t in targets]
+            else:
+                g = torch.Generator(device=f"cuda:{device}").manual_seed(seed + 2)
+                self.targets = [torch.randn(R, model.d, device=f"cuda:{device}", generator=g) for _ in range(N)]
+            self.loss = torch.zeros(1, device=f"cuda:{device}")
+        # ---------------- links: inboxes on receivers, outboxes on senders
+        token = self._bcast(secrets.token_hex(4) if rank == 0 else None)
+        self._host_names = {}
+        self.in_fwd, self.in_bwd, self.out_fwd, self.out_bwd = {}, {}, {}, {}
+        exports = {}
+        for i in self.local:
+            if i > 0:
+                nm = f"/adaptra_{token}_{i - 1}_f" if host_links else None
+                h = C.c_void_p()
+                L.check(lib.adaptra_inbox_create(device, N, self.msg_bytes, nm.encode() if nm else None,
+                                                 C.byref(h)))
+                self.in_fwd[i] = h
+                exports[("f", i - 1)] = (self._export(h), nm)
+            if i < S - 1:
+                nm = f"/adaptra_{token}_{i}_b" if host_links else None
+                h = C.c_void_p()
+                L.check(lib.adaptra_inbox_create(device, N, self.msg_bytes, nm.encode() if nm else None,
+                                                 C.byref(h)))
+                self.in_bwd[i] = h
+                exports[("b", i)] = (self._export(h), nm)
+        all_exports = self._allgather(exports)
+        for i in self.local:
+            if i < S - 1:   # forward link i -> inbox of stage i+1
+                self.out_fwd[i] = self._open_out(i + 1, self.in_fwd, ("f", i), all_exports, link_mode)
+            if i > 0:       # backward link i-1 -> inbox of stage i-1
+                self.out_bwd[i] = self._open_out(i - 1, self.in_bwd, ("b", i - 1), all_exports, link_mode)
+        # ---------------- executors
+        self.streams, self.execs = {}, {}
+        self._keep = []
+        for i in self.local:
+            s = torch.cuda.Stream(device=device)
+            self.streams[i] = s
+            d = L.ExecDesc()
+            d.stage = self.stages[i].handle
+            d.stage_index, d.n_stages, d.n_microbatches = i, S, N
+            d.in_fwd = self.in_fwd.get(i)
+            d.in_bwd = self.in_bwd.get(i)
+            d.out_fwd = self.out_fwd.get(i)
+            d.out_bwd = self.out_bwd.get(i)
+            d.compute_stream = s.cuda_stream
+            if i == 0:
+                arr = (C.c_void_p * N)(*[t.data_ptr() for t in self.inputs])
+                self._keep.append(arr)
+                d.inputs = arr
+            if i == S - 1:
+                arr = (C.c_void_p * N)(*[t.data_ptr() for t in self.targets])
+                self._keep.append(arr)
+                d.targets = arr
+                d.loss_acc = self.loss.data_ptr()
+            h = C.c_void_p()
+            L.check(lib.adaptra_exec_create(C.byref(d), C.byref(h)))
+            self.execs[i] = h
+        self.epoch = 0
+        self.latency = [0] * (S - 1)
+        torch.cuda.synchronize(device)
+        self._barrier()
+
+    # ------------------------------------------------------------ setup helpers
+    def _init_params(self, st: Stage, i: int, seed: int):
+        """GPT-2 init drawn on the device (bench sizes): weights N(0, 0.02), output
+        projections scaled by 1/sqrt(2 n_layers); LN gamma 1, beta 0; biases 0."""
+        m = self.model
+        g = torch.Generator(device=st.device).manual_seed(seed * 1000 + i)
+        w = torch.randn(st.wts.numel(), device=st.device, generator=g) * 0.02
+        st.wts.copy_(w.to(st.tdt))
+        v = torch.zeros(st.vecs.numel(), device=st.device)
+        if m.block == "gpt":
+            per = 2 * m.d + 3 * m.d + m.d + 2 * m.d + m.d_ff + m.d
+            for l in range(self.Ls):
+                o = l * per
+                v[o:o + m.d] = 1.0                            # ln1_g
+                v[o + 6 * m.d:o + 7 * m.d] = 1.0              # ln2_g
+        st.vecs.copy_(v)
+
+    def _export(self, h):
+        buf = (C.c_uint8 * L.IPC_BYTES)()
+        L.check(L.lib().adaptra_inbox_export(h, buf))
+        return bytes(buf)
+
+    def _open_out(self, peer_stage, local_inboxes, key, all_exports, mode):
+        lib = L.lib()
+        h = C.c_void_p()
+        if self.stage_rank[peer_stage] == self.rank:
+            L.check(lib.adaptra_outbox_open_local(self.dev, local_inboxes[peer_stage], mode, C.byref(h)))
+        else:
+            handle, nm = all_exports[key]
+            hb = (C.c_uint8 * L.IPC_BYTES)(*handle)
+            L.check(lib.adaptra_outbox_open_ipc(self.dev, hb, self.N, self.msg_bytes,
+                                                nm.encode() if nm else None, mode, C.byref(h)))
+        return h
+
+    def _bcast(self, obj):
+        if self.world == 1:
+            return obj
+        import torch.distributed as dist
+        lst = [obj]
+        dist.broadcast_object_list(lst, src=0, group=self.group)
+        return lst[0]
+
+    def _allgather(self, d):
+        if self.world == 1:
+            return dict(d)
+        import torch.distributed as dist
+        out = [None] * self.world
+        dist.all_gather_object(out, d, group=self.group)
+        merged = {}
+        for x in out:
+            merged.update(x)
+        return merged
+
+    def _barrier(self):
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier(group=self.group)
+
+    # ------------------------------------------------------------ control
+    def set_latency(self, link: int, ns: int):
+        """Inject latency c_link (ns) or L.LINK_DOWN on both directions of `link`."""
+        lib = L.lib()
+        self.latency[link] = ns
+        if link in self.out_fwd:
+            L.check(lib.adaptra_set_link_latency(self.out_fwd[link], ns))
+        if link + 1 in self.out_bwd:
+            L.check(lib.adaptra_set_link_latency(self.out_bwd[link + 1], ns))
+        down = 1 if ns == L.LINK_DOWN else 0
+        if link + 1 in self.in_fwd:
+            L.check(lib.adaptra_inbox_set_host(self.in_fwd[link + 1], down))
+        if link in self.in_bwd:
+            L.check(lib.adaptra_inbox_set_host(self.in_bwd[link], down))
+
+    def run(self, orders, merge_w=False, want_times=False):
+        """One iteration.  orders[i] = [(kind, mb), ...] for every stage i (only
+        local stages are executed here).  Returns IterResult with local stats."""
+        lib = L.lib()
+        self.epoch += 1
+        flags = L.MERGE_W if merge_w else 0
+        keep = []
+        for i in self.local:
+            arr = _op_array(orders[i])
+            keep.append(arr)
+            L.check(lib.adaptra_run_iteration(self.execs[i], arr, len(orders[i]), self.epoch, flags))
+        errs = []
+        for i in self.local:
+            rc = lib.adaptra_exec_join(self.execs[i])
+            if rc != L.OK:
+                errs.append((i, rc, lib.adaptra_last_error().decode()))
+        if errs:
+            self.abort()
+            raise L.AdaptraError(errs[0][1], f"stage {errs[0][0]}: {errs[0][2]}")
+        stats = {}
+        for i in self.local:
+            s = L.IterStats()
+            n = len(orders[i])
+            times = (C.c_int64 * (2 * max(1, n)))()
+            rc = lib.adaptra_exec_wait(self.execs[i], C.byref(s), times)
+            if rc != L.OK:
+                msg = lib.adaptra_last_error().decode()
+                self.abort()
+                raise L.AdaptraError(rc, f"stage {i}: {msg}")
+            st = {"busy_ns": s.busy_ns, "first_start_ns": s.first_start_ns, "last_end_ns": s.last_end_ns,
+                  "op_ns": list(s.op_ns), "op_cnt": list(s.op_cnt), "host_enqueue_ns": s.host_enqueue_ns}
+            if want_times:
+                st["op_times"] = [(times[2 * q], times[2 * q + 1]) for q in range(n)]
+            stats[i] = st
+        loss = float(self.loss.item()) if self.S - 1 in self.stages else None
+        return IterResult(self.epoch, stats, loss)
+
+    def abort(self):
+        """Release every GPU-side wait of this rank (after a failure)."""
+        lib = L.lib()
+        for h in list(self.in_fwd.values()) + list(self.in_bwd.values()):
+            lib.adaptra_inbox_poison(h)
+        try:
+            torch.cuda.synchronize(self.dev)
+        except Exception:
+            pass
+
+    def zero_grads(self):
+        for i in self.local:
+            self.stages[i].zero_grads(self.streams[i])
+        torch.cuda.synchronize(self.dev)
+
+    def link_stats(self):
+        out = {}
+        lib = L.lib()
+        for name, boxes in (("fwd", self.out_fwd), ("bwd", self.out_bwd)):
+            for i, h in boxes.items():
+                n, s, m = C.c_int64(), C.c_int64(), C.c_int64()
+                L.check(lib.adaptra_link_stats(h, C.byref(n), C.byref(s), C.byref(m)))
+                out[(name, i)] = (n.value, s.value, m.value)
+        return out
+
+    def close(self):
+        lib = L.lib()
+        for h in self.execs.values():
+            lib.adaptra_exec_destroy(h)
+        self.execs = {}
+        torch.cuda.synchronize(self.dev)
+        for h in list(self.out_fwd.values()) + list(self.out_bwd.values()):
+            lib.adaptra_outbox_close(h)
+        self.out_fwd, self.out_bwd = {}, {}
+        self._barrier()
+        for h in list(self.in_fwd.values()) + list(self.in_bwd.values()):
+            lib.adaptra_inbox_destroy(h)
+        self.in_fwd, self.in_bwd = {}, {}
+        for st in self.stages.values():
+            st.close()
+
+
+# ---------------------------------------------------------------- schedules
+def orders_from(X):
+    return [[(k, mb) for (k, mb, _s, _e) in ops] for ops in X]
+
+
+class Arm:
+    """Schedule policy for one arm (R18 / R21)."""
+
+    def __init__(self, name, S, N, tF, tB, tW, *, x_init=None, ratio=30, x_cap=None):
+        self.name, self.S, self.N = name, S, N
+        self.tF, self.tB, self.tW = list(tF), list(tB), list(tW)
+        self.delta = max(1, max(max(tF), max(tB), max(tW)) // ratio)
+        self.merge_w = name == "1f1b"
+        self.x_cap = x_cap
+        zero = [0] * (S - 1)
+        if name == "1f1b":
+            x = [min(S - i, N) for i in range(S)]
+            X, _, _ = cs.schedule(S, N, tF, tB, tW, zero, x, self.delta, mode="cap", merge_w=True)
+        elif name == "zb":
+            x = cs.plan_adapt(S, N, tF, tB, zero)
+            X, _, _ = cs.schedule(S, N, tF, tB, tW, zero, x, self.delta)
+        elif name == "adaptive":
+            x = list(x_init) if x_init else cs.plan_adapt(S, N, tF, tB, zero)
+            self.x_init = list(x)
+            X, _, _ = cs.schedule(S, N, tF, tB, tW, zero, x, self.delta)
+        else:
+            raise ValueError(name)
+        self.x = x
+        self.orders = orders_from(X)
+        self.c = zero
+        self.replans = 0
+
+    def _clamp(self, x):
+        if not self.x_cap:
+            return x
+        out = [min(v, cap) for v, cap in zip(x, self.x_cap)]
+        for i in range(len(out) - 2, -1, -1):          # keep the Lemma after clamping
+            out[i] = max(out[i], out[i + 1])
+        return out
+
+    def plan(self, c):
+        """Orders for the next iteration given the link latencies c (ns, finite)."""
+        if self.name != "adaptive" or list(c) == list(self.c):
+            return self.orders
+        S, N = self.S, self.N
+        if all(v == 0 for v in c):
+            x = list(self.x_init)
+        elif not all(cs.eq1_holds(self.tF, self.tB, c, self.x)):
+            x = self._clamp(cs.plan_adapt(S, N, self.tF, self.tB, c))
+        else:
+            x = list(self.x)
+        X, _, _ = cs.schedule(S, N, self.tF, self.tB, self.tW, c, x, self.delta)
+        if x != self.x:
+            self.replans += 1
+        self.x, self.c = x, list(c)
+        self.orders = orders_from(X)
+        return self.orders

@@ -22,7 +22,7 @@ TORCH_DT = {L.F32: torch.float32, L.BF16: torch.bfloat16}
 
 class Stage:
     def __init__(self, block, dtype, n_layers, d, d_ff, n_heads, b, T, is_first, is_last, n_microbatches,
-                 n_slots, device):
+                 n_slots, device, n_slots_fb=None):
         self.block, self.dtype = block, dtype
         self.n_layers, self.d, self.d_ff, self.n_heads, self.b, self.T = n_layers, d, d_ff, n_heads, b, T
         self.is_first, self.is_last = is_first, is_last
@@ -33,24 +33,29 @@ class Stage:
         desc.n_layers, desc.d, desc.d_ff, desc.n_heads = n_layers, d, d_ff, n_heads
         desc.b, desc.T, desc.is_first, desc.is_last = b, T, int(is_first), int(is_last)
         desc.n_microbatches, desc.n_slots = n_microbatches, n_slots
+        desc.n_slots_fb = n_slots_fb or n_slots
         lib = L.lib()
         nw = lib.adaptra_stage_wts_elems(C.byref(desc))
         nv = lib.adaptra_stage_vecs_elems(C.byref(desc))
         sb = lib.adaptra_stage_slot_bytes(C.byref(desc))
         wb = lib.adaptra_stage_work_bytes(C.byref(desc))
-        if sb < 0 or wb < 0:
+        fb = lib.adaptra_stage_slot_fb_bytes(C.byref(desc))
+        if sb < 0 or wb < 0 or fb < 0:
             L.check(L.EINVAL)
-        self.slot_bytes, self.work_bytes = sb, wb
+        self.slot_bytes, self.work_bytes, self.slot_fb_bytes = sb, wb, fb
+        self.n_slots, self.n_slots_fb = n_slots, desc.n_slots_fb
         dev = self.device
         self.wts = torch.zeros(nw, dtype=self.tdt, device=dev)
         self.vecs = torch.zeros(nv, dtype=torch.float32, device=dev)
         self.gwts = torch.zeros(nw, dtype=torch.float32, device=dev)
         self.gvecs = torch.zeros(nv, dtype=torch.float32, device=dev)
         self.stash = torch.empty(n_slots * sb, dtype=torch.uint8, device=dev)
+        self.stash_fb = torch.empty(desc.n_slots_fb * fb, dtype=torch.uint8, device=dev)
         self.work = torch.empty(max(wb, 256), dtype=torch.uint8, device=dev)
         desc.wts, desc.vecs = self.wts.data_ptr(), self.vecs.data_ptr()
         desc.gwts, desc.gvecs = self.gwts.data_ptr(), self.gvecs.data_ptr()
         desc.stash, desc.work = self.stash.data_ptr(), self.work.data_ptr()
+        desc.stash_fb = self.stash_fb.data_ptr()
         self.desc = desc
         h = C.c_void_p()
         L.check(lib.adaptra_stage_create(C.byref(desc), C.byref(h)))

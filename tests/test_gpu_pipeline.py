@@ -1,0 +1,103 @@
+"""Whole pipelined iteration (all stages co-located on cuda:0, one executor
+thread per stage, mailboxes + flags, latency gate, delegated host path) vs
+the oracle's unpipelined full-batch loss and gradients (P12), for every arm."""
+import time
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import numerics as nu
+import synthetic as sy
+from paper_2504_19232_b200 import _lib as L
+from paper_2504_19232_b200.pipeline import Arm, ModelCfg, Pipeline
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30))
+
+
+def _setup(kind, dtype, S, N, Lt, d, dff, H, b, T, **kw):
+    bf = dtype == L.BF16
+    Ls = Lt // S
+    params = (sy.mlp_params(0, S, Ls, d, dff, bf16=bf) if kind == "mlp"
+              else sy.gpt_params(0, S, Ls, d, dff, perturb=True, bf16=bf))
+    xs = sy.microbatches(1, N, b, T, d, bf16=bf)
+    tg = sy.targets(2, N, b, T, d)
+    m = ModelCfg(block=kind, n_layers=Lt, d=d, d_ff=dff, n_heads=H or 1, b=b, T=T, dtype=dtype)
+    pipe = Pipeline(m, S, N, params=params, inputs=xs, targets=tg, **kw)
+    Lref, gref, _ = nu.full_batch(kind, params, xs, tg, H)
+    return pipe, Lref, gref
+
+
+def _check(pipe, res, Lref, gref, tol):
+    assert abs(res.loss - Lref) <= tol * abs(Lref), (res.loss, Lref)
+    for i, st in pipe.stages.items():
+        got = st.grads()
+        for l in range(len(got)):
+            for k in gref[i][l]:
+                e = rel(got[l][k], gref[i][l][k])
+                assert e < tol, (i, l, k, e)
+
+
+CFGS = [
+    # C0 (S=4, N=8, 2-layer MLP per stage hidden=64, fp32)
+    ("mlp", L.F32, 4, 8, 4, 64, 64, None, 1, 32, 1e-4),
+    ("gpt", L.BF16, 2, 4, 4, 256, 1024, 2, 1, 128, 2e-2),
+]
+
+
+@pytest.mark.parametrize("arm", ["1f1b", "zb", "adaptive"])
+@pytest.mark.parametrize("kind,dtype,S,N,Lt,d,dff,H,b,T,tol", CFGS)
+def test_pipeline_iteration_matches_full_batch(kind, dtype, S, N, Lt, d, dff, H, b, T, tol, arm):
+    pipe, Lref, gref = _setup(kind, dtype, S, N, Lt, d, dff, H, b, T)
+    try:
+        t = [1000] * S
+        a = Arm(arm, S, N, t, t, t)
+        c = [0] * (S - 1)
+        if arm == "adaptive":
+            c[S // 2 - 1] = 2_000_000       # 2 ms injected on one link
+            pipe.set_latency(S // 2 - 1, c[S // 2 - 1])
+        orders = a.plan(c)
+        for _ in range(2):                  # twice: epochs / mailbox reuse / zeroed grads
+            res = pipe.run(orders, merge_w=a.merge_w, want_times=True)
+        _check(pipe, res, Lref, gref, tol)
+        for i, st in res.stats.items():
+            assert st["op_cnt"][0] == N
+            times = st["op_times"]
+            assert all(times[q][0] >= times[q - 1][1] - 1000 for q in range(1, len(times)))
+    finally:
+        pipe.close()
+
+
+@pytest.mark.parametrize("mode", [L.LINK_DIRECT, L.LINK_P2P])
+def test_latency_injection_and_link_down(mode):
+    S, N = 4, 8
+    pipe, Lref, gref = _setup("mlp", L.F32, S, N, 4, 64, 64, None, 1, 32, link_mode=mode)
+    try:
+        t = [1000] * S
+        a = Arm("zb", S, N, t, t, t)
+        orders = a.plan([0] * (S - 1))
+        base = pipe.run(orders, want_times=True)
+        # 5 ms on link 1: stage 2's first F cannot start before stage 1's first F ends + 5 ms
+        pipe.set_latency(1, 5_000_000)
+        res = pipe.run(orders, want_times=True)
+        f1_end = res.stats[1]["op_times"][0][1]
+        f2_start = res.stats[2]["op_times"][0][0]
+        assert f2_start - f1_end >= 4_900_000, (f1_end, f2_start)
+        _check(pipe, res, Lref, gref, 1e-4)
+        n, s, m = pipe.link_stats()[("fwd", 1)]
+        assert n >= N and s / n >= 4_900_000
+        # link 1 fails: traffic moves to the delegated host path, results unchanged
+        pipe.set_latency(1, L.LINK_DOWN)
+        res = pipe.run(orders)
+        _check(pipe, res, Lref, gref, 1e-4)
+        pipe.set_latency(1, 0)
+        res = pipe.run(orders)
+        _check(pipe, res, Lref, gref, 1e-4)
+    finally:
+        pipe.close()
