@@ -261,6 +261,11 @@ int adaptra_stage_zero_grads(adaptra_stage_t s, void* stream);
  *            HOST: D2H into the host ring).
  *   send     enqueues the transfer on the outbox's own stream after the
  *            producing op (never on the compute stream) and posts the flag.
+ * Waiting is a one-thread kernel on the consumer stream polling the flag with
+ * acquire loads, bounded by $ADAPTRA_TIMEOUT_MS (default 120 s); posting is a
+ * one-thread release-store kernel after a system fence.  (Stream memory ops
+ * are not used: on this driver a launch behind an unsatisfied stream wait
+ * blocks the host.)
  * Latency injection (R16): with latency c > 0 the flag of each message is
  * posted c ns after its data is in place, by a process-wide gate thread that
  * polls the completion event (no SM use, messages pipeline).  Latency
@@ -287,7 +292,7 @@ void* adaptra_inbox_slot(adaptra_inbox_t ib, int32_t mb);
  * no SM) until message mb of iteration epoch is in the mailbox; the slot
  * address is returned in slot_out. */
 int adaptra_recv(adaptra_inbox_t ib, int32_t mb, uint32_t epoch, void* consumer, void** slot_out);
-/* Abort path: set every flag to 0xFFFFFFFF so that all waiters proceed
+/* Abort path: set every flag to 0x3F3F3F3F (>= any epoch) so that all waiters proceed
  * (after a failed or timed-out iteration); adaptra_inbox_reset clears flags
  * (and host flags) back to 0 before epochs restart at 1. */
 int adaptra_inbox_poison(adaptra_inbox_t ib);

@@ -9,6 +9,10 @@ import os
 # Streams that block on stream memory waits must not share a hardware channel
 # with the streams that release them: give every stream its own connection.
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# Load all kernels when the context is created: a kernel loaded lazily while a
+# flag-wait kernel spins on the device can stall behind it (must be set before
+# the CUDA driver initialises; bench.py and tests/conftest.py set it first).
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
 from . import _lib  # noqa: E402,F401
 

@@ -3,8 +3,8 @@
 // delegated path), the latency gate thread (injected c_i, R16) and the
 // delegate thread of the host path.
 //
-// GPU-side synchronisation uses stream memory operations only
-// (cuStreamWaitValue32 / cuStreamWriteValue32): no spinning kernels, no SM use.
+// GPU-side synchronisation: a one-thread bounded wait kernel on the consumer
+// stream and a one-thread release-store signal kernel (csrc/comm/flags.cu).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <fcntl.h>
@@ -31,45 +31,6 @@
 
 namespace adaptra {
 
-// ------------------------------------------------------------ driver entry points
-typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-
-static PFN_waitValue32 p_wait = nullptr;
-static PFN_writeValue32 p_write = nullptr;
-static std::once_flag g_memop_once;
-
-static int memops() {
-  std::call_once(g_memop_once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      p_wait = (PFN_waitValue32)p;
-    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      p_write = (PFN_writeValue32)p;
-  });
-  if (!p_wait || !p_write) return set_error(ADAPTRA_ECUDA, "stream memory operations unavailable");
-  return ADAPTRA_OK;
-}
-
-int stream_wait_geq(cudaStream_t st, const uint32_t* addr, uint32_t v) {
-  int rc = memops();
-  if (rc) return rc;
-  CUresult r = p_wait((CUstream)st, (CUdeviceptr)addr, v, CU_STREAM_WAIT_VALUE_GEQ);
-  if (r != CUDA_SUCCESS) return set_error(ADAPTRA_ECUDA, "cuStreamWaitValue32 failed: " + std::to_string((int)r));
-  return ADAPTRA_OK;
-}
-
-int stream_write(cudaStream_t st, uint32_t* addr, uint32_t v) {
-  int rc = memops();
-  if (rc) return rc;
-  CUresult r = p_write((CUstream)st, (CUdeviceptr)addr, v, CU_STREAM_WRITE_VALUE_DEFAULT);
-  if (r != CUDA_SUCCESS) return set_error(ADAPTRA_ECUDA, "cuStreamWriteValue32 failed: " + std::to_string((int)r));
-  return ADAPTRA_OK;
-}
-
 // One stream per device for gate-issued flag writes: it never waits on
 // anything, so it cannot be held behind a blocked stream wait.
 cudaStream_t signal_stream(int dev) {
@@ -93,8 +54,8 @@ int64_t now_ns() {
 
 // ------------------------------------------------------------ gate thread
 // Pending items wait for their CUDA event; on completion (observed at t) the
-// action runs at t + delay.  Actions only enqueue stream memops or store host
-// flags, so they never block.
+// action runs at t + delay.  Actions only launch a signal kernel on the
+// device's signal stream (which never waits) or store a host flag.
 struct GateItem {
   cudaEvent_t ev;
   int64_t delay;
@@ -394,7 +355,8 @@ extern "C" int adaptra_inbox_poison(adaptra_inbox_t ib) {
   if (!ib) return set_error(ADAPTRA_EINVAL, "inbox_poison: null");
   cudaSetDevice(ib->dev);
   // release every waiter (abort path after a failed or timed-out iteration)
-  ADAPTRA_CUDA_TRY(cudaMemsetAsync(ib->flags, 0xFF, (size_t)ib->n_mb * 4, signal_stream(ib->dev)));
+  // 0x3F3F3F3F compares >= every epoch in use (wrap-around compare)
+  ADAPTRA_CUDA_TRY(cudaMemsetAsync(ib->flags, 0x3F, (size_t)ib->n_mb * 4, signal_stream(ib->dev)));
   return ADAPTRA_OK;
 }
 
@@ -562,7 +524,8 @@ extern "C" int adaptra_send(adaptra_outbox_t ob, int32_t mb, void* producer, uin
     }
     if (lat == 0) {
       // no injected latency: post the flag right behind the producer (DIRECT)
-      // or behind the copy (P2P), on the same stream
+      // or behind the copy (P2P), on the same stream (stream order puts it
+      // after the data stores)
       return stream_write(mode == ADAPTRA_LINK_P2P ? ob->lstream : (cudaStream_t)producer, flag, epoch);
     }
     cudaStream_t fs = signal_stream(ob->dev);

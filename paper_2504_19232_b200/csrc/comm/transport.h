@@ -8,4 +8,5 @@ int stream_wait_geq(cudaStream_t st, const uint32_t* addr, uint32_t v);
 int stream_write(cudaStream_t st, uint32_t* addr, uint32_t v);
 int64_t now_ns();
 cudaStream_t signal_stream(int dev);
+int wait_timed_out(int dev);
 }  // namespace adaptra

@@ -9,6 +9,7 @@
 
 #include <chrono>
 #include <condition_variable>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -25,6 +26,16 @@ int stage_device(adaptra_stage_t s);
 }  // namespace adaptra
 
 using namespace adaptra;
+
+static const bool g_dbg = getenv("ADAPTRA_DEBUG") != nullptr;
+#define DBG(...)                                  \
+  do {                                            \
+    if (g_dbg) {                                  \
+      fprintf(stderr, "[exec %d] ", d.stage_index); \
+      fprintf(stderr, __VA_ARGS__);               \
+      fprintf(stderr, "\n");                      \
+    }                                             \
+  } while (0)
 
 struct adaptra_exec {
   adaptra_exec_desc_t d{};
@@ -54,10 +65,24 @@ struct adaptra_exec {
     ADAPTRA_CUDA_TRY(cudaEventRecord(ev_t0, cs));
     if (i == S - 1 && d.loss_acc) ADAPTRA_CUDA_TRY(cudaMemsetAsync(d.loss_acc, 0, sizeof(float), cs));
     int rc;
+    DBG("start epoch %u n_ops %zu", epoch, ops.size());
     if ((rc = adaptra_stage_zero_grads(d.stage, cs))) return rc;  // gradients of this iteration only
+    DBG("zeroed");
+    static const int lookahead = [] {
+      const char* v = getenv("ADAPTRA_LOOKAHEAD");
+      return v ? atoi(v) : 3;
+    }();
     for (size_t q = 0; q < ops.size(); ++q) {
       const adaptra_op_t& o = ops[q];
       const int mb = o.mb;
+      DBG("op %zu kind %d mb %d", q, o.kind, o.mb);
+      // bounded run-ahead: keep at most `lookahead` ops queued on the stream so
+      // the launch queue stays shallow (waits on this stage's own work only)
+      if ((int)q >= lookahead) {
+        cudaEvent_t prev = ev_e[q - lookahead];
+        while (cudaEventQuery(prev) == cudaErrorNotReady) std::this_thread::sleep_for(std::chrono::microseconds(5));
+        cudaGetLastError();
+      }
       if (mb < 1 || mb > N) return set_error(ADAPTRA_EINVAL, "exec: bad microbatch");
       if (o.kind == ADAPTRA_OP_F) {
         if (free_slots.empty()) return set_error(ADAPTRA_ENOMEM, "exec: stash slots exhausted (plan needs more)");
@@ -74,9 +99,11 @@ struct adaptra_exec {
         }
         void* y = (i < S - 1) ? adaptra_outbox_dst(d.out_fwd, mb - 1) : nullptr;
         ADAPTRA_CUDA_TRY(cudaEventRecord(ev_s[q], cs));
+        DBG("  F recv done x=%p y=%p", x, y);
         if ((rc = adaptra_stage_F(d.stage, slot, x, y, i == S - 1 ? d.targets[mb - 1] : nullptr,
                                   i == S - 1 ? d.loss_acc : nullptr, cs)))
           return rc;
+        DBG("  F launched");
         ADAPTRA_CUDA_TRY(cudaEventRecord(ev_e[q], cs));
         if (i < S - 1 && (rc = adaptra_send(d.out_fwd, mb - 1, cs, epoch))) return rc;
       } else if (o.kind == ADAPTRA_OP_B) {
@@ -86,7 +113,9 @@ struct adaptra_exec {
         if (i < S - 1 && (rc = adaptra_recv(d.in_bwd, mb - 1, epoch, cs, &dy))) return rc;
         void* dx = (i > 0) ? adaptra_outbox_dst(d.out_bwd, mb - 1) : nullptr;
         ADAPTRA_CUDA_TRY(cudaEventRecord(ev_s[q], cs));
+        DBG("  B recv done dy=%p dx=%p", dy, dx);
         if ((rc = adaptra_stage_B(d.stage, slot, dy, dx, cs))) return rc;
+        DBG("  B launched");
         if (merge) {
           if ((rc = adaptra_stage_W(d.stage, slot, cs))) return rc;
           free_slots.push_back(slot);
@@ -107,6 +136,7 @@ struct adaptra_exec {
       }
     }
     host_ns = now_ns() - t_start;
+    DBG("enqueued all");
     return ADAPTRA_OK;
   }
 
@@ -215,6 +245,7 @@ extern "C" int adaptra_exec_wait(adaptra_exec_t e, adaptra_iter_stats_t* st, int
     if (now_ns() - t0 > timeout_ns) return set_error(ADAPTRA_ELINK, "exec_wait: iteration timed out (message lost?)");
     std::this_thread::sleep_for(std::chrono::microseconds(20));
   }
+  if (wait_timed_out(e->dev)) return set_error(ADAPTRA_ELINK, "exec_wait: a message wait timed out on the GPU");
   adaptra_iter_stats_t s{};
   s.n_ops = (int64_t)e->ops.size();
   s.first_start_ns = INT64_MAX;

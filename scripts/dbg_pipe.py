@@ -1,4 +1,6 @@
 """Debug: smallest pipelines, printing progress (run on the GPU box)."""
+import os
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 import faulthandler
 import os
 import sys

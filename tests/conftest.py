@@ -1,6 +1,12 @@
 import os
 import sys
 
+# Before the CUDA driver initialises: load every kernel eagerly (a kernel
+# loaded lazily while a flag-wait kernel spins could stall behind it) and give
+# every stream its own hardware connection.
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
