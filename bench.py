@@ -219,6 +219,7 @@ def main():
         torch.cuda.synchronize()
         if prof:
             lib.adaptra_prof_enable(1)
+        n_launch0 = lib.adaptra_launch_count()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(timer)
@@ -249,7 +250,8 @@ def main():
         ms = e0.elapsed_time(e1)
         if prof:
             lib.adaptra_prof_enable(0)
-        g = gather({"ms": ms, "busy": busy_tot, "span": span_tot, "dev_busy": dev_busy,
+        n_launch = lib.adaptra_launch_count() - n_launch0
+        g = gather({"ms": ms, "busy": busy_tot, "span": span_tot, "dev_busy": dev_busy, "launches": n_launch,
                     "links": {str(k): v for k, v in pipe.link_stats().items()}})
         ms_max = max(x["ms"] for x in g)
         busy = sum(x["busy"] for x in g)
@@ -260,7 +262,8 @@ def main():
                # R15: utilisation bubble 1 - sum busy / (S T) with T the step time
                "bubble": 1.0 - busy / (S * ms_max * 1e6),
                "device_bubble": 1.0 - dbusy / (world * ms_max * 1e6),
-               "replans": arm.replans, "x_final": arm.x}
+               "replans": arm.replans, "x_final": arm.x,
+               "gpu_launches": sum(x["launches"] for x in g)}
         if losses:
             out["loss_last"] = losses[-1]
         return out
@@ -318,7 +321,7 @@ def main():
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"},
             "clocks": clocks,
             "e2e": e2e,
-            "gpu_launches": None,
+            "gpu_launches": head["gpu_launches"],
         }
         if not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline(model, S, N)

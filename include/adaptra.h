@@ -168,6 +168,8 @@ int adaptra_gemm(const adaptra_gemm_desc_t* g, void* stream);
  * algorithmic FLOPs (2MNK per batch, causal products counted at 1/2, R28) and
  * operand/result bytes, and forgets them. */
 int adaptra_prof_enable(int32_t on);
+/* Number of this library's kernel launches in this process so far. */
+int64_t adaptra_launch_count(void);
 int adaptra_prof_collect(int32_t kind, int64_t* n_launches, double* sum_ms, double* flops, double* bytes);
 
 /* ================================================================ stage compute

@@ -92,6 +92,7 @@ _SIGS = {
                                 _P(_i32)]),
     "adaptra_gemm": (_i32, [_P(GemmDesc), _vp]),
     "adaptra_prof_enable": (_i32, [_i32]),
+    "adaptra_launch_count": (_i64, []),
     "adaptra_prof_collect": (_i32, [_i32, _P(_i64), _P(C.c_double), _P(C.c_double), _P(C.c_double)]),
     "adaptra_stage_slot_bytes": (_i64, [_P(StageDesc)]),
     "adaptra_stage_slot_fb_bytes": (_i64, [_P(StageDesc)]),

@@ -9,10 +9,13 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <chrono>
 #include <mutex>
+#include <thread>
 #include <string>
 
 #include "../../../include/adaptra.h"
+#include "../prof.h"
 #include "../util.h"
 #include "transport.h"
 
@@ -74,10 +77,37 @@ static uint64_t wait_timeout_ns() {
   return t;
 }
 
+// Profiling-only mode (ADAPTRA_HOST_WAIT=1): the calling thread polls the
+// flag from the host instead of enqueueing a wait kernel.  ncu serialises all
+// launches, under which a device-side wait could only time out.
+static bool host_wait_mode() {
+  static const bool on = getenv("ADAPTRA_HOST_WAIT") != nullptr;
+  return on;
+}
+
+static int host_wait(const uint32_t* addr, uint32_t v) {
+  thread_local uint32_t* h = nullptr;
+  thread_local cudaStream_t s = nullptr;
+  if (!h) {
+    cudaHostAlloc((void**)&h, 64, cudaHostAllocDefault);
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  }
+  const uint64_t t0 = (uint64_t)now_ns();
+  for (;;) {
+    cudaMemcpyAsync(h, addr, 4, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    if ((int32_t)(*h - v) >= 0) return ADAPTRA_OK;
+    if ((uint64_t)now_ns() - t0 > wait_timeout_ns()) return set_error(ADAPTRA_ELINK, "host wait timed out");
+    std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+
 int stream_wait_geq(cudaStream_t st, const uint32_t* addr, uint32_t v) {
+  if (host_wait_mode()) return host_wait(addr, v);
   int dev = 0;
   cudaGetDevice(&dev);
   wait_flag_kernel<<<1, 1, 0, st>>>(addr, v, err_word(dev), wait_timeout_ns());
+  count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(ADAPTRA_ECUDA, std::string("wait_flag launch: ") + cudaGetErrorString(e));
   return ADAPTRA_OK;
@@ -85,6 +115,7 @@ int stream_wait_geq(cudaStream_t st, const uint32_t* addr, uint32_t v) {
 
 int stream_write(cudaStream_t st, uint32_t* addr, uint32_t v) {
   signal_flag_kernel<<<1, 1, 0, st>>>(addr, v);
+  count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(ADAPTRA_ECUDA, std::string("signal_flag launch: ") + cudaGetErrorString(e));
   return ADAPTRA_OK;

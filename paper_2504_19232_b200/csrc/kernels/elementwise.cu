@@ -8,6 +8,7 @@
 #include <string>
 
 #include "../../../include/adaptra.h"
+#include "../prof.h"
 #include "../util.h"
 #include "common.cuh"
 #include "kernels.h"
@@ -246,6 +247,7 @@ __global__ void copy16_kernel(const uint4* __restrict__ src, uint4* __restrict__
 
 // ================================================================ launchers
 static int launch_check(const char* what) {
+  count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(ADAPTRA_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
   return ADAPTRA_OK;

@@ -7,6 +7,7 @@
 #include <string>
 
 #include "../../../include/adaptra.h"
+#include "../prof.h"
 #include "../util.h"
 #include "common.cuh"
 #include "epilogue.cuh"
@@ -94,6 +95,7 @@ int gemm_simt(const adaptra_gemm_desc_t& g, cudaStream_t st) {
     gemm_simt_kernel<float><<<grid, 256, 0, st>>>(g);
   else
     gemm_simt_kernel<bf16><<<grid, 256, 0, st>>>(g);
+  count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(ADAPTRA_ECUDA, std::string("gemm_simt launch: ") + cudaGetErrorString(e));
   return ADAPTRA_OK;

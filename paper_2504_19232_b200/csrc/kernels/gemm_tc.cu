@@ -13,6 +13,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstring>
 #include <mutex>
 #include <string>
 
@@ -35,13 +36,33 @@ struct TcCfg {
   static constexpr int kBBytes = BN * BK * 2;  // 32 / 16 KB
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;     // two accumulators
-  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kEpiBytes = 4 * 2 * 4096;  // 4 epilogue warps x 2 staging buffers x 32x32 fp32
+  static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 struct TileInfo {
   int m_blocks, n_blocks, Z;
   int k_blocks;  // full K range in BK blocks
 };
+
+// TMA-store epilogue: batch offsets of C and of the GELU pre-activation output
+// (aux) as (row, col) coordinates of their 2-D tensor maps.
+struct EpiTma {
+  int on;
+  int c_r1, c_r2, c_q1, c_q2;
+  int x_r1, x_r2, x_q1, x_q2;
+};
+
+// 32 consecutive bf16 of one row (guarded tail) -> fp32
+__device__ __forceinline__ void ld_row32(const bf16* p, int n0, int N, bool vec, float* out) {
+  if (vec && n0 + 32 <= N) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) ld_bf16x8(p + j, out + j);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) out[j] = (n0 + j < N) ? __bfloat162float(p[j]) : 0.f;
+  }
+}
 
 __device__ __forceinline__ void tile_coords(int t, const TileInfo& ti, int& mb, int& nb, int& z) {
   mb = t % ti.m_blocks;
@@ -70,13 +91,15 @@ __device__ __forceinline__ bool tile_range(const adaptra_gemm_desc_t& g, const T
 template <int BN, int AMN, int BMN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const adaptra_gemm_desc_t g, const TileInfo ti, int vec_ok) {
+                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX,
+                   const adaptra_gemm_desc_t g, const TileInfo ti, int vec_ok, const EpiTma et) {
   using Cfg = TcCfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
   uint8_t* sB = smem + Cfg::kStages * Cfg::kABytes;
-  uint64_t* full = (uint64_t*)(smem + Cfg::kStages * Cfg::kStageBytes);
+  uint8_t* sEpi = smem + Cfg::kStages * Cfg::kStageBytes;
+  uint64_t* full = (uint64_t*)(smem + Cfg::kStages * Cfg::kStageBytes + Cfg::kEpiBytes);
   uint64_t* empty = full + Cfg::kStages;
   uint64_t* tfull = empty + Cfg::kStages;
   uint64_t* tempty = tfull + 2;
@@ -195,32 +218,130 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ===================== epilogue (warps 2..5) =====================
+    // TMEM -> registers (thread = row) -> fused epilogue -> 32x32 chunk staged
+    // in shared memory -> TMA store (or TMA reduce-add for the fp32 dW
+    // accumulation), double-buffered per warp; inputs of the chunk (residual,
+    // GeLU pre-activation, softmax probabilities) are loaded one chunk ahead.
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+    uint8_t* stg = sEpi + (warp - 2) * 8192;
+    int sbuf = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
+    const bool f32o = (g.epi == ADAPTRA_EPI_ACC_F32 || g.epi == ADAPTRA_EPI_STORE_F32);
+    const bool has_in = (g.epi == ADAPTRA_EPI_RESID || g.epi == ADAPTRA_EPI_DGELU || g.epi == ADAPTRA_EPI_DSOFTMAX);
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
       int mb, nb, z, kb0, kb1;
       tile_coords(t, ti, mb, nb, z);
       if (!tile_range<BN>(g, ti, mb, nb, kb0, kb1)) continue;
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
       EpiCtx e = make_epi<bf16>(g, z);
       const int m = mb * BM + quad * 32 + lane;
+      const bool row_ok = m < e.M;
+      const int z1 = z / g.zdiv, z2 = z % g.zdiv;
+      const int crow = z1 * et.c_r1 + z2 * et.c_r2 + mb * BM + quad * 32;
+      const int ccol = z1 * et.c_q1 + z2 * et.c_q2 + nb * BN;
+      const int xrow = z1 * et.x_r1 + z2 * et.x_r2 + mb * BM + quad * 32;
+      const int xcol = z1 * et.x_q1 + z2 * et.x_q2 + nb * BN;
+      const bf16* in_row = nullptr;
+      if (has_in && row_ok)
+        in_row = g.epi == ADAPTRA_EPI_RESID ? (const bf16*)e.R + (long)m * e.ldr
+                                            : (const bf16*)e.aux + (long)m * e.ldaux;
+      float nxt[32];
+      if (in_row) ld_row32(in_row + nb * BN, nb * BN, e.N, vec_ok, nxt);
+      const float Dm = (g.epi == ADAPTRA_EPI_DSOFTMAX && row_ok) ? e.rowv[m] : 0.f;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
+        const int n0 = nb * BN + c * 32;
         uint32_t r[32];
         tmem_ld32(tbase + c * 32, r);
+        float in[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) in[j] = nxt[j];
+        if (in_row && c + 1 < BN / 32 && n0 + 32 < e.N) ld_row32(in_row + n0 + 32, n0 + 32, e.N, vec_ok, nxt);
         tmem_ld_wait();
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        const int n0 = nb * BN + c * 32;
-        if (n0 >= e.N) break;
-        if (vec_ok && m < e.M && n0 + 32 <= e.N)
-          epi_row32_bf16_fast(e, m, n0, v);
-        else
-          epi_row<bf16, 32>(e, m, n0, v);
+        if (n0 >= e.N) continue;
+        if (!et.on) {
+          if (vec_ok && row_ok && n0 + 32 <= e.N)
+            epi_row32_bf16_fast(e, m, n0, v);
+          else
+            epi_row<bf16, 32>(e, m, n0, v);
+          continue;
+        }
+        float bv[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) bv[j] = 0.f;
+        if (e.bias && (g.epi == ADAPTRA_EPI_STORE || g.epi == ADAPTRA_EPI_GELU || g.epi == ADAPTRA_EPI_RESID)) {
+          if (vec_ok && n0 + 32 <= e.N) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              float4 b4 = *reinterpret_cast<const float4*>(e.bias + n0 + j);
+              bv[j] = b4.x; bv[j + 1] = b4.y; bv[j + 2] = b4.z; bv[j + 3] = b4.w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) bv[j] = (n0 + j < e.N) ? e.bias[n0 + j] : 0.f;
+          }
+        }
+        // wait until this staging buffer's previous TMA store has read it
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+        uint8_t* sb = stg + sbuf * 4096;
+        switch (g.epi) {
+          case ADAPTRA_EPI_STORE:
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = e.alpha * v[j] + bv[j];
+            break;
+          case ADAPTRA_EPI_GELU: {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += bv[j];
+            bf16* xs = (bf16*)(sb + 2048) + lane * 32;
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) st_bf16x8(xs + j, v + j);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = gelu_fast(__bfloat162float(__float2bfloat16_rn(v[j])));
+          } break;
+          case ADAPTRA_EPI_RESID:
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += bv[j] + in[j];
+            break;
+          case ADAPTRA_EPI_DGELU:
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] *= gelu_grad_fast(in[j]);
+            break;
+          case ADAPTRA_EPI_DSOFTMAX:
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = in[j] * (v[j] - Dm) * e.alpha;
+            break;
+          default:  // ACC_F32, STORE_F32
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] *= e.alpha;
+            break;
+        }
+        if (f32o) {
+          float* fs = (float*)sb + lane * 32;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(fs + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        } else {
+          bf16* cs = (bf16*)sb + lane * 32;
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) st_bf16x8(cs + j, v + j);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (g.epi == ADAPTRA_EPI_ACC_F32)
+            tma_reduce_add_2d(&tmC, sb, ccol + c * 32, crow);
+          else
+            tma_store_2d(&tmC, sb, ccol + c * 32, crow);
+          if (g.epi == ADAPTRA_EPI_GELU) tma_store_2d(&tmX, sb + 2048, xcol + c * 32, xrow);
+          bulk_commit();
+        }
+        sbuf ^= 1;
       }
       tc_fence_before();
       __syncwarp();
@@ -230,6 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) bulk_wait<0>();
   }
   tc_fence_before();
   __syncthreads();
@@ -256,17 +378,19 @@ static PFN_encodeTiled get_encode() {
   return fn;
 }
 
-// 2-D bf16 map over a [rows, cols] row-major matrix with leading dimension ld.
+// 2-D map over a [rows, cols] row-major matrix with leading dimension ld
+// (bf16 operands: SWIZZLE_128B boxes; epilogue outputs: unswizzled 32x32 boxes).
 static int make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_c,
-                    int box_r) {
+                    int box_r, bool f32 = false, bool swz = true) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return set_error(ADAPTRA_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * (f32 ? 4 : 2))};
   cuuint32_t box[2] = {(cuuint32_t)box_c, (cuuint32_t)box_r};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  CUresult r = enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(ADAPTRA_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return ADAPTRA_OK;
@@ -319,8 +443,47 @@ static int launch_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
                (g.c_1 % 8 == 0) && (g.c_2 % 8 == 0) && (g.aux_1 % 8 == 0) && (g.aux_2 % 8 == 0);
   int grid = n_tiles < num_sms() ? n_tiles : num_sms();
   if (grid < 1) return ADAPTRA_OK;
+  // TMA-store epilogue when C (and the GELU aux output) decompose into 2-D
+  // coordinates and live on this device (a peer mailbox is written with
+  // plain stores).
+  EpiTma et{};
+  CUtensorMap mc, mx;
+  memset(&mc, 0, sizeof(mc));
+  memset(&mx, 0, sizeof(mx));
+  {
+    const int64_t esz = f32out ? 4 : 2;
+    auto decomp = [&](int64_t o1, int64_t o2, int64_t ld, int& r1, int& r2, int& q1, int& q2, int64_t& rows,
+                      int64_t& cols) {
+      r1 = (int)(o1 / ld); q1 = (int)(o1 % ld);
+      r2 = (int)(o2 / ld); q2 = (int)(o2 % ld);
+      const int64_t z1m = (g.Z - 1) / g.zdiv, z2m = g.Z > 1 ? (g.zdiv - 1) : 0;
+      cols = z1m * q1 + z2m * q2 + g.N;
+      rows = z1m * r1 + z2m * r2 + g.M;
+      return cols <= ld || g.Z == 1;
+    };
+    bool ok = vec_ok && ((uintptr_t)g.C % 16 == 0) && (g.ldc * esz) % 16 == 0;
+    if (ok && g.epi == ADAPTRA_EPI_RESID) {
+      cudaPointerAttributes pa;
+      int dev = 0;
+      cudaGetDevice(&dev);
+      ok = cudaPointerGetAttributes(&pa, g.C) == cudaSuccess && pa.type == cudaMemoryTypeDevice && pa.device == dev;
+      cudaGetLastError();
+    }
+    int64_t rows = 0, cols = 0;
+    if (ok) ok = decomp(g.c_1, g.c_2, g.ldc, et.c_r1, et.c_r2, et.c_q1, et.c_q2, rows, cols);
+    if (ok) ok = make_map(&mc, g.C, rows, g.Z == 1 ? g.N : cols, g.ldc, 32, 32, f32out, false) == ADAPTRA_OK;
+    if (ok && g.epi == ADAPTRA_EPI_GELU) {
+      int64_t xr = 0, xc = 0;
+      ok = g.aux && ((uintptr_t)g.aux % 16 == 0) &&
+           decomp(g.aux_1, g.aux_2, g.ldaux, et.x_r1, et.x_r2, et.x_q1, et.x_q2, xr, xc) &&
+           make_map(&mx, g.aux, xr, g.Z == 1 ? g.N : xc, g.ldaux, 32, 32, false, false) == ADAPTRA_OK;
+    }
+    et.on = ok ? 1 : 0;
+    cudaGetLastError();
+  }
   void* pb = prof_on() ? prof_begin(st) : nullptr;
-  kern<<<grid, kThreads, Cfg::kSmem, st>>>(ma, mbm, g, ti, vec_ok);
+  kern<<<grid, kThreads, Cfg::kSmem, st>>>(ma, mbm, mc, mx, g, ti, vec_ok, et);
+  count_launch();
   if (pb) {
     // algorithmic FLOPs: 2MNK per batch; causal variants count the lower half (R28)
     double fl = 2.0 * g.M * (double)g.N * g.K * g.Z * (g.causal ? 0.5 : 1.0);

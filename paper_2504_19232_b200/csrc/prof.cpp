@@ -3,6 +3,7 @@
 // collect() sums durations and the algorithmic FLOPs of the launches.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -36,6 +37,10 @@ cudaEvent_t take() {
 
 bool prof_on() { return g_on; }
 
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(); }
+
 void* prof_begin(cudaStream_t st) {
   std::lock_guard<std::mutex> lk(g_mu);
   cudaEvent_t e = take();
@@ -52,6 +57,8 @@ void prof_end(void* begin, cudaStream_t st, int kind, double flops, double bytes
 }  // namespace adaptra
 
 using namespace adaptra;
+
+extern "C" int64_t adaptra_launch_count(void) { return (int64_t)launch_count(); }
 
 extern "C" int adaptra_prof_enable(int32_t on) {
   std::lock_guard<std::mutex> lk(g_mu);

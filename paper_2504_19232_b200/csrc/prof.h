@@ -4,6 +4,8 @@
 namespace adaptra {
 enum { PROF_GEMM_TC = 0, PROF_GEMM_SIMT = 1 };
 bool prof_on();
+void count_launch();
+long long launch_count();
 void* prof_begin(cudaStream_t st);
 void prof_end(void* begin, cudaStream_t st, int kind, double flops, double bytes);
 }  // namespace adaptra

@@ -165,6 +165,14 @@ class Pipeline:
         m = self.model
         g = torch.Generator(device=st.device).manual_seed(seed * 1000 + i)
         w = torch.randn(st.wts.numel(), device=st.device, generator=g) * 0.02
+        if m.block == "gpt":
+            D, F = m.d, m.d_ff
+            per = 3 * D * D + D * D + F * D + D * F
+            ro = 1.0 / (2.0 * m.n_layers) ** 0.5
+            for l in range(self.Ls):
+                o = l * per
+                w[o + 3 * D * D:o + 4 * D * D] *= ro                       # Wo
+                w[o + 4 * D * D + F * D:o + per] *= ro                     # W2
         st.wts.copy_(w.to(st.tdt))
         v = torch.zeros(st.vecs.numel(), device=st.device)
         if m.block == "gpt":
