@@ -1,11 +1,14 @@
 // tcgen05 / TMEM / TMA bf16 GEMM for sm_100a (stage F, B = dX and W = dW
 // contractions, and the batched attention products).
 //
-// Persistent warp-specialised kernel, one CTA per SM:
+// Persistent warp-specialised kernel, one CTA per SM (CG = 1) or one CTA pair
+// per 2 SMs (CG = 2, tcgen05 cta_group::2: a 256 x BN tile whose A rows and B
+// rows are split over the two CTAs' shared memory, MMA issued by the leader):
 //   warp 0      TMA producer (one elected lane) -> smem ring of kStages stages
 //   warp 1      TMEM allocator + MMA issuer (one elected lane, tcgen05.mma
-//               kind::f16, 128 x BN x 16 per instruction, fp32 accumulate)
-//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> fused epilogue -> HBM
+//               kind::f16, (128 CG) x BN x 16 per instruction, fp32 accumulate)
+//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> fused epilogue ->
+//               shared-memory staging -> TMA store / TMA reduce-add
 // Two TMEM accumulators (2 x BN columns) let the epilogue of tile t overlap
 // the main loop of tile t+1.  Operands may be K-major or MN-major (SWIZZLE_128B
 // canonical layouts, selected by the instruction descriptor's major bits), so
@@ -13,6 +16,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -29,15 +33,17 @@ constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one SWIZZLE_128B row
 constexpr int kThreads = 192;
 
-template <int BN>
+template <int CG, int BN>
 struct TcCfg {
-  static constexpr int kStages = (BN == 256) ? 4 : 6;
-  static constexpr int kABytes = BM * BK * 2;  // 16 KB
-  static constexpr int kBBytes = BN * BK * 2;  // 32 / 16 KB
+  static constexpr int kBRows = BN / CG;        // B rows held by each CTA
+  static constexpr int kStages = CG == 2 ? 6 : (BN == 256 ? 4 : 6);
+  static constexpr int kABytes = BM * BK * 2;    // 16 KB
+  static constexpr int kBBytes = kBRows * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kTmemCols = 2 * BN;     // two accumulators
+  static constexpr int kTmemCols = 2 * BN;       // two accumulators of 128 lanes x BN columns
   static constexpr int kEpiBytes = 4 * 2 * 4096;  // 4 epilogue warps x 2 staging buffers x 32x32 fp32
   static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int TM = BM * CG;             // tile rows
 };
 
 struct TileInfo {
@@ -72,28 +78,186 @@ __device__ __forceinline__ void tile_coords(int t, const TileInfo& ti, int& mb, 
 }
 
 // K-block range of a tile (causal variants restrict it), and whether it is skipped.
-template <int BN>
+template <int TM, int BN>
 __device__ __forceinline__ bool tile_range(const adaptra_gemm_desc_t& g, const TileInfo& ti, int mb, int nb,
                                            int& kb0, int& kb1) {
   kb0 = 0;
   kb1 = ti.k_blocks;
   if (g.causal == ADAPTRA_CAUSAL_TILE) {
-    if (nb * BN > mb * BM + BM - 1) return false;
+    if (nb * BN > mb * TM + TM - 1) return false;
   } else if (g.causal == ADAPTRA_CAUSAL_KEND) {
-    int kend = min(g.K, mb * BM + BM);
+    int kend = min(g.K, mb * TM + TM);
     kb1 = (kend + BK - 1) / BK;
   } else if (g.causal == ADAPTRA_CAUSAL_KSTART) {
-    kb0 = (mb * BM) / BK;
+    kb0 = (mb * TM) / BK;
   }
   return kb1 > kb0;
 }
 
-template <int BN, int AMN, int BMN>
+// ---------------------------------------------------------------- epilogue
+// Runs in warps 2..5 of every CTA.  Rows of this CTA: tile row0 + rank*128.
+template <int CG, int BN>
+__device__ __forceinline__ void epilogue_loop(const adaptra_gemm_desc_t& g, const TileInfo& ti, const EpiTma& et,
+                                              const CUtensorMap* tmC, const CUtensorMap* tmX, int vec_ok,
+                                              uint8_t* sEpi, uint32_t tmem_base, uint64_t* tfull, uint64_t* tempty,
+                                              int warp, int lane, int cid, int ncl, int rank) {
+  constexpr int TM = TcCfg<CG, BN>::TM;
+  const int n_tiles = ti.m_blocks * ti.n_blocks * ti.Z;
+  const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+  uint8_t* stg = sEpi + (warp - 2) * 8192;
+  int sbuf = 0;
+  int acc = 0;
+  uint32_t acc_phase = 0;
+  const bool f32o = (g.epi == ADAPTRA_EPI_ACC_F32 || g.epi == ADAPTRA_EPI_STORE_F32);
+  const bool has_in = (g.epi == ADAPTRA_EPI_RESID || g.epi == ADAPTRA_EPI_DGELU || g.epi == ADAPTRA_EPI_DSOFTMAX);
+  for (int t = cid; t < n_tiles; t += ncl) {
+    int mb, nb, z, kb0, kb1;
+    tile_coords(t, ti, mb, nb, z);
+    if (!tile_range<TM, BN>(g, ti, mb, nb, kb0, kb1)) continue;
+    EpiCtx e = make_epi<bf16>(g, z);
+    const int rbase = mb * TM + rank * BM + quad * 32;
+    const int m = rbase + lane;
+    const bool row_ok = m < e.M;
+    const int z1 = z / g.zdiv, z2 = z % g.zdiv;
+    const int crow = z1 * et.c_r1 + z2 * et.c_r2 + rbase;
+    const int ccol = z1 * et.c_q1 + z2 * et.c_q2 + nb * BN;
+    const int xrow = z1 * et.x_r1 + z2 * et.x_r2 + rbase;
+    const int xcol = z1 * et.x_q1 + z2 * et.x_q2 + nb * BN;
+    const bf16* in_row = nullptr;
+    if (has_in && row_ok)
+      in_row = g.epi == ADAPTRA_EPI_RESID ? (const bf16*)e.R + (long)m * e.ldr : (const bf16*)e.aux + (long)m * e.ldaux;
+    float nxt[32];
+    if (in_row) ld_row32(in_row + nb * BN, nb * BN, e.N, vec_ok, nxt);
+    const float Dm = (g.epi == ADAPTRA_EPI_DSOFTMAX && row_ok) ? e.rowv[m] : 0.f;
+    mbar_wait(&tfull[acc], acc_phase);
+    tc_fence_after();
+    const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
+    uint32_t r[32];
+    tmem_ld32(tbase, r);  // chunk 0; chunk c+1 is requested while chunk c is processed
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      const int n0 = nb * BN + c * 32;
+      tmem_ld_wait_regs(r);
+      float v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+      if (c + 1 < BN / 32) tmem_ld32(tbase + (c + 1) * 32, r);
+      float in[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) in[j] = nxt[j];
+      if (in_row && c + 1 < BN / 32 && n0 + 32 < e.N) ld_row32(in_row + n0 + 32, n0 + 32, e.N, vec_ok, nxt);
+      if (n0 >= e.N) continue;
+      if (et.on == 2) continue;  // diagnostic: accumulator drained, no epilogue work
+      if (!et.on) {
+        if (vec_ok && row_ok && n0 + 32 <= e.N)
+          epi_row32_bf16_fast(e, m, n0, v);
+        else
+          epi_row<bf16, 32>(e, m, n0, v);
+        continue;
+      }
+      float bv[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) bv[j] = 0.f;
+      if (e.bias && (g.epi == ADAPTRA_EPI_STORE || g.epi == ADAPTRA_EPI_GELU || g.epi == ADAPTRA_EPI_RESID)) {
+        if (vec_ok && n0 + 32 <= e.N) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            float4 b4 = *reinterpret_cast<const float4*>(e.bias + n0 + j);
+            bv[j] = b4.x; bv[j + 1] = b4.y; bv[j + 2] = b4.z; bv[j + 3] = b4.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) bv[j] = (n0 + j < e.N) ? e.bias[n0 + j] : 0.f;
+        }
+      }
+      // wait until this staging buffer's previous TMA store has read it
+      if (lane == 0) bulk_wait_read<1>();
+      __syncwarp();
+      uint8_t* sb = stg + sbuf * 4096;
+      switch (g.epi) {
+        case ADAPTRA_EPI_STORE:
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = e.alpha * v[j] + bv[j];
+          break;
+        case ADAPTRA_EPI_GELU: {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] += bv[j];
+          uint8_t* xrow = sb + 2048 + lane * 64;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) st_bf16x8((bf16*)(xrow + ((j ^ ((lane >> 1) & 3)) << 4)), v + 8 * j);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = gelu_fast(__bfloat162float(__float2bfloat16_rn(v[j])));
+        } break;
+        case ADAPTRA_EPI_RESID:
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] += bv[j] + in[j];
+          break;
+        case ADAPTRA_EPI_DGELU:
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] *= gelu_grad_fast(in[j]);
+          break;
+        case ADAPTRA_EPI_DSOFTMAX:
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = in[j] * (v[j] - Dm) * e.alpha;
+          break;
+        default:  // ACC_F32, STORE_F32
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] *= e.alpha;
+          break;
+      }
+      // staging layout = TMA SWIZZLE_128B (fp32, 128 B rows) / SWIZZLE_64B (bf16,
+      // 64 B rows): 16 B chunk k of row r at chunk k ^ f(r) -> conflict-free
+      if (f32o) {
+        uint8_t* frow = sb + lane * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<float4*>(frow + ((j ^ (lane & 7)) << 4)) =
+              make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      } else {
+        uint8_t* crow_s = sb + lane * 64;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) st_bf16x8((bf16*)(crow_s + ((j ^ ((lane >> 1) & 3)) << 4)), v + 8 * j);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (et.on == 3) {  // diagnostic: full epilogue except the TMA store itself
+        sbuf ^= 1;
+        continue;
+      }
+      if (lane == 0) {
+        if (g.epi == ADAPTRA_EPI_ACC_F32)
+          tma_reduce_add_2d(tmC, sb, ccol + c * 32, crow);
+        else
+          tma_store_2d(tmC, sb, ccol + c * 32, crow);
+        if (g.epi == ADAPTRA_EPI_GELU) tma_store_2d(tmX, sb + 2048, xcol + c * 32, xrow);
+        bulk_commit();
+      }
+      sbuf ^= 1;
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+      if (CG == 1)
+        mbar_arrive(&tempty[acc]);
+      else
+        mbar_arrive_remote(&tempty[acc], 0);  // the leader reuses the accumulator
+    }
+    if (++acc == 2) {
+      acc = 0;
+      acc_phase ^= 1;
+    }
+  }
+  if (lane == 0) bulk_wait<0>();
+}
+
+// ---------------------------------------------------------------- kernel
+template <int CG, int BN, int AMN, int BMN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX,
                    const adaptra_gemm_desc_t g, const TileInfo ti, int vec_ok, const EpiTma et) {
-  using Cfg = TcCfg<BN>;
+  using Cfg = TcCfg<CG, BN>;
+  constexpr int TM = Cfg::TM;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
@@ -107,6 +271,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
+  const int cid = CG == 2 ? blockIdx.x / 2 : blockIdx.x;
+  const int ncl = CG == 2 ? gridDim.x / 2 : gridDim.x;
   const int n_tiles = ti.m_blocks * ti.n_blocks * ti.Z;
 
   if (warp == 0 && lane == 0) {
@@ -118,13 +285,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4);
+      mbar_init(&tempty[s], 4 * CG);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, Cfg::kTmemCols);
+  if (warp == 1) {
+    if (CG == 1)
+      tmem_alloc(tmem_slot, Cfg::kTmemCols);
+    else
+      tmem_alloc2(tmem_slot, Cfg::kTmemCols);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -133,33 +308,50 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      for (int t = cid; t < n_tiles; t += ncl) {
         int mb, nb, z, kb0, kb1;
         tile_coords(t, ti, mb, nb, z);
-        if (!tile_range<BN>(g, ti, mb, nb, kb0, kb1)) continue;
+        if (!tile_range<TM, BN>(g, ti, mb, nb, kb0, kb1)) continue;
         const int z1 = z / g.zdiv, z2 = z % g.zdiv;
         const int a_r = (int)(z1 * g.a_row1 + z2 * g.a_row2), a_c = (int)(z1 * g.a_col1 + z2 * g.a_col2);
         const int b_r = (int)(z1 * g.b_row1 + z2 * g.b_row2), b_c = (int)(z1 * g.b_col1 + z2 * g.b_col2);
-        const int m0 = mb * BM, n0 = nb * BN;
+        const int m0 = mb * TM + rank * BM, n0 = nb * BN + rank * Cfg::kBRows;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes * CG);
           uint8_t* a_dst = sA + stage * Cfg::kABytes;
           uint8_t* b_dst = sB + stage * Cfg::kBBytes;
           const int k0 = kb * BK;
-          if (AMN == 0) {
-            tma_load_2d(a_dst, &tmA, &full[stage], a_c + k0, a_r + m0);
-          } else {
+          if (CG == 1) {
+            if (AMN == 0) {
+              tma_load_2d(a_dst, &tmA, &full[stage], a_c + k0, a_r + m0);
+            } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j)
-              tma_load_2d(a_dst + j * (BK * 128), &tmA, &full[stage], a_c + m0 + 64 * j, a_r + k0);
-          }
-          if (BMN == 0) {
-            tma_load_2d(b_dst, &tmB, &full[stage], b_c + k0, b_r + n0);
-          } else {
+              for (int j = 0; j < BM / 64; ++j)
+                tma_load_2d(a_dst + j * (BK * 128), &tmA, &full[stage], a_c + m0 + 64 * j, a_r + k0);
+            }
+            if (BMN == 0) {
+              tma_load_2d(b_dst, &tmB, &full[stage], b_c + k0, b_r + n0);
+            } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_2d(b_dst + j * (BK * 128), &tmB, &full[stage], b_c + n0 + 64 * j, b_r + k0);
+              for (int j = 0; j < Cfg::kBRows / 64; ++j)
+                tma_load_2d(b_dst + j * (BK * 128), &tmB, &full[stage], b_c + n0 + 64 * j, b_r + k0);
+            }
+          } else {
+            if (AMN == 0) {
+              tma_load_2d_2sm(a_dst, &tmA, &full[stage], a_c + k0, a_r + m0);
+            } else {
+#pragma unroll
+              for (int j = 0; j < BM / 64; ++j)
+                tma_load_2d_2sm(a_dst + j * (BK * 128), &tmA, &full[stage], a_c + m0 + 64 * j, a_r + k0);
+            }
+            if (BMN == 0) {
+              tma_load_2d_2sm(b_dst, &tmB, &full[stage], b_c + k0, b_r + n0);
+            } else {
+#pragma unroll
+              for (int j = 0; j < Cfg::kBRows / 64; ++j)
+                tma_load_2d_2sm(b_dst + j * (BK * 128), &tmB, &full[stage], b_c + n0 + 64 * j, b_r + k0);
+            }
           }
           if (++stage == Cfg::kStages) {
             stage = 0;
@@ -169,194 +361,81 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer =====================
+    // ===================== MMA issuer (leader CTA) =====================
     // Instruction descriptor, kind::f16: D f32 (bit 4), A bf16 (bits 7-9 = 1),
     // B bf16 (bits 10-12 = 1), A/B major (bits 15/16), N>>3 (17-22), M>>4 (24-28).
-    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)AMN << 15) | ((uint32_t)BMN << 16) |
-                           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-    int stage = 0;
-    uint32_t phase = 0;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-      int mb, nb, z, kb0, kb1;
-      tile_coords(t, ti, mb, nb, z);
-      if (!tile_range<BN>(g, ti, mb, nb, kb0, kb1)) continue;
-      mbar_wait(&tempty[acc], acc_phase ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait(&full[stage], phase);
+    if (rank == 0) {
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)AMN << 15) | ((uint32_t)BMN << 16) |
+                             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = cid; t < n_tiles; t += ncl) {
+        int mb, nb, z, kb0, kb1;
+        tile_coords(t, ti, mb, nb, z);
+        if (!tile_range<TM, BN>(g, ti, mb, nb, kb0, kb1)) continue;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t a_addr = smem_u32(sA + stage * Cfg::kABytes);
-          const uint32_t b_addr = smem_u32(sB + stage * Cfg::kBBytes);
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a_addr = smem_u32(sA + stage * Cfg::kABytes);
+            const uint32_t b_addr = smem_u32(sB + stage * Cfg::kBBytes);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            // K-major: advance 16 elements = 32 B inside the swizzled row; SBO = 8 rows x 128 B.
-            // MN-major: advance 16 K-rows = 2 KB; LBO = one 64-wide MN chunk (BK x 128 B), SBO = 8 rows.
-            uint64_t ad = AMN == 0 ? umma_desc_sw128(a_addr + k * 32, 16, 1024)
-                                   : umma_desc_sw128(a_addr + k * 2048, BK * 128, 1024);
-            uint64_t bd = BMN == 0 ? umma_desc_sw128(b_addr + k * 32, 16, 1024)
-                                   : umma_desc_sw128(b_addr + k * 2048, BK * 128, 1024);
-            tc_mma_f16(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < BK / 16; ++k) {
+              // K-major: advance 16 elements = 32 B inside the swizzled row; SBO = 8 rows x 128 B.
+              // MN-major: advance 16 K-rows = 2 KB; LBO = one 64-wide MN chunk (BK x 128 B), SBO = 8 rows.
+              uint64_t ad = AMN == 0 ? umma_desc_sw128(a_addr + k * 32, 16, 1024)
+                                     : umma_desc_sw128(a_addr + k * 2048, BK * 128, 1024);
+              uint64_t bd = BMN == 0 ? umma_desc_sw128(b_addr + k * 32, 16, 1024)
+                                     : umma_desc_sw128(b_addr + k * 2048, BK * 128, 1024);
+              if (CG == 1)
+                tc_mma_f16(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+              else
+                tc_mma_f16_2sm(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            }
+            if (CG == 1)
+              tc_commit(&empty[stage]);
+            else
+              tc_commit_2sm_mc(&empty[stage]);
           }
-          tc_commit(&empty[stage]);
+          __syncwarp();
+          if (++stage == Cfg::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (lane == 0) {
+          if (CG == 1)
+            tc_commit(&tfull[acc]);
+          else
+            tc_commit_2sm_mc(&tfull[acc]);
         }
         __syncwarp();
-        if (++stage == Cfg::kStages) {
-          stage = 0;
-          phase ^= 1;
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
         }
-      }
-      if (lane == 0) tc_commit(&tfull[acc]);
-      __syncwarp();
-      if (++acc == 2) {
-        acc = 0;
-        acc_phase ^= 1;
       }
     }
   } else {
-    // ===================== epilogue (warps 2..5) =====================
-    // TMEM -> registers (thread = row) -> fused epilogue -> 32x32 chunk staged
-    // in shared memory -> TMA store (or TMA reduce-add for the fp32 dW
-    // accumulation), double-buffered per warp; inputs of the chunk (residual,
-    // GeLU pre-activation, softmax probabilities) are loaded one chunk ahead.
-    const int quad = warp & 3;  // TMEM lane quadrant this warp may access
-    uint8_t* stg = sEpi + (warp - 2) * 8192;
-    int sbuf = 0;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    const bool f32o = (g.epi == ADAPTRA_EPI_ACC_F32 || g.epi == ADAPTRA_EPI_STORE_F32);
-    const bool has_in = (g.epi == ADAPTRA_EPI_RESID || g.epi == ADAPTRA_EPI_DGELU || g.epi == ADAPTRA_EPI_DSOFTMAX);
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-      int mb, nb, z, kb0, kb1;
-      tile_coords(t, ti, mb, nb, z);
-      if (!tile_range<BN>(g, ti, mb, nb, kb0, kb1)) continue;
-      EpiCtx e = make_epi<bf16>(g, z);
-      const int m = mb * BM + quad * 32 + lane;
-      const bool row_ok = m < e.M;
-      const int z1 = z / g.zdiv, z2 = z % g.zdiv;
-      const int crow = z1 * et.c_r1 + z2 * et.c_r2 + mb * BM + quad * 32;
-      const int ccol = z1 * et.c_q1 + z2 * et.c_q2 + nb * BN;
-      const int xrow = z1 * et.x_r1 + z2 * et.x_r2 + mb * BM + quad * 32;
-      const int xcol = z1 * et.x_q1 + z2 * et.x_q2 + nb * BN;
-      const bf16* in_row = nullptr;
-      if (has_in && row_ok)
-        in_row = g.epi == ADAPTRA_EPI_RESID ? (const bf16*)e.R + (long)m * e.ldr
-                                            : (const bf16*)e.aux + (long)m * e.ldaux;
-      float nxt[32];
-      if (in_row) ld_row32(in_row + nb * BN, nb * BN, e.N, vec_ok, nxt);
-      const float Dm = (g.epi == ADAPTRA_EPI_DSOFTMAX && row_ok) ? e.rowv[m] : 0.f;
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        const int n0 = nb * BN + c * 32;
-        uint32_t r[32];
-        tmem_ld32(tbase + c * 32, r);
-        float in[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) in[j] = nxt[j];
-        if (in_row && c + 1 < BN / 32 && n0 + 32 < e.N) ld_row32(in_row + n0 + 32, n0 + 32, e.N, vec_ok, nxt);
-        tmem_ld_wait();
-        float v[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        if (n0 >= e.N) continue;
-        if (!et.on) {
-          if (vec_ok && row_ok && n0 + 32 <= e.N)
-            epi_row32_bf16_fast(e, m, n0, v);
-          else
-            epi_row<bf16, 32>(e, m, n0, v);
-          continue;
-        }
-        float bv[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) bv[j] = 0.f;
-        if (e.bias && (g.epi == ADAPTRA_EPI_STORE || g.epi == ADAPTRA_EPI_GELU || g.epi == ADAPTRA_EPI_RESID)) {
-          if (vec_ok && n0 + 32 <= e.N) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              float4 b4 = *reinterpret_cast<const float4*>(e.bias + n0 + j);
-              bv[j] = b4.x; bv[j + 1] = b4.y; bv[j + 2] = b4.z; bv[j + 3] = b4.w;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) bv[j] = (n0 + j < e.N) ? e.bias[n0 + j] : 0.f;
-          }
-        }
-        // wait until this staging buffer's previous TMA store has read it
-        if (lane == 0) bulk_wait_read<1>();
-        __syncwarp();
-        uint8_t* sb = stg + sbuf * 4096;
-        switch (g.epi) {
-          case ADAPTRA_EPI_STORE:
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = e.alpha * v[j] + bv[j];
-            break;
-          case ADAPTRA_EPI_GELU: {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] += bv[j];
-            bf16* xs = (bf16*)(sb + 2048) + lane * 32;
-#pragma unroll
-            for (int j = 0; j < 32; j += 8) st_bf16x8(xs + j, v + j);
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = gelu_fast(__bfloat162float(__float2bfloat16_rn(v[j])));
-          } break;
-          case ADAPTRA_EPI_RESID:
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] += bv[j] + in[j];
-            break;
-          case ADAPTRA_EPI_DGELU:
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] *= gelu_grad_fast(in[j]);
-            break;
-          case ADAPTRA_EPI_DSOFTMAX:
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = in[j] * (v[j] - Dm) * e.alpha;
-            break;
-          default:  // ACC_F32, STORE_F32
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] *= e.alpha;
-            break;
-        }
-        if (f32o) {
-          float* fs = (float*)sb + lane * 32;
-#pragma unroll
-          for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(fs + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-        } else {
-          bf16* cs = (bf16*)sb + lane * 32;
-#pragma unroll
-          for (int j = 0; j < 32; j += 8) st_bf16x8(cs + j, v + j);
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          if (g.epi == ADAPTRA_EPI_ACC_F32)
-            tma_reduce_add_2d(&tmC, sb, ccol + c * 32, crow);
-          else
-            tma_store_2d(&tmC, sb, ccol + c * 32, crow);
-          if (g.epi == ADAPTRA_EPI_GELU) tma_store_2d(&tmX, sb + 2048, xcol + c * 32, xrow);
-          bulk_commit();
-        }
-        sbuf ^= 1;
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (++acc == 2) {
-        acc = 0;
-        acc_phase ^= 1;
-      }
-    }
-    if (lane == 0) bulk_wait<0>();
+    epilogue_loop<CG, BN>(g, ti, et, &tmC, &tmX, vec_ok, sEpi, tmem_base, tfull, tempty, warp, lane, cid, ncl, rank);
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc(tmem_base, Cfg::kTmemCols);
+  if (warp == 1) {
+    if (CG == 1)
+      tmem_dealloc(tmem_base, Cfg::kTmemCols);
+    else
+      tmem_dealloc2(tmem_base, Cfg::kTmemCols);
+  }
 }
 
 // ------------------------------------------------------------------ host side
@@ -381,7 +460,7 @@ static PFN_encodeTiled get_encode() {
 // 2-D map over a [rows, cols] row-major matrix with leading dimension ld
 // (bf16 operands: SWIZZLE_128B boxes; epilogue outputs: unswizzled 32x32 boxes).
 static int make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_c,
-                    int box_r, bool f32 = false, bool swz = true) {
+                    int box_r, bool f32 = false, int swz = 128) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return set_error(ADAPTRA_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
@@ -390,7 +469,9 @@ static int make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols
   cuuint32_t es[2] = {1, 1};
   CUresult r = enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                    const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   swz == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                              : (swz == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE),
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(ADAPTRA_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return ADAPTRA_OK;
@@ -407,9 +488,9 @@ static int num_sms() {
   return n;
 }
 
-template <int BN, int AMN, int BMN>
+template <int CG, int BN, int AMN, int BMN>
 static int launch_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
-  using Cfg = TcCfg<BN>;
+  using Cfg = TcCfg<CG, BN>;
   CUtensorMap ma, mbm;
   int rc;
   if (AMN == 0)
@@ -418,17 +499,17 @@ static int launch_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
     rc = make_map(&ma, g.A, g.a_rows, g.a_cols, g.lda, 64, BK);
   if (rc) return rc;
   if (BMN == 0)
-    rc = make_map(&mbm, g.B, g.b_rows, g.b_cols, g.ldb, BK, BN);
+    rc = make_map(&mbm, g.B, g.b_rows, g.b_cols, g.ldb, BK, Cfg::kBRows);
   else
     rc = make_map(&mbm, g.B, g.b_rows, g.b_cols, g.ldb, 64, BK);
   if (rc) return rc;
   TileInfo ti;
-  ti.m_blocks = (g.M + BM - 1) / BM;
+  ti.m_blocks = (g.M + Cfg::TM - 1) / Cfg::TM;
   ti.n_blocks = (g.N + BN - 1) / BN;
   ti.Z = g.Z;
   ti.k_blocks = (g.K + BK - 1) / BK;
   const int n_tiles = ti.m_blocks * ti.n_blocks * ti.Z;
-  auto kern = gemm_tc_kernel<BN, AMN, BMN>;
+  auto kern = gemm_tc_kernel<CG, BN, AMN, BMN>;
   static unsigned attr_mask = 0;  // per device
   int dev = 0;
   cudaGetDevice(&dev);
@@ -441,7 +522,8 @@ static int launch_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
                (!g.aux || (g.ldaux % 8 == 0 && (uintptr_t)g.aux % 16 == 0)) &&
                (!g.R || (g.ldr % 8 == 0 && (uintptr_t)g.R % 16 == 0)) && ((uintptr_t)g.bias % 16 == 0) &&
                (g.c_1 % 8 == 0) && (g.c_2 % 8 == 0) && (g.aux_1 % 8 == 0) && (g.aux_2 % 8 == 0);
-  int grid = n_tiles < num_sms() ? n_tiles : num_sms();
+  const int slots = num_sms() / CG;
+  int grid = (n_tiles < slots ? n_tiles : slots) * CG;
   if (grid < 1) return ADAPTRA_OK;
   // TMA-store epilogue when C (and the GELU aux output) decompose into 2-D
   // coordinates and live on this device (a peer mailbox is written with
@@ -471,18 +553,39 @@ static int launch_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
     }
     int64_t rows = 0, cols = 0;
     if (ok) ok = decomp(g.c_1, g.c_2, g.ldc, et.c_r1, et.c_r2, et.c_q1, et.c_q2, rows, cols);
-    if (ok) ok = make_map(&mc, g.C, rows, g.Z == 1 ? g.N : cols, g.ldc, 32, 32, f32out, false) == ADAPTRA_OK;
+    if (ok)
+      ok = make_map(&mc, g.C, rows, g.Z == 1 ? g.N : cols, g.ldc, 32, 32, f32out, f32out ? 128 : 64) == ADAPTRA_OK;
     if (ok && g.epi == ADAPTRA_EPI_GELU) {
       int64_t xr = 0, xc = 0;
       ok = g.aux && ((uintptr_t)g.aux % 16 == 0) &&
            decomp(g.aux_1, g.aux_2, g.ldaux, et.x_r1, et.x_r2, et.x_q1, et.x_q2, xr, xc) &&
-           make_map(&mx, g.aux, xr, g.Z == 1 ? g.N : xc, g.ldaux, 32, 32, false, false) == ADAPTRA_OK;
+           make_map(&mx, g.aux, xr, g.Z == 1 ? g.N : xc, g.ldaux, 32, 32, false, 64) == ADAPTRA_OK;
     }
     et.on = ok ? 1 : 0;
+    // timing experiments only: 1 = skip all epilogue work, 2 = skip the TMA store
+    static const int diag = getenv("ADAPTRA_DIAG_NOEPI") ? atoi(getenv("ADAPTRA_DIAG_NOEPI")) : 0;
+    if (diag == 1 && ok) et.on = 2;
+    if (diag == 2 && ok) et.on = 3;
     cudaGetLastError();
   }
   void* pb = prof_on() ? prof_begin(st) : nullptr;
-  kern<<<grid, kThreads, Cfg::kSmem, st>>>(ma, mbm, mc, mx, g, ti, vec_ok, et);
+  if (CG == 1) {
+    kern<<<grid, kThreads, Cfg::kSmem, st>>>(ma, mbm, mc, mx, g, ti, vec_ok, et);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Cfg::kSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, ma, mbm, mc, mx, g, ti, vec_ok, et);
+  }
   count_launch();
   if (pb) {
     // algorithmic FLOPs: 2MNK per batch; causal variants count the lower half (R28)
@@ -501,22 +604,36 @@ int gemm_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
   // cross a batch boundary: require tile-aligned extents when Z > 1).
   if (g.Z > 1 && (g.M % BM || g.K % BK)) return set_error(ADAPTRA_EINVAL, "batched tc gemm needs M%128==0, K%64==0");
   if ((g.lda * 2) % 16 || (g.ldb * 2) % 16) return set_error(ADAPTRA_EINVAL, "tc gemm needs 16B-aligned rows");
-  bool big = (g.Z == 1 && g.N >= 2048 && g.causal == ADAPTRA_CAUSAL_NONE);
   if (g.Z > 1 && g.N % 128) return set_error(ADAPTRA_EINVAL, "batched tc gemm needs N%128==0");
+  // Large unbatched products: CTA pair, 256 x 256 tiles (cta_group::2);
+  // otherwise (attention batches, small N) one CTA, 128 x 128 tiles.
+  static const int mode = [] {
+    const char* v = getenv("ADAPTRA_GEMM_PAIR");
+    return v ? atoi(v) : 1;
+  }();
+  const bool big = (g.Z == 1 && g.N >= 2048 && g.M >= 256 && g.causal == ADAPTRA_CAUSAL_NONE);
   const int key = g.a_mn * 2 + g.b_mn;
+  if (big && mode == 1) {
+    switch (key) {
+      case 0: return launch_tc<2, 256, 0, 0>(g, st);
+      case 1: return launch_tc<2, 256, 0, 1>(g, st);
+      case 2: return launch_tc<2, 256, 1, 0>(g, st);
+      default: return launch_tc<2, 256, 1, 1>(g, st);
+    }
+  }
   if (big) {
     switch (key) {
-      case 0: return launch_tc<256, 0, 0>(g, st);
-      case 1: return launch_tc<256, 0, 1>(g, st);
-      case 2: return launch_tc<256, 1, 0>(g, st);
-      default: return launch_tc<256, 1, 1>(g, st);
+      case 0: return launch_tc<1, 256, 0, 0>(g, st);
+      case 1: return launch_tc<1, 256, 0, 1>(g, st);
+      case 2: return launch_tc<1, 256, 1, 0>(g, st);
+      default: return launch_tc<1, 256, 1, 1>(g, st);
     }
   }
   switch (key) {
-    case 0: return launch_tc<128, 0, 0>(g, st);
-    case 1: return launch_tc<128, 0, 1>(g, st);
-    case 2: return launch_tc<128, 1, 0>(g, st);
-    default: return launch_tc<128, 1, 1>(g, st);
+    case 0: return launch_tc<1, 128, 0, 0>(g, st);
+    case 1: return launch_tc<1, 128, 0, 1>(g, st);
+    case 2: return launch_tc<1, 128, 1, 0>(g, st);
+    default: return launch_tc<1, 128, 1, 1>(g, st);
   }
 }
 

@@ -1,0 +1,70 @@
+"""Multi-process pipeline parity (launch with torchrun, one rank per GPU):
+every rank checks its own stages' gradients and the last stage's loss against
+the oracle's full-batch definition; exercises CUDA-IPC mailboxes over NVLink,
+latency injection and the delegated host path across processes."""
+import os
+import sys
+
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+os.environ.setdefault("ADAPTRA_TIMEOUT_MS", "30000")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from oracle import numerics as nu  # noqa: E402
+import synthetic as sy  # noqa: E402
+from paper_2504_19232_b200 import _lib as L  # noqa: E402
+from paper_2504_19232_b200.pipeline import Arm, ModelCfg, Pipeline  # noqa: E402
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    grp = dist.new_group(backend="gloo")
+    S = int(os.environ.get("S", 4))
+    N = int(os.environ.get("N", 8))
+    mode = int(os.environ.get("MODE", L.LINK_DIRECT))
+    d, dff, H, T, Lt = 256, 1024, 2, 128, S
+    params = sy.gpt_params(0, S, Lt // S, d, dff, perturb=True, bf16=True)
+    xs = sy.microbatches(1, N, 1, T, d, bf16=True)
+    tg = sy.targets(2, N, 1, T, d)
+    m = ModelCfg(block="gpt", n_layers=Lt, d=d, d_ff=dff, n_heads=H, b=1, T=T, dtype=L.BF16)
+    pipe = Pipeline(m, S, N, params=params, inputs=xs, targets=tg, rank=rank, world=world, device=local,
+                    group=grp, link_mode=mode)
+    Lref, gref, _ = nu.full_batch("gpt", params, xs, tg, H)
+    ok = True
+    t = [1000] * S
+    for arm_name, lat in (("zb", None), ("1f1b", None), ("adaptive", (1, 3_000_000)), ("zb", (1, L.LINK_DOWN))):
+        a = Arm(arm_name, S, N, t, t, t)
+        c = [0] * (S - 1)
+        for l in range(S - 1):
+            pipe.set_latency(l, 0)
+        if lat:
+            pipe.set_latency(lat[0], lat[1])
+            c[lat[0]] = lat[1] if lat[1] != L.LINK_DOWN else 500_000
+        dist.barrier(group=grp)
+        res = pipe.run(a.plan(c), merge_w=a.merge_w)
+        dist.barrier(group=grp)
+        worst = 0.0
+        for i, st in pipe.stages.items():
+            got = st.grads()
+            for l in range(len(got)):
+                for k, ref in gref[i][l].items():
+                    e = float(np.abs(got[l][k] - ref).max() / max(np.abs(ref).max(), 1e-30))
+                    worst = max(worst, e)
+        lerr = abs(res.loss - Lref) / abs(Lref) if res.loss is not None else 0.0
+        good = worst < 2e-2 and lerr < 2e-2
+        ok &= good
+        print(f"rank {rank} arm {arm_name} lat {lat}: worst grad err {worst:.2e} loss err {lerr:.2e} "
+              f"{'OK' if good else 'FAIL'}", flush=True)
+    pipe.close()
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()
