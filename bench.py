@@ -258,7 +258,11 @@ def main():
         dbusy = sum(x["dev_busy"] for x in g)
         span = max(x["span"] for x in g)
         toks = steps * N * model.tokens_per_mb
+        # algorithmic FLOPs per microbatch per block = 72 T d^2 + 6 T^2 d
+        Tt, dd = model.T, model.d
+        fl = steps * N * model.b * model.n_layers * (72.0 * Tt * dd * dd + 6.0 * Tt * Tt * dd)
         out = {"tokens_per_s": toks / (ms_max / 1e3), "ms_per_step": ms_max / steps,
+               "step_tflops": fl / (ms_max / 1e3) / 1e12,
                # R15: utilisation bubble 1 - sum busy / (S T) with T the step time
                "bubble": 1.0 - busy / (S * ms_max * 1e6),
                "device_bubble": 1.0 - dbusy / (world * ms_max * 1e6),
@@ -276,6 +280,8 @@ def main():
                              __import__("ctypes").c_double(), __import__("ctypes").c_double())
             lib.adaptra_prof_collect(0, n, ms, fl, by)
             gem = gather((n.value, ms.value, fl.value, by.value))
+            lib.adaptra_prof_collect(2, n, ms, fl, by)
+            gem_attn = gather((n.value, ms.value, fl.value, by.value))
         results[(name, "nominal")] = run_arm(name, False, max(3, args.steps // 2), 1)
     e2e = None
     if not args.no_e2e and "adaptive" in arms:
@@ -298,6 +304,13 @@ def main():
         fl_l = sum(x[2] for x in gem)
         avg_ms = ms_l / max(1, n_l)
         achieved = (fl_l / max(1, n_l)) / (avg_ms / 1e3) / 1e12 if n_l else None
+        na = sum(x[0] for x in gem_attn)
+        attn_line = None
+        if na:
+            ams = sum(x[1] for x in gem_attn) / na
+            afl = sum(x[2] for x in gem_attn) / na
+            attn_line = {"launches": na, "avg_launch_us": round(ams * 1e3, 2),
+                         "achieved_tflops": round(afl / (ams / 1e3) / 1e12, 1)}
         line = {
             "metric": "tokens/sec and bubble rate at 8 stages under injected straggler trace",
             "value": round(head["tokens_per_s"], 1), "unit": "tokens/s", "n_gpus": world,
@@ -305,6 +318,8 @@ def main():
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded N(0,1) inputs/targets, GPT-2 init weights)",
             "bubble_rate": round(head["bubble"], 4), "device_bubble_rate": round(head["device_bubble"], 4),
+            "step_tflops": round(head["step_tflops"], 1),
+            "step_tflops_frac_of_peak": round(head["step_tflops"] / peaks.get("bf16_tflops_sustained", 1400.0), 4),
             "config": {"workload": f"C1: GPT-style {args.layers}x(d={args.d},h={args.heads},ff={4 * args.d}) "
                                    f"S={S} N={N} seq={args.T} bf16, paper trace compressed 1 event/step",
                        "stages": S, "microbatches": N, "tokens_per_step": N * model.tokens_per_mb,
@@ -316,8 +331,12 @@ def main():
             "roofline": {"bound": "tensor", "achieved": round(achieved, 1) if achieved else None,
                          "peak": peak, "unit": "TFLOP/s",
                          "frac": round(achieved / peak, 4) if achieved else None, "traffic": None,
-                         "kernel": "gemm_tc_kernel (tcgen05)", "launches": n_l,
+                         "kernel": "gemm_tc_kernel (tcgen05), stage linear layers (Z=1)", "launches": n_l,
                          "avg_launch_us": round(avg_ms * 1e3, 2),
+                         "note": "per-launch CUDA-event durations on the launching stream during the timed "
+                                 "steps; stages co-located on one GPU run concurrently, which stretches each "
+                                 "launch (see profiles/ for serialised ncu shares)",
+                         "attention_gemm": attn_line,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"},
             "clocks": clocks,
             "e2e": e2e,

@@ -163,7 +163,8 @@ typedef struct adaptra_gemm_desc {
 int adaptra_gemm(const adaptra_gemm_desc_t* g, void* stream);
 
 /* Live kernel timing (bench roofline): when enabled, every tcgen05 GEMM launch
- * (kind 0) is bracketed by CUDA events on its own stream.  collect() waits for
+ * is bracketed by CUDA events on its own stream; kind 0 = the stage's linear
+ * layers (unbatched), kind 2 = the batched attention products.  collect() waits for
  * the recorded launches of `kind`, returns their count, summed duration (ms),
  * algorithmic FLOPs (2MNK per batch, causal products counted at 1/2, R28) and
  * operand/result bytes, and forgets them. */

@@ -592,7 +592,7 @@ static int launch_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
     double fl = 2.0 * g.M * (double)g.N * g.K * g.Z * (g.causal ? 0.5 : 1.0);
     bool f32o = (g.epi == ADAPTRA_EPI_ACC_F32 || g.epi == ADAPTRA_EPI_STORE_F32);
     double by = 2.0 * ((double)g.M * g.K + (double)g.N * g.K) * g.Z + (f32o ? 4.0 : 2.0) * g.M * (double)g.N * g.Z;
-    prof_end(pb, st, PROF_GEMM_TC, fl, by);
+    prof_end(pb, st, g.Z == 1 ? PROF_GEMM_TC : PROF_GEMM_ATTN, fl, by);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(ADAPTRA_ECUDA, std::string("gemm_tc launch: ") + cudaGetErrorString(e));
