@@ -171,6 +171,144 @@ __global__ void colsum_kernel(const T* __restrict__ y, const T* __restrict__ x, 
   }
 }
 
+// Register-resident variants (one warp per row, the row kept in registers:
+// V 8-element vectors per lane, d = 256 V): one HBM read of each input.
+template <typename T, int V>
+__global__ void __launch_bounds__(128) ln_fwd_reg_kernel(const T* __restrict__ x, const float* __restrict__ g,
+                                                         const float* __restrict__ b, T* __restrict__ h,
+                                                         float* __restrict__ mean_out, float* __restrict__ rstd_out,
+                                                         int R, int d) {
+  int row = blockIdx.x * 4 + threadIdx.x / 32;
+  int lane = threadIdx.x % 32;
+  if (row >= R) return;
+  const T* xr = x + (long)row * d;
+  float v[V][8];
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    load8(xr + k * 256 + lane * 8, v[k]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += v[k][j];
+  }
+  const float mu = warp_sum(s) / d;
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < V; ++k)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) q += (v[k][j] - mu) * (v[k][j] - mu);
+  const float rs = rsqrtf(warp_sum(q) / d + kLnEps);
+  T* hr = h + (long)row * d;
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const int c = k * 256 + lane * 8;
+    float gg[8], bb[8], o[8];
+    *reinterpret_cast<float4*>(gg) = *reinterpret_cast<const float4*>(g + c);
+    *reinterpret_cast<float4*>(gg + 4) = *reinterpret_cast<const float4*>(g + c + 4);
+    *reinterpret_cast<float4*>(bb) = *reinterpret_cast<const float4*>(b + c);
+    *reinterpret_cast<float4*>(bb + 4) = *reinterpret_cast<const float4*>(b + c + 4);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = (v[k][j] - mu) * rs * gg[j] + bb[j];
+    store8(hr + c, o);
+  }
+  if (lane == 0) {
+    mean_out[row] = mu;
+    rstd_out[row] = rs;
+  }
+}
+
+template <typename T, int V>
+__global__ void __launch_bounds__(128) ln_bwd_reg_kernel(const T* __restrict__ dh, const T* __restrict__ x,
+                                                         const float* __restrict__ mean, const float* __restrict__ rstd,
+                                                         const float* __restrict__ g, const T* __restrict__ dres,
+                                                         T* __restrict__ dx, int R, int d) {
+  int row = blockIdx.x * 4 + threadIdx.x / 32;
+  int lane = threadIdx.x % 32;
+  if (row >= R) return;
+  const float mu = mean[row], rs = rstd[row];
+  float gd[V][8], xh[V][8];
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const int c = k * 256 + lane * 8;
+    float a[8], gg[8];
+    load8(dh + (long)row * d + c, a);
+    load8(x + (long)row * d + c, xh[k]);
+    *reinterpret_cast<float4*>(gg) = *reinterpret_cast<const float4*>(g + c);
+    *reinterpret_cast<float4*>(gg + 4) = *reinterpret_cast<const float4*>(g + c + 4);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      gd[k][j] = a[j] * gg[j];
+      xh[k][j] = (xh[k][j] - mu) * rs;
+      s1 += gd[k][j];
+      s2 += gd[k][j] * xh[k][j];
+    }
+  }
+  s1 = warp_sum(s1) / d;
+  s2 = warp_sum(s2) / d;
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const int c = k * 256 + lane * 8;
+    float r[8], o[8];
+    load8(dres + (long)row * d + c, r);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = r[j] + rs * (gd[k][j] - s1 - xh[k][j] * s2);
+    store8(dx + (long)row * d + c, o);
+  }
+}
+
+// Column sums with 16 B loads: block = 256 threads over 64 columns x 256 rows
+// (8 column groups of 8 x 32 row lanes), shared-memory reduction, one
+// atomicAdd per column per block.  LN: out_a += dh * xhat, out_b += dh.
+template <typename T, bool LN>
+__global__ void __launch_bounds__(256) colsum_vec_kernel(const T* __restrict__ y, const T* __restrict__ x,
+                                                         const float* __restrict__ mean,
+                                                         const float* __restrict__ rstd, float* __restrict__ out_a,
+                                                         float* __restrict__ out_b, int R, int N) {
+  __shared__ float sa[32][65], sb[32][65];
+  const int cg = threadIdx.x & 7, rl = threadIdx.x >> 3;
+  const int c0 = blockIdx.x * 64 + cg * 8;
+  const int r0 = blockIdx.y * 256;
+  float a[8] = {}, bsum[8] = {};
+  if (c0 < N) {
+    for (int r = r0 + rl; r < min(R, r0 + 256); r += 32) {
+      float v[8];
+      load8(y + (long)r * N + c0, v);
+      if (LN) {
+        float xv[8];
+        load8(x + (long)r * N + c0, xv);
+        const float mu = mean[r], rs = rstd[r];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          a[j] += v[j] * (xv[j] - mu) * rs;
+          bsum[j] += v[j];
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[j] += v[j];
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    sa[rl][cg * 8 + j] = a[j];
+    if (LN) sb[rl][cg * 8 + j] = bsum[j];
+  }
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    const int c = blockIdx.x * 64 + threadIdx.x;
+    float ta = 0.f, tb = 0.f;
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) {
+      ta += sa[k][threadIdx.x];
+      if (LN) tb += sb[k][threadIdx.x];
+    }
+    if (c < N) {
+      atomicAdd(out_a + c, ta);
+      if (LN) atomicAdd(out_b + c, tb);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- attention
 // Row i of batch z: P[i, j] = exp(S[i, j] - max) / sum over j <= i; zeros for
 // i < j < roundup(i + 1, 128) so that tile-granular consumers read zeros.
@@ -255,28 +393,53 @@ static int launch_check(const char* what) {
 
 template <typename T>
 int ln_fwd(const T* x, const float* g, const float* b, T* h, float* mean, float* rstd, int R, int d, cudaStream_t st) {
-  ln_fwd_kernel<T><<<(R + 7) / 8, 256, 0, st>>>(x, g, b, h, mean, rstd, R, d);
+  const dim3 gr((R + 3) / 4);
+  switch (d % 256 ? 0 : d / 256) {
+    case 1: ln_fwd_reg_kernel<T, 1><<<gr, 128, 0, st>>>(x, g, b, h, mean, rstd, R, d); break;
+    case 2: ln_fwd_reg_kernel<T, 2><<<gr, 128, 0, st>>>(x, g, b, h, mean, rstd, R, d); break;
+    case 4: ln_fwd_reg_kernel<T, 4><<<gr, 128, 0, st>>>(x, g, b, h, mean, rstd, R, d); break;
+    case 8: ln_fwd_reg_kernel<T, 8><<<gr, 128, 0, st>>>(x, g, b, h, mean, rstd, R, d); break;
+    case 16: ln_fwd_reg_kernel<T, 16><<<gr, 128, 0, st>>>(x, g, b, h, mean, rstd, R, d); break;
+    default: ln_fwd_kernel<T><<<(R + 7) / 8, 256, 0, st>>>(x, g, b, h, mean, rstd, R, d);
+  }
   return launch_check("ln_fwd");
 }
 template <typename T>
 int ln_bwd(const T* dh, const T* x, const float* mean, const float* rstd, const float* g, const T* dres, T* dx, int R,
            int d, cudaStream_t st) {
-  ln_bwd_kernel<T><<<(R + 7) / 8, 256, 0, st>>>(dh, x, mean, rstd, g, dres, dx, R, d);
+  const dim3 gr((R + 3) / 4);
+  switch (d % 256 ? 0 : d / 256) {
+    case 1: ln_bwd_reg_kernel<T, 1><<<gr, 128, 0, st>>>(dh, x, mean, rstd, g, dres, dx, R, d); break;
+    case 2: ln_bwd_reg_kernel<T, 2><<<gr, 128, 0, st>>>(dh, x, mean, rstd, g, dres, dx, R, d); break;
+    case 4: ln_bwd_reg_kernel<T, 4><<<gr, 128, 0, st>>>(dh, x, mean, rstd, g, dres, dx, R, d); break;
+    case 8: ln_bwd_reg_kernel<T, 8><<<gr, 128, 0, st>>>(dh, x, mean, rstd, g, dres, dx, R, d); break;
+    case 16: ln_bwd_reg_kernel<T, 16><<<gr, 128, 0, st>>>(dh, x, mean, rstd, g, dres, dx, R, d); break;
+    default: ln_bwd_kernel<T><<<(R + 7) / 8, 256, 0, st>>>(dh, x, mean, rstd, g, dres, dx, R, d);
+  }
   return launch_check("ln_bwd");
 }
 template <typename T>
 int ln_param_grad(const T* dh, const T* x, const float* mean, const float* rstd, float* dg, float* db, int R, int d,
                   cudaStream_t st) {
-  int rpb = 256;
-  dim3 grid((d + 31) / 32, (R + rpb - 1) / rpb);
-  colsum_kernel<T, true><<<grid, dim3(32, 8), 0, st>>>(dh, x, mean, rstd, dg, db, R, d, rpb);
+  if (d % 8 == 0) {
+    colsum_vec_kernel<T, true><<<dim3((d + 63) / 64, (R + 255) / 256), 256, 0, st>>>(dh, x, mean, rstd, dg, db, R, d);
+  } else {
+    int rpb = 256;
+    dim3 grid((d + 31) / 32, (R + rpb - 1) / rpb);
+    colsum_kernel<T, true><<<grid, dim3(32, 8), 0, st>>>(dh, x, mean, rstd, dg, db, R, d, rpb);
+  }
   return launch_check("ln_param_grad");
 }
 template <typename T>
 int col_sum(const T* y, float* out, int R, int N, cudaStream_t st) {
-  int rpb = 256;
-  dim3 grid((N + 31) / 32, (R + rpb - 1) / rpb);
-  colsum_kernel<T, false><<<grid, dim3(32, 8), 0, st>>>(y, nullptr, nullptr, nullptr, out, nullptr, R, N, rpb);
+  if (N % 8 == 0) {
+    colsum_vec_kernel<T, false>
+        <<<dim3((N + 63) / 64, (R + 255) / 256), 256, 0, st>>>(y, nullptr, nullptr, nullptr, out, nullptr, R, N);
+  } else {
+    int rpb = 256;
+    dim3 grid((N + 31) / 32, (R + rpb - 1) / rpb);
+    colsum_kernel<T, false><<<grid, dim3(32, 8), 0, st>>>(y, nullptr, nullptr, nullptr, out, nullptr, R, N, rpb);
+  }
   return launch_check("col_sum");
 }
 template <typename T>

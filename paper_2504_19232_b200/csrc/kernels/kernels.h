@@ -28,4 +28,8 @@ int attn_rowdot(const T* dO, const T* O, float* D, int b, int H, int Tn, int dh,
 template <typename T>
 int mse_loss(const T* y, const float* tgt, T* dy, float* loss_acc, long n, int n_mb, cudaStream_t st);
 int copy_async(void* dst, const void* src, long bytes, cudaStream_t st);
+// fused causal attention (bf16, head dim 128): attn_tc.cu
+int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d, cudaStream_t st);
+int attn_bwd_tc(const bf16* qkv, const bf16* dO, const float* lse, const float* D, bf16* dqkv, float* dq_acc, int b,
+                int H, int T, int d, cudaStream_t st);
 }  // namespace adaptra

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -69,7 +70,8 @@ struct SlotLayout {
   long yL, seed;  // stage-level (after the per-layer block)
   long slot_bytes;
   // work area
-  long w_S, w_dS, w_do, w_D, work_bytes;
+  long w_S, w_dS, w_do, w_D, w_dq, work_bytes;
+  bool flash;  // fused tcgen05 attention (bf16, head dim 128)
 };
 
 struct adaptra_stage_impl;
@@ -88,6 +90,11 @@ struct adaptra_stage {
 };
 
 namespace adaptra {
+
+static bool getenv_materialized() {
+  const char* v = getenv("ADAPTRA_ATTN");
+  return v && std::string(v) == "materialized";
+}
 
 static int compute_layout(const adaptra_stage_desc_t& d, SlotLayout& L) {
   if (d.n_layers < 1 || d.d < 8 || d.d % 8 || d.b < 1 || d.T < 1) return set_error(ADAPTRA_EINVAL, "stage: bad dims");
@@ -127,11 +134,13 @@ static int compute_layout(const adaptra_stage_desc_t& d, SlotLayout& L) {
     L.rstd1 = put(R * 4);
     L.mean2 = put(R * 4);
     L.rstd2 = put(R * 4);
-    // F->B pool (freed when B ends)
+    // F->B pool (freed when B ends): the fused attention keeps only the
+    // per-row log-sum-exp instead of the T x T probabilities
+    L.flash = d.dtype == ADAPTRA_BF16 && dh == 128 && !getenv_materialized();
     long off_w = off;
     off = 0;
     L.qkv = put(R * 3 * D * e);
-    L.P = put(PT * e);
+    L.P = L.flash ? put((long)d.b * d.n_heads * d.T * 4) : put(PT * e);
     L.a = put(R * F * e);
     L.fb_layer_bytes = off;
     off = off_w;
@@ -156,12 +165,13 @@ static int compute_layout(const adaptra_stage_desc_t& d, SlotLayout& L) {
   L.fb_slot_bytes = L.fb_layer_bytes * d.n_layers;
   long w = 0;
   if (d.block == ADAPTRA_BLOCK_GPT) {
-    long PT = (long)d.b * d.n_heads * d.T * d.T;
+    long PT = L.flash ? 0 : (long)d.b * d.n_heads * d.T * d.T;
     L.w_S = 0;
     L.w_dS = align256(PT * 4);
     L.w_do = align256(L.w_dS + PT * e);
     L.w_D = align256(L.w_do + R * D * e);
-    w = align256(L.w_D + (long)d.b * d.n_heads * d.T * 4);
+    L.w_dq = align256(L.w_D + (long)d.b * d.n_heads * d.T * 4);
+    w = L.flash ? align256(L.w_dq + R * D * 4) : L.w_dq;
   }
   L.work_bytes = w;
   return ADAPTRA_OK;
@@ -274,6 +284,10 @@ struct StageOps {
       TRY(ln_fwd<T>(x, V(p.ln1_g), V(p.ln1_b), h1, fbuf(slot, l, s->L.mean1), fbuf(slot, l, s->L.rstd1), R, Dm, st));
       TRY(GB(dt()).shape(R, 3 * Dm, Dm).A(h1, Dm, R, Dm).B(W(p.Wqkv), Dm, 3 * Dm, Dm).C(qkv, 3 * Dm)
               .epi(ADAPTRA_EPI_STORE).bias(V(p.bqkv)).run(st));
+      if (s->L.flash) {
+        // fused causal attention: o and the per-row LSE (kept for B)
+        TRY(attn_fwd_tc((const bf16*)qkv, (bf16*)o, (float*)P, b, H, Tn, (int)Dm, st));
+      } else {
       // scores S[z] = q_h k_h^T / sqrt(dh), z = (sequence, head); causal tiles only
       const float scale = 1.f / std::sqrt((float)dh);
       TRY(GB(dt()).shape(Tn, Tn, dh).batch(b * H, H)
@@ -287,6 +301,7 @@ struct StageOps {
               .A(P, Tn, (long)b * H * Tn, Tn, 0, (long)H * Tn, Tn, 0, 0)
               .B(qkv + 2 * Dm, 3 * Dm, R, Dm, 1, Tn, 0, 0, dh)
               .C(o, Dm, (long)Tn * Dm, dh).causal(ADAPTRA_CAUSAL_KEND).run(st));
+      }
       TRY(GB(dt()).shape(R, Dm, Dm).A(o, Dm, R, Dm).B(W(p.Wo), Dm, Dm, Dm).C(y1, Dm)
               .epi(ADAPTRA_EPI_RESID).bias(V(p.bo)).res(x, Dm).run(st));
       TRY(ln_fwd<T>(y1, V(p.ln2_g), V(p.ln2_b), h2, fbuf(slot, l, s->L.mean2), fbuf(slot, l, s->L.rstd2), R, Dm, st));
@@ -343,6 +358,11 @@ struct StageOps {
       // do = dy1 Wo
       TRY(GB(dt()).shape(R, Dm, Dm).A(dy1, Dm, R, Dm).B(W(p.Wo), Dm, Dm, Dm, 1).C(dO, Dm).run(st));
       TRY(attn_rowdot<T>(dO, o, Dv, b, H, Tn, dh, Dm, st));
+      if (s->L.flash) {
+        float* dq_acc = (float*)((char*)D.work + s->L.w_dq);
+        TRY(attn_bwd_tc((const bf16*)qkv, (const bf16*)dO, (const float*)P, Dv, (bf16*)dqkv, dq_acc, b, H, Tn, (int)Dm,
+                        st));
+      } else {
       const float scale = 1.f / std::sqrt((float)dh);
       // dS = P * (do_h v_h^T - D) / sqrt(dh)
       TRY(GB(dt()).shape(Tn, Tn, dh).batch(b * H, H)
@@ -366,6 +386,7 @@ struct StageOps {
               .A(P, Tn, (long)b * H * Tn, Tn, 1, (long)H * Tn, Tn, 0, 0)
               .B(dO, Dm, R, Dm, 1, Tn, 0, 0, dh)
               .C(dqkv + 2 * Dm, 3 * Dm, (long)Tn * 3 * Dm, dh).causal(ADAPTRA_CAUSAL_KSTART).run(st));
+      }
       // dh1 = dqkv Wqkv ; dx = dy1 + LN1_bwd(dh1)
       TRY(GB(dt()).shape(R, Dm, 3 * Dm).A(dqkv, 3 * Dm, R, 3 * Dm).B(W(p.Wqkv), Dm, 3 * Dm, Dm, 1).C(dh1, Dm)
               .run(st));
@@ -472,6 +493,12 @@ extern "C" int adaptra_stage_create(const adaptra_stage_desc_t* d, adaptra_stage
   else cudaGetDevice(&s->dev);
   s->x_in.assign(d->n_slots, nullptr);
   s->dy_in.assign(d->n_slots, nullptr);
+  if (s->L.flash && s->L.work_bytes > 0) {
+    // the fused attention backward accumulates dQ with TMA reduce-add; the
+    // finalize kernel re-zeroes it after every use
+    cudaMemset((char*)d->work + s->L.w_dq, 0, (size_t)s->R * d->d * 4);
+    cudaDeviceSynchronize();
+  }
   s->fb_of.assign(d->n_slots, -1);
   for (int k = d->n_slots_fb - 1; k >= 0; --k) s->fb_free.push_back(k);
   *out = s;
