@@ -37,6 +37,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="1.3b", choices=["1.3b", "7b"])
     ap.add_argument("--layers", type=int, default=24)
     ap.add_argument("--d", type=int, default=2048)
     ap.add_argument("--heads", type=int, default=16)
@@ -140,6 +141,8 @@ def main():
         group = dist.new_group(backend="gloo")
     S = args.S or (8 if world >= 8 else 4)
     N = args.N or (32 if S == 8 else 16)
+    if args.model == "7b":  # configs C2/C3: GPT-style 7B-shaped stack
+        args.layers, args.d, args.heads = 32, 4096, 32
     model = ModelCfg(block="gpt", n_layers=args.layers, d=args.d, d_ff=4 * args.d, n_heads=args.heads,
                      b=1, T=args.T, dtype=L.BF16)
     mode = L.LINK_DIRECT if args.link_mode == "direct" else L.LINK_P2P
@@ -320,7 +323,8 @@ def main():
             "bubble_rate": round(head["bubble"], 4), "device_bubble_rate": round(head["device_bubble"], 4),
             "step_tflops": round(head["step_tflops"], 1),
             "step_tflops_frac_of_peak": round(head["step_tflops"] / peaks.get("bf16_tflops_sustained", 1400.0), 4),
-            "config": {"workload": f"C1: GPT-style {args.layers}x(d={args.d},h={args.heads},ff={4 * args.d}) "
+            "config": {"workload": f"{'C2/C3' if args.model == '7b' else 'C1'}: GPT-style "
+                                   f"{args.layers}x(d={args.d},h={args.heads},ff={4 * args.d}) "
                                    f"S={S} N={N} seq={args.T} bf16, paper trace compressed 1 event/step",
                        "stages": S, "microbatches": N, "tokens_per_step": N * model.tokens_per_mb,
                        "stage_map": [i * world // S for i in range(S)],
@@ -342,7 +346,7 @@ def main():
             "e2e": e2e,
             "gpu_launches": head["gpu_launches"],
         }
-        if not args.no_cpu:
+        if not args.no_cpu and world == 1:  # rank 0 at N = 1 only
             line["cpu_baseline"] = cpu_baseline(model, S, N)
         print(json.dumps(line), flush=True)
     pipe.close()

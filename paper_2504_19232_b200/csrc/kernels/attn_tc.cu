@@ -72,7 +72,7 @@ struct AttnArgs {
   float scale;           // 1 / sqrt(dh)
   // forward
   bf16* o;               // [b*T, d]
-  float* lse;            // [b*H*T]
+  float* lse;            // [b*H*T] log-sum-exp of the scaled scores, log2 units
   // backward
   const float* D;        // [b*H*T] rowsum(dO o O)
   bf16* dqkv;            // [b*T, 3d] (k and v sections written here)
@@ -81,7 +81,24 @@ struct AttnArgs {
 }  // namespace
 
 // ============================================================== forward
-__global__ void __launch_bounds__(kThreads, 1)
+constexpr int kAttnThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 softmax
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+// 1-D bulk copy global -> shared, completion counted on an mbarrier (16 B multiple)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kAttnThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const AttnArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -89,7 +106,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sK = sQ + TILE;                  // 2 stages x 32 KB
   uint8_t* sV = sK + 2 * TILE;              // 2 stages x 32 KB
   uint8_t* sP = sV + 2 * TILE;              // 32 KB
-  uint64_t* bar = (uint64_t*)(sP + TILE);
+  float* sStat = (float*)(sP + TILE);       // [2 halves][2 (m, l)][128]
+  uint64_t* bar = (uint64_t*)(sStat + 4 * AT);
   uint64_t* q_full = bar + 0;
   uint64_t* kv_full = bar + 1;   // [2]
   uint64_t* kv_empty = bar + 3;  // [2]
@@ -115,9 +133,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 4);
+      mbar_init(&s_empty[i], 8);
     }
-    mbar_init(p_full, 4);
+    mbar_init(p_full, 8);
     mbar_init(p_empty, 1);
     mbar_init(o_full, 1);
     fence_barrier_init();
@@ -127,7 +145,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS[2] = {tmem, tmem + 128};
   const uint32_t tO = tmem + 256;
 
   if (warp == 0) {
@@ -170,7 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t aK = smem_u32(sK + st * TILE);
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
-          tc_mma_f16(tS[st], desc_kmajor(aQ, ks), desc_kmajor(aK, ks), idesc(0, 0), ks > 0 ? 1u : 0u);
+          tc_mma_f16(tmem + st * 128, desc_kmajor(aQ, ks), desc_kmajor(aK, ks), idesc(0, 0), ks > 0 ? 1u : 0u);
         tc_commit(&s_full[st]);
         if (gi <= qb) tc_commit(&kv_empty[st]);  // pass 1 only needs K
       }
@@ -197,100 +214,108 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) tc_commit(o_full);
     __syncwarp();
   } else {
-    const int quad = warp & 3;
+    // softmax warps: lane quadrant quad (rows), column half (64 keys / head dims)
+    const int quad = warp & 3, half = (warp - 2) >> 2;
     const int r = quad * 32 + lane;           // row within the query block
     const int qi = qb * AT + r;               // query position in the sequence
-    const uint32_t lanes = (uint32_t)(quad * 32) << 16;
+    const uint32_t lanes = ((uint32_t)(quad * 32) << 16) + half * 64;
+    const float c2 = a.scale * kLog2e;        // scores in log2 units
     float m = -INFINITY, l = 0.f;
-    int sb = 0;
-    uint32_t sph = 0, pph = 0;
-    // ---- pass 1: row max and sum
+    // ---- pass 1: row max and sum (log2 domain) over this half of the keys
     for (int j = 0; j <= qb; ++j) {
-      mbar_wait(&s_full[sb], sph);
+      const int sb = j & 1;
+      mbar_wait(&s_full[sb], (j >> 1) & 1);
       tc_fence_after();
-      uint32_t rr[32];
-      tmem_ld32(tS[sb] + lanes, rr);
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        tmem_ld_wait_regs(rr);
-        float u[32];
-#pragma unroll
-        for (int t = 0; t < 32; ++t) u[t] = __uint_as_float(rr[t]) * a.scale;
-        if (c + 1 < 4) tmem_ld32(tS[sb] + lanes + (c + 1) * 32, rr);
-        const int key0 = j * AT + c * 32;
-        float cm = -INFINITY;
-#pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          if (key0 + t > qi) u[t] = -INFINITY;
-          cm = fmaxf(cm, u[t]);
-        }
-        const float mn = fmaxf(m, cm);
-        float acc = 0.f;
-        if (mn != -INFINITY) {
-#pragma unroll
-          for (int t = 0; t < 32; ++t) acc += __expf(u[t] - mn);
-          l = l * __expf(m - mn) + acc;
-          m = mn;
-        }
-      }
+      uint32_t r0[32], r1[32];
+      tmem_ld32(tmem + sb * 128 + lanes, r0);
+      tmem_ld32(tmem + sb * 128 + lanes + 32, r1);
+      tmem_ld_wait_regs(r0);
+      tmem_ld_wait_regs(r1);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_empty[sb]);
-      if (++sb == 2) {
-        sb = 0;
-        sph ^= 1;
+      float u[64];
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        u[t] = __uint_as_float(r0[t]) * c2;
+        u[32 + t] = __uint_as_float(r1[t]) * c2;
+      }
+      if (j == qb) {
+        const int key0 = j * AT + half * 64;
+#pragma unroll
+        for (int t = 0; t < 64; ++t)
+          if (key0 + t > qi) u[t] = -INFINITY;
+      }
+      float cm = u[0];
+#pragma unroll
+      for (int t = 1; t < 64; ++t) cm = fmaxf(cm, u[t]);
+      const float mn = fmaxf(m, cm);
+      if (mn != -INFINITY) {
+        float acc = 0.f;
+#pragma unroll
+        for (int t = 0; t < 64; ++t) acc += ex2(u[t] - mn);
+        l = l * ex2(m - mn) + acc;
+        m = mn;
       }
     }
-    const float lse = m + __logf(l);
-    // ---- pass 2: P = exp(S/sqrt(dh) - LSE) -> shared memory
+    // combine the two halves of the row
+    sStat[(half * 2 + 0) * AT + r] = m;
+    sStat[(half * 2 + 1) * AT + r] = l;
+    named_sync(1, 256);
+    const float m0 = sStat[0 * AT + r], l0 = sStat[1 * AT + r];
+    const float m1 = sStat[2 * AT + r], l1 = sStat[3 * AT + r];
+    const float M = fmaxf(m0, m1);
+    const float lse2 = M + __log2f(l0 * ex2(m0 - M) + l1 * ex2(m1 - M));
+    // ---- pass 2: P = 2^(S c2 - lse2) -> shared memory
     for (int j = 0; j <= qb; ++j) {
-      mbar_wait(&s_full[sb], sph);
+      const int gi = qb + 1 + j, sb = gi & 1;
+      mbar_wait(&s_full[sb], (gi >> 1) & 1);
       tc_fence_after();
-      mbar_wait(p_empty, pph ^ 1);  // previous P V has read the P buffer
-      uint32_t rr[32];
-      tmem_ld32(tS[sb] + lanes, rr);
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        tmem_ld_wait_regs(rr);
-        float p[32];
-#pragma unroll
-        for (int t = 0; t < 32; ++t) p[t] = __uint_as_float(rr[t]);
-        if (c + 1 < 4) tmem_ld32(tS[sb] + lanes + (c + 1) * 32, rr);
-        const int key0 = j * AT + c * 32;
-#pragma unroll
-        for (int t = 0; t < 32; ++t) p[t] = (key0 + t > qi) ? 0.f : __expf(p[t] * a.scale - lse);
-        st_tile_row32(sP, r, c * 32, p);
-      }
+      uint32_t r0[32], r1[32];
+      tmem_ld32(tmem + sb * 128 + lanes, r0);
+      tmem_ld32(tmem + sb * 128 + lanes + 32, r1);
+      tmem_ld_wait_regs(r0);
+      tmem_ld_wait_regs(r1);
       tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[sb]);
+      float p[64];
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        p[t] = ex2(fmaf(__uint_as_float(r0[t]), c2, -lse2));
+        p[32 + t] = ex2(fmaf(__uint_as_float(r1[t]), c2, -lse2));
+      }
+      if (j == qb) {
+        const int key0 = j * AT + half * 64;
+#pragma unroll
+        for (int t = 0; t < 64; ++t)
+          if (key0 + t > qi) p[t] = 0.f;
+      }
+      mbar_wait(p_empty, (j & 1) ^ 1);  // previous P V has read the P buffer
+      st_tile_row32(sP, r, half * 64, p);
+      st_tile_row32(sP, r, half * 64 + 32, p + 32);
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&s_empty[sb]);
-        mbar_arrive(p_full);
-      }
-      pph ^= 1;
-      if (++sb == 2) {
-        sb = 0;
-        sph ^= 1;
-      }
+      if (lane == 0) mbar_arrive(p_full);
     }
-    // ---- epilogue: O -> bf16, LSE
+    // ---- epilogue: O -> bf16 (this half of the head dims), LSE (log2 units)
     mbar_wait(o_full, 0);
     tc_fence_after();
-    bf16* orow = a.o + (size_t)(row0 + qi) * a.d + h * AT;
-    uint32_t rr[32];
-    tmem_ld32(tO + lanes, rr);
-#pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
-      tmem_ld_wait_regs(rr);
-      float v[32];
+    bf16* orow = a.o + (size_t)(row0 + qi) * a.d + h * AT + half * 64;
+    uint32_t r0[32], r1[32];
+    tmem_ld32(tO + lanes, r0);
+    tmem_ld32(tO + lanes + 32, r1);
+    tmem_ld_wait_regs(r0);
+    tmem_ld_wait_regs(r1);
+    float v[64];
 #pragma unroll
-      for (int t = 0; t < 32; ++t) v[t] = __uint_as_float(rr[t]);
-      if (c + 1 < 4) tmem_ld32(tO + lanes + (c + 1) * 32, rr);
-#pragma unroll
-      for (int t = 0; t < 32; t += 8) st_bf16x8(orow + c * 32 + t, v + t);
+    for (int t = 0; t < 32; ++t) {
+      v[t] = __uint_as_float(r0[t]);
+      v[32 + t] = __uint_as_float(r1[t]);
     }
-    a.lse[(size_t)z * a.T + qi] = lse;
+#pragma unroll
+    for (int t = 0; t < 64; t += 8) st_bf16x8(orow + t, v + t);
+    if (half == 0) a.lse[(size_t)z * a.T + qi] = lse2;
   }
   tc_fence_before();
   __syncthreads();
@@ -299,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ============================================================== backward
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kAttnThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                     const __grid_constant__ CUtensorMap tm_dq, const AttnArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -310,18 +335,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sdO = sQ + TILE;      // 32 KB
   uint8_t* sPT = sdO + TILE;     // 32 KB  P^T  [keys x queries]
   uint8_t* sdST = sPT + TILE;    // 32 KB  dS^T [keys x queries]
-  uint8_t* sStg = sdST + TILE;   // 4 warps x 2 x 4 KB dQ staging
-  float* sLse = (float*)(sStg + 4 * 8192);  // [128]
+  uint8_t* sStg = sdST + TILE;   // 8 warps x 4 KB dQ staging
+  float* sLse = (float*)(sStg + 8 * 4096);  // [128] (log2 units)
   float* sD = sLse + AT;                    // [128]
   uint64_t* bar = (uint64_t*)(sD + AT);
   uint64_t* kv_full = bar + 0;
   uint64_t* qd_full = bar + 1;
   uint64_t* qd_empty = bar + 2;
   uint64_t* sd_full = bar + 3;   // S^T and dP^T in TMEM
-  uint64_t* pd_full = bar + 4;   // P^T, dS^T in smem (4 warps)
+  uint64_t* pd_full = bar + 4;   // P^T, dS^T in smem (8 warps)
   uint64_t* pd_empty = bar + 5;  // MMAs done reading P^T, dS^T
   uint64_t* dq_full = bar + 6;   // dQ partial in TMEM
-  uint64_t* dq_empty = bar + 7;  // dQ drained (4 warps)
+  uint64_t* dq_empty = bar + 7;  // dQ drained (8 warps)
   uint64_t* kv_done = bar + 8;   // dK, dV final
   uint32_t* tmem_slot = (uint32_t*)(bar + 9);
 
@@ -341,10 +366,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(qd_full, 1);
     mbar_init(qd_empty, 1);
     mbar_init(sd_full, 1);
-    mbar_init(pd_full, 4);
+    mbar_init(pd_full, 8);
     mbar_init(pd_empty, 1);
     mbar_init(dq_full, 1);
-    mbar_init(dq_empty, 4);
+    mbar_init(dq_empty, 8);
     mbar_init(kv_done, 1);
     fence_barrier_init();
   }
@@ -366,11 +391,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t ph = 0;
       for (int i = kb; i < nb; ++i) {
         mbar_wait(qd_empty, ph ^ 1);
-        mbar_arrive_expect_tx(qd_full, 2 * TILE);
+        mbar_arrive_expect_tx(qd_full, 2 * TILE + 2 * AT * 4);
         for (int c = 0; c < 2; ++c) {
           tma_load_2d(sQ + c * CHUNK, &tm_qkv, qd_full, qcol + 64 * c, row0 + i * AT);
           tma_load_2d(sdO + c * CHUNK, &tm_do, qd_full, h * AT + 64 * c, row0 + i * AT);
         }
+        bulk_g2s(sLse, a.lse + (size_t)z * a.T + i * AT, AT * 4, qd_full);
+        bulk_g2s(sD, a.D + (size_t)z * a.T + i * AT, AT * 4, qd_full);
         ph ^= 1;
       }
     }
@@ -398,15 +425,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) {
         const uint32_t acc = (i > kb) ? 1u : 0u;
 #pragma unroll
+        for (int ks = 0; ks < 8; ++ks)  // dQ_i = dS K first: its drain overlaps dV, dK
+          tc_mma_f16(tdQ, desc_mnmajor(adST, ks), desc_mnmajor(aK, ks), idesc(1, 1), ks > 0 ? 1u : 0u);
+        tc_commit(dq_full);
+#pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
           // dV += P^T dO_i ; dK += dS^T Q_i  (B operands read MN-major)
           tc_mma_f16(tdV, desc_kmajor(aPT, ks), desc_mnmajor(adO, ks), idesc(0, 1), (acc || ks > 0) ? 1u : 0u);
           tc_mma_f16(tdK, desc_kmajor(adST, ks), desc_mnmajor(aQ, ks), idesc(0, 1), (acc || ks > 0) ? 1u : 0u);
         }
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks)  // dQ_i = dS K (A = dS^T read MN-major)
-          tc_mma_f16(tdQ, desc_mnmajor(adST, ks), desc_mnmajor(aK, ks), idesc(1, 1), ks > 0 ? 1u : 0u);
-        tc_commit(dq_full);
         tc_commit(pd_empty);
         tc_commit(qd_empty);
       }
@@ -416,109 +443,105 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) tc_commit(kv_done);
     __syncwarp();
   } else {
-    const int quad = warp & 3;
-    const int r = quad * 32 + lane;  // key row of this CTA's block
+    const int quad = warp & 3, half = (warp - 2) >> 2;
+    const int r = quad * 32 + lane;  // key row (S^T, dP^T, dK, dV) / query row (dQ)
     const int kj = kb * AT + r;      // key position
-    const uint32_t lanes = (uint32_t)(quad * 32) << 16;
-    uint8_t* stg = sStg + quad * 8192;
-    int sbuf = 0;
+    const uint32_t lanes = ((uint32_t)(quad * 32) << 16) + half * 64;
+    const float c2 = a.scale * kLog2e;
+    uint8_t* stg = sStg + (warp - 2) * 4096;
     uint32_t ph = 0;
     for (int i = kb; i < nb; ++i) {
       mbar_wait(sd_full, ph);
       tc_fence_after();
-      const float* lse_i = a.lse + (size_t)z * a.T + i * AT;
-      const float* D_i = a.D + (size_t)z * a.T + i * AT;
-      mbar_wait(pd_empty, ph ^ 1);  // previous MMAs done reading P^T / dS^T
-      uint32_t rs[32], rd[32];
-      tmem_ld32(tS + lanes, rs);
-      tmem_ld32(tdP + lanes, rd);
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        tmem_ld_wait_regs(rs);
-        tmem_ld_wait_regs(rd);
-        float p[32], ds[32];
+      uint32_t rs0[32], rs1[32];
+      tmem_ld32(tS + lanes, rs0);
+      tmem_ld32(tS + lanes + 32, rs1);
+      tmem_ld_wait_regs(rs0);
+      tmem_ld_wait_regs(rs1);
+      float p[64], ds[64];
+      const int q0 = i * AT + half * 64;
+      const float* lse = sLse + half * 64;
+      const float* Dq = sD + half * 64;
 #pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          p[t] = __uint_as_float(rs[t]);
-          ds[t] = __uint_as_float(rd[t]);
-        }
-        if (c + 1 < 4) {
-          tmem_ld32(tS + lanes + (c + 1) * 32, rs);
-          tmem_ld32(tdP + lanes + (c + 1) * 32, rd);
-        }
-        const int q0 = i * AT + c * 32;
-#pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          const float pe = (q0 + t < kj) ? 0.f : __expf(p[t] * a.scale - __ldg(lse_i + c * 32 + t));
-          p[t] = pe;
-          ds[t] = pe * (ds[t] - __ldg(D_i + c * 32 + t));
-        }
-        st_tile_row32(sPT, r, c * 32, p);
-        st_tile_row32(sdST, r, c * 32, ds);
+      for (int t = 0; t < 32; ++t) {
+        p[t] = ex2(fmaf(__uint_as_float(rs0[t]), c2, -lse[t]));
+        p[32 + t] = ex2(fmaf(__uint_as_float(rs1[t]), c2, -lse[32 + t]));
       }
+      if (i == kb) {
+#pragma unroll
+        for (int t = 0; t < 64; ++t)
+          if (q0 + t < kj) p[t] = 0.f;
+      }
+      tmem_ld32(tdP + lanes, rs0);
+      tmem_ld32(tdP + lanes + 32, rs1);
+      tmem_ld_wait_regs(rs0);
+      tmem_ld_wait_regs(rs1);
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        ds[t] = p[t] * (__uint_as_float(rs0[t]) - Dq[t]);
+        ds[32 + t] = p[32 + t] * (__uint_as_float(rs1[t]) - Dq[32 + t]);
+      }
+      mbar_wait(pd_empty, ph ^ 1);  // previous MMAs done reading P^T / dS^T
+      st_tile_row32(sPT, r, half * 64, p);
+      st_tile_row32(sPT, r, half * 64 + 32, p + 32);
+      st_tile_row32(sdST, r, half * 64, ds);
+      st_tile_row32(sdST, r, half * 64 + 32, ds + 32);
       tc_fence_before();
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(pd_full);
-      // dQ partial (thread = query row) -> TMA reduce-add (scaled).  The TMEM
-      // columns are released as soon as the last chunk is in registers.
+      // dQ partial (thread = query row, this half of the head dims) -> TMA reduce-add
       mbar_wait(dq_full, ph);
       tc_fence_after();
-      uint32_t rq[32];
-      tmem_ld32(tdQ + lanes, rq);
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        tmem_ld_wait_regs(rq);
-        float v[32];
-#pragma unroll
-        for (int t = 0; t < 32; ++t) v[t] = __uint_as_float(rq[t]) * a.scale;
-        if (c + 1 < 4) {
-          tmem_ld32(tdQ + lanes + (c + 1) * 32, rq);
-        } else {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(dq_empty);
-        }
-        if (lane == 0) bulk_wait_read<1>();
+      uint32_t rq0[32], rq1[32];
+      tmem_ld32(tdQ + lanes, rq0);
+      tmem_ld32(tdQ + lanes + 32, rq1);
+      tmem_ld_wait_regs(rq0);
+      tmem_ld_wait_regs(rq1);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dq_empty);
+      auto drain = [&](const uint32_t(&rq)[32], int c) {
+        if (lane == 0) bulk_wait_read<0>();
         __syncwarp();
-        uint8_t* sb = stg + sbuf * 4096;
-        uint8_t* frow = sb + lane * 128;
+        uint8_t* frow = stg + lane * 128;
 #pragma unroll
         for (int q = 0; q < 8; ++q)
           *reinterpret_cast<float4*>(frow + ((q ^ (lane & 7)) << 4)) =
-              make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+              make_float4(__uint_as_float(rq[4 * q]) * a.scale, __uint_as_float(rq[4 * q + 1]) * a.scale,
+                          __uint_as_float(rq[4 * q + 2]) * a.scale, __uint_as_float(rq[4 * q + 3]) * a.scale);
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_reduce_add_2d(&tm_dq, sb, h * AT + c * 32, row0 + i * AT + quad * 32);
+          tma_reduce_add_2d(&tm_dq, stg, h * AT + half * 64 + c * 32, row0 + i * AT + quad * 32);
           bulk_commit();
         }
-        sbuf ^= 1;
-      }
+      };
+      drain(rq0, 0);
+      drain(rq1, 1);
       ph ^= 1;
     }
     if (lane == 0) bulk_wait<0>();
     // dK (scaled), dV -> bf16 into dqkv (k and v sections), thread = key row
     mbar_wait(kv_done, 0);
     tc_fence_after();
-    bf16* dk_row = a.dqkv + (size_t)(row0 + kj) * 3 * a.d + a.d + h * AT;
-    bf16* dv_row = a.dqkv + (size_t)(row0 + kj) * 3 * a.d + 2 * a.d + h * AT;
     for (int which = 0; which < 2; ++which) {
       const uint32_t tb = (which == 0 ? tdK : tdV) + lanes;
-      bf16* out = which == 0 ? dk_row : dv_row;
+      bf16* out = a.dqkv + (size_t)(row0 + kj) * 3 * a.d + (which == 0 ? a.d : 2 * a.d) + h * AT + half * 64;
       const float sc = which == 0 ? a.scale : 1.f;
-      uint32_t rr[32];
-      tmem_ld32(tb, rr);
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        tmem_ld_wait_regs(rr);
-        float v[32];
+      uint32_t r0[32], r1[32];
+      tmem_ld32(tb, r0);
+      tmem_ld32(tb + 32, r1);
+      tmem_ld_wait_regs(r0);
+      tmem_ld_wait_regs(r1);
+      float v[64];
 #pragma unroll
-        for (int t = 0; t < 32; ++t) v[t] = __uint_as_float(rr[t]) * sc;
-        if (c + 1 < 4) tmem_ld32(tb + (c + 1) * 32, rr);
-#pragma unroll
-        for (int t = 0; t < 32; t += 8) st_bf16x8(out + c * 32 + t, v + t);
+      for (int t = 0; t < 32; ++t) {
+        v[t] = __uint_as_float(r0[t]) * sc;
+        v[32 + t] = __uint_as_float(r1[t]) * sc;
       }
+#pragma unroll
+      for (int t = 0; t < 64; t += 8) st_bf16x8(out + t, v + t);
     }
   }
   tc_fence_before();
@@ -583,8 +606,8 @@ static int check_launch(const char* w) {
   return ADAPTRA_OK;
 }
 
-constexpr int kFwdSmem = 6 * TILE + 1024 + 256;
-constexpr int kBwdSmem = 6 * TILE + 4 * 8192 + 2 * AT * 4 + 1024 + 256;
+constexpr int kFwdSmem = 6 * TILE + 4 * AT * 4 + 1024 + 256;
+constexpr int kBwdSmem = 6 * TILE + 8 * 4096 + 2 * AT * 4 + 1024 + 256;
 
 int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d, cudaStream_t st) {
   if (d != H * AT || T % AT) return set_error(ADAPTRA_EINVAL, "attn_fwd_tc: head dim 128 and T % 128 required");
@@ -604,7 +627,7 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
   a.o = o;
   a.lse = lse;
   void* pb = prof_on() ? prof_begin(st) : nullptr;
-  attn_fwd_kernel<<<b * H * (T / AT), kThreads, kFwdSmem, st>>>(m, a);
+  attn_fwd_kernel<<<b * H * (T / AT), kAttnThreads, kFwdSmem, st>>>(m, a);
   if (pb) {
     double fl = 4.0 * (double)T * T * AT * b * H * 0.5;  // algorithmic: QK^T + PV, causal half (R28)
     prof_end(pb, st, PROF_ATTN, fl, 0);
@@ -635,7 +658,7 @@ int attn_bwd_tc(const bf16* qkv, const bf16* dO, const float* lse, const float* 
   a.dqkv = dqkv;
   a.dq_acc = dq_acc;
   void* pb = prof_on() ? prof_begin(st) : nullptr;
-  attn_bwd_kernel<<<b * H * (T / AT), kThreads, kBwdSmem, st>>>(mq, mdo, mdq, a);
+  attn_bwd_kernel<<<b * H * (T / AT), kAttnThreads, kBwdSmem, st>>>(mq, mdo, mdq, a);
   if (pb) {
     double fl = 8.0 * (double)T * T * AT * b * H * 0.5;  // dP, dV, dK, dQ (causal half)
     prof_end(pb, st, PROF_ATTN, fl, 0);
