@@ -31,7 +31,12 @@ namespace adaptra {
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one SWIZZLE_128B row
-constexpr int kThreads = 192;
+// 12 warps: 0..7 epilogue (two warpgroups, two warps per TMEM lane quadrant,
+// each owning half of the tile's columns), 8 TMA producer, 9 TMEM allocator +
+// MMA issuer, 10..11 idle (they complete the third warpgroup for setmaxnreg).
+constexpr int kThreads = 384;
+constexpr int kEpiWarps = 8;
+constexpr int kWarpProducer = 8, kWarpMma = 9;
 
 template <int CG, int BN>
 struct TcCfg {
@@ -41,7 +46,7 @@ struct TcCfg {
   static constexpr int kBBytes = kBRows * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;       // two accumulators of 128 lanes x BN columns
-  static constexpr int kEpiBytes = 4 * 2 * 4096;  // 4 epilogue warps x 2 staging buffers x 32x32 fp32
+  static constexpr int kEpiBytes = kEpiWarps * 4096;  // one 32x32 fp32 staging buffer per epilogue warp
   static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int TM = BM * CG;             // tile rows
 };
@@ -95,7 +100,8 @@ __device__ __forceinline__ bool tile_range(const adaptra_gemm_desc_t& g, const T
 }
 
 // ---------------------------------------------------------------- epilogue
-// Runs in warps 2..5 of every CTA.  Rows of this CTA: tile row0 + rank*128.
+// Runs in warps 0..7 of every CTA.  Rows of this CTA: tile row0 + rank*128;
+// warp w drains lane quadrant w % 4, columns [(w / 4) BN/2, (w / 4 + 1) BN/2).
 template <int CG, int BN>
 __device__ __forceinline__ void epilogue_loop(const adaptra_gemm_desc_t& g, const TileInfo& ti, const EpiTma& et,
                                               const CUtensorMap* tmC, const CUtensorMap* tmX, int vec_ok,
@@ -104,8 +110,9 @@ __device__ __forceinline__ void epilogue_loop(const adaptra_gemm_desc_t& g, cons
   constexpr int TM = TcCfg<CG, BN>::TM;
   const int n_tiles = ti.m_blocks * ti.n_blocks * ti.Z;
   const int quad = warp & 3;  // TMEM lane quadrant this warp may access
-  uint8_t* stg = sEpi + (warp - 2) * 8192;
-  int sbuf = 0;
+  const int co = (warp >> 2) * (BN / 2);  // first column of this warp's half
+  constexpr int NC = BN / 64;            // 32-column chunks per warp
+  uint8_t* stg = sEpi + warp * 4096;
   int acc = 0;
   uint32_t acc_phase = 0;
   const bool f32o = (g.epi == ADAPTRA_EPI_ACC_F32 || g.epi == ADAPTRA_EPI_STORE_F32);
@@ -120,32 +127,32 @@ __device__ __forceinline__ void epilogue_loop(const adaptra_gemm_desc_t& g, cons
     const bool row_ok = m < e.M;
     const int z1 = z / g.zdiv, z2 = z % g.zdiv;
     const int crow = z1 * et.c_r1 + z2 * et.c_r2 + rbase;
-    const int ccol = z1 * et.c_q1 + z2 * et.c_q2 + nb * BN;
+    const int ccol = z1 * et.c_q1 + z2 * et.c_q2 + nb * BN + co;
     const int xrow = z1 * et.x_r1 + z2 * et.x_r2 + rbase;
-    const int xcol = z1 * et.x_q1 + z2 * et.x_q2 + nb * BN;
+    const int xcol = z1 * et.x_q1 + z2 * et.x_q2 + nb * BN + co;
     const bf16* in_row = nullptr;
     if (has_in && row_ok)
       in_row = g.epi == ADAPTRA_EPI_RESID ? (const bf16*)e.R + (long)m * e.ldr : (const bf16*)e.aux + (long)m * e.ldaux;
     float nxt[32];
-    if (in_row) ld_row32(in_row + nb * BN, nb * BN, e.N, vec_ok, nxt);
+    if (in_row) ld_row32(in_row + nb * BN + co, nb * BN + co, e.N, vec_ok, nxt);
     const float Dm = (g.epi == ADAPTRA_EPI_DSOFTMAX && row_ok) ? e.rowv[m] : 0.f;
     mbar_wait(&tfull[acc], acc_phase);
     tc_fence_after();
-    const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
+    const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + co;
     uint32_t r[32];
     tmem_ld32(tbase, r);  // chunk 0; chunk c+1 is requested while chunk c is processed
 #pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
-      const int n0 = nb * BN + c * 32;
+    for (int c = 0; c < NC; ++c) {
+      const int n0 = nb * BN + co + c * 32;
       tmem_ld_wait_regs(r);
       float v[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-      if (c + 1 < BN / 32) tmem_ld32(tbase + (c + 1) * 32, r);
+      if (c + 1 < NC) tmem_ld32(tbase + (c + 1) * 32, r);
       float in[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) in[j] = nxt[j];
-      if (in_row && c + 1 < BN / 32 && n0 + 32 < e.N) ld_row32(in_row + n0 + 32, n0 + 32, e.N, vec_ok, nxt);
+      if (in_row && c + 1 < NC && n0 + 32 < e.N) ld_row32(in_row + n0 + 32, n0 + 32, e.N, vec_ok, nxt);
       if (n0 >= e.N) continue;
       if (et.on == 2) continue;  // diagnostic: accumulator drained, no epilogue work
       if (!et.on) {
@@ -170,10 +177,10 @@ __device__ __forceinline__ void epilogue_loop(const adaptra_gemm_desc_t& g, cons
           for (int j = 0; j < 32; ++j) bv[j] = (n0 + j < e.N) ? e.bias[n0 + j] : 0.f;
         }
       }
-      // wait until this staging buffer's previous TMA store has read it
-      if (lane == 0) bulk_wait_read<1>();
+      // wait until the staging buffer's previous TMA store has read it
+      if (lane == 0) bulk_wait_read<0>();
       __syncwarp();
-      uint8_t* sb = stg + sbuf * 4096;
+      uint8_t* sb = stg;
       switch (g.epi) {
         case ADAPTRA_EPI_STORE:
 #pragma unroll
@@ -220,10 +227,7 @@ __device__ __forceinline__ void epilogue_loop(const adaptra_gemm_desc_t& g, cons
       }
       fence_proxy_async_smem();
       __syncwarp();
-      if (et.on == 3) {  // diagnostic: full epilogue except the TMA store itself
-        sbuf ^= 1;
-        continue;
-      }
+      if (et.on == 3) continue;  // diagnostic: full epilogue except the TMA store itself
       if (lane == 0) {
         if (g.epi == ADAPTRA_EPI_ACC_F32)
           tma_reduce_add_2d(tmC, sb, ccol + c * 32, crow);
@@ -232,7 +236,6 @@ __device__ __forceinline__ void epilogue_loop(const adaptra_gemm_desc_t& g, cons
         if (g.epi == ADAPTRA_EPI_GELU) tma_store_2d(tmX, sb + 2048, xcol + c * 32, xrow);
         bulk_commit();
       }
-      sbuf ^= 1;
     }
     tc_fence_before();
     __syncwarp();
@@ -276,7 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int ncl = CG == 2 ? gridDim.x / 2 : gridDim.x;
   const int n_tiles = ti.m_blocks * ti.n_blocks * ti.Z;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == kWarpProducer && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     for (int s = 0; s < Cfg::kStages; ++s) {
@@ -285,11 +288,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4 * CG);
+      mbar_init(&tempty[s], kEpiWarps * CG);
     }
     fence_barrier_init();
   }
-  if (warp == 1) {
+  if (warp == kWarpMma) {
     if (CG == 1)
       tmem_alloc(tmem_slot, Cfg::kTmemCols);
     else
@@ -303,7 +306,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
+  // register budget: the epilogue warpgroups grow, the producer/MMA warpgroup
+  // shrinks (setmaxnreg executed uniformly per warpgroup at the top of its branch)
+  if (warp >= kEpiWarps) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory");
+  if (warp == kWarpProducer) {
     // ===================== TMA producer =====================
     if (lane == 0) {
       int stage = 0;
@@ -360,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kWarpMma) {
     // ===================== MMA issuer (leader CTA) =====================
     // Instruction descriptor, kind::f16: D f32 (bit 4), A bf16 (bits 7-9 = 1),
     // B bf16 (bits 10-12 = 1), A/B major (bits 15/16), N>>3 (17-22), M>>4 (24-28).
@@ -421,7 +428,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+  }
   } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
     epilogue_loop<CG, BN>(g, ti, et, &tmC, &tmX, vec_ok, sEpi, tmem_base, tfull, tempty, warp, lane, cid, ncl, rank);
   }
   tc_fence_before();
@@ -430,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   else
     __syncthreads();
   tc_fence_after();
-  if (warp == 1) {
+  if (warp == kWarpMma) {
     if (CG == 1)
       tmem_dealloc(tmem_base, Cfg::kTmemCols);
     else
