@@ -427,6 +427,33 @@ def adaptive_plan(S, N, tF, tB, c, x_cur, x_init, c_nominal=None):
     return list(x_cur), False
 
 
+def clamp_plan(x, cap):
+    """R26: without host activation offload (N4) the device stash caps the
+    warm-up counts: x_i <- min(x_i, cap_i), then the Lemma is
+    restored from the last stage upwards, x_i <- max(x_i, x_{i+1})."""
+    out = [min(v, c) for v, c in zip(x, cap)]
+    for i in range(len(out) - 2, -1, -1):
+        out[i] = max(out[i], out[i + 1])
+    return out
+
+
+def adaptive_orders(S, N, tF, tB, tW, cs_seq, x_init, x_cap=None, ratio=30):
+    """The adaptive arm over a sequence of per-iteration latency vectors
+    (R18): returns [(x, per-stage (kind, mb) order)] for every iteration."""
+    delta = default_delta(tF, tB, tW, ratio)
+    x = list(x_init)
+    out = []
+    for c in cs_seq:
+        if all(v == 0 for v in c):
+            x = list(x_init)
+        elif not all(eq1_holds(tF, tB, c, x)):
+            xa = get_adapted_warmup_fwds(S, N, tF, tB, c)
+            x = clamp_plan(xa, x_cap) if x_cap else xa
+        X, _, _ = schedule(S, N, tF, tB, tW, c, x, delta)
+        out.append((list(x), order_of(X)))
+    return out
+
+
 # ---------------------------------------------------------------------------
 # Brute force optimum on tiny instances (stand-in for the paper's MILP, A12)
 # ---------------------------------------------------------------------------
