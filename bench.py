@@ -191,7 +191,7 @@ def main():
     timer = torch.cuda.Stream(device=local_rank)
 
     def run_arm(name, with_trace, steps, warmup, e2e=False, prof=False):
-        arm = Arm(name, S, N, tF, tB, tW, x_init=x_init if name == "adaptive" else None, x_cap=x_cap)
+        arm = Arm(name, S, N, tF, tB, tW, x_init=x_init if name.startswith("adaptive") else None, x_cap=x_cap)
         host_in = None
         if e2e and 0 in pipe.stages:
             host_in = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in pipe.inputs]
@@ -212,7 +212,7 @@ def main():
                 for h, t in zip(host_in, pipe.inputs):
                     t.copy_(h, non_blocking=True)
                 torch.cuda.current_stream().synchronize()
-            res = pipe.run(orders, merge_w=arm.merge_w, want_times=True)
+            res = pipe.run(orders, merge_w=arm.merge_w, want_times=True, inorder=arm.inorder)
             return res
 
         for k in range(warmup):
@@ -322,7 +322,7 @@ def main():
             "data": "synthetic (seeded N(0,1) inputs/targets, GPT-2 init weights)",
             "bubble_rate": round(head["bubble"], 4), "device_bubble_rate": round(head["device_bubble"], 4),
             "step_tflops": round(head["step_tflops"], 1),
-            "step_tflops_frac_of_peak": round(head["step_tflops"] / peaks.get("bf16_tflops_sustained", 1400.0), 4),
+            "step_tflops_frac_of_peak": round(head["step_tflops"] / (world * peaks.get("bf16_tflops_sustained", 1400.0)), 4),
             "config": {"workload": f"{'C2/C3' if args.model == '7b' else 'C1'}: GPT-style "
                                    f"{args.layers}x(d={args.d},h={args.heads},ff={4 * args.d}) "
                                    f"S={S} N={N} seq={args.T} bf16, paper trace compressed 1 event/step",

@@ -315,6 +315,12 @@ int adaptra_set_link_latency(adaptra_outbox_t ob, int64_t latency_ns);
 /* Send message mb of iteration epoch once the work already enqueued on
  * `producer` (the producing op) has completed. */
 int adaptra_send(adaptra_outbox_t ob, int32_t mb, void* producer, uint32_t epoch);
+/* Host-blocking variants used by the in-order baseline (ADAPTRA_EXEC_INORDER):
+ * block the calling thread until message mb of iteration epoch is in the
+ * mailbox / has been delivered to the receiver (as a synchronous send/recv in
+ * the compute sequence would). */
+int adaptra_recv_blocking(adaptra_inbox_t ib, int32_t mb, uint32_t epoch, void** slot_out);
+int adaptra_send_wait(adaptra_outbox_t ob, int32_t mb, uint32_t epoch);
 /* Gate statistics since open: messages, sum/max of (flag post - data ready) in ns. */
 int adaptra_link_stats(adaptra_outbox_t ob, int64_t* n_msgs, int64_t* sum_delay_ns, int64_t* max_delay_ns);
 
@@ -354,7 +360,10 @@ typedef struct adaptra_iter_stats {
 int adaptra_exec_create(const adaptra_exec_desc_t* d, adaptra_exec_t* out);
 int adaptra_exec_destroy(adaptra_exec_t e);
 /* Post one iteration: ops[n] (kind, mb) in order; flags: ADAPTRA_MERGE_W runs W
- * right after each B (1F1B).  Non-blocking (the stage thread enqueues). */
+ * right after each B (1F1B); ADAPTRA_EXEC_INORDER makes every receive and every
+ * send block the stage thread (the sequential-launch baseline that exhibits
+ * head-of-line blocking).  Non-blocking (the stage thread enqueues). */
+#define ADAPTRA_EXEC_INORDER 16u
 int adaptra_run_iteration(adaptra_exec_t e, const adaptra_op_t* ops, int32_t n, uint32_t epoch, uint32_t flags);
 /* Wait until the stage thread has enqueued the whole iteration; returns its
  * error, if any (call on every stage before adaptra_exec_wait so that a

@@ -17,6 +17,7 @@ EINVAL, EPLAN, EDEADLOCK, ECUDA, ENOMEM, ELINK, ETOOBIG = -1, -2, -3, -4, -5, -6
 
 OP_F, OP_B, OP_W = 0, 1, 2
 SEL_PAPER, SEL_CAP, MERGE_W = 0, 1, 2
+EXEC_INORDER = 16
 F32, BF16 = 0, 1
 BLOCK_MLP, BLOCK_GPT = 0, 1
 
@@ -119,6 +120,8 @@ _SIGS = {
     "adaptra_outbox_dst": (_vp, [_vp, _i32]),
     "adaptra_set_link_latency": (_i32, [_vp, _i64]),
     "adaptra_send": (_i32, [_vp, _i32, _vp, _u32]),
+    "adaptra_recv_blocking": (_i32, [_vp, _i32, _u32, _P(_vp)]),
+    "adaptra_send_wait": (_i32, [_vp, _i32, _u32]),
     "adaptra_link_stats": (_i32, [_vp, _P(_i64), _P(_i64), _P(_i64)]),
     "adaptra_exec_create": (_i32, [_P(ExecDesc), _P(_vp)]),
     "adaptra_exec_destroy": (_i32, [_vp]),

@@ -85,7 +85,7 @@ static bool host_wait_mode() {
   return on;
 }
 
-static int host_wait(const uint32_t* addr, uint32_t v) {
+int host_wait(const uint32_t* addr, uint32_t v) {
   thread_local uint32_t* h = nullptr;
   thread_local cudaStream_t s = nullptr;
   if (!h) {

@@ -556,6 +556,26 @@ extern "C" int adaptra_send(adaptra_outbox_t ob, int32_t mb, void* producer, uin
   return ADAPTRA_OK;
 }
 
+extern "C" int adaptra_recv_blocking(adaptra_inbox_t ib, int32_t mb, uint32_t epoch, void** slot_out) {
+  if (!ib || mb < 0 || mb >= ib->n_mb) return set_error(ADAPTRA_EINVAL, "recv_blocking: bad mb");
+  cudaSetDevice(ib->dev);
+  int rc = host_wait(ib->flags + mb, epoch);
+  if (rc) return rc;
+  if (slot_out) *slot_out = (char*)ib->mbox + (size_t)mb * ib->bytes;
+  return ADAPTRA_OK;
+}
+
+extern "C" int adaptra_send_wait(adaptra_outbox_t ob, int32_t mb, uint32_t epoch) {
+  if (!ob || mb < 0 || mb >= ob->n_mb) return set_error(ADAPTRA_EINVAL, "send_wait: bad mb");
+  cudaSetDevice(ob->dev);
+  if (ob->latency.load() == ADAPTRA_LINK_DOWN) {  // delegated path: wait for the host flag
+    volatile uint32_t* hf = ob->ring.flags(ob->bytes, ob->n_mb) + mb;
+    while ((int32_t)(*hf - epoch) < 0) std::this_thread::sleep_for(std::chrono::microseconds(5));
+    return ADAPTRA_OK;
+  }
+  return host_wait(ob->peer_flags + mb, epoch);  // the receiver's flag (UVA / IPC-mapped)
+}
+
 extern "C" int adaptra_link_stats(adaptra_outbox_t ob, int64_t* n, int64_t* sum, int64_t* mx) {
   if (!ob) return set_error(ADAPTRA_EINVAL, "link_stats: null");
   if (n) *n = ob->n_msgs.load();

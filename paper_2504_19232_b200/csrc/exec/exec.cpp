@@ -58,6 +58,7 @@ struct adaptra_exec {
     cudaSetDevice(dev);
     const int S = d.n_stages, i = d.stage_index, N = d.n_microbatches;
     const bool merge = flags & ADAPTRA_MERGE_W;
+    const bool inorder = flags & ADAPTRA_EXEC_INORDER;
     const int64_t t_start = now_ns();
     std::vector<int> free_slots;
     for (int k = stage_n_slots(d.stage) - 1; k >= 0; --k) free_slots.push_back(k);
@@ -94,7 +95,9 @@ struct adaptra_exec {
           x = d.inputs[mb - 1];
         } else {
           void* p = nullptr;
-          if ((rc = adaptra_recv(d.in_fwd, mb - 1, epoch, cs, &p))) return rc;
+          if ((rc = inorder ? adaptra_recv_blocking(d.in_fwd, mb - 1, epoch, &p)
+                            : adaptra_recv(d.in_fwd, mb - 1, epoch, cs, &p)))
+            return rc;
           x = p;
         }
         void* y = (i < S - 1) ? adaptra_outbox_dst(d.out_fwd, mb - 1) : nullptr;
@@ -106,11 +109,14 @@ struct adaptra_exec {
         DBG("  F launched");
         ADAPTRA_CUDA_TRY(cudaEventRecord(ev_e[q], cs));
         if (i < S - 1 && (rc = adaptra_send(d.out_fwd, mb - 1, cs, epoch))) return rc;
+        if (inorder && i < S - 1 && (rc = adaptra_send_wait(d.out_fwd, mb - 1, epoch))) return rc;
       } else if (o.kind == ADAPTRA_OP_B) {
         int slot = slot_of_mb[mb];
         if (slot < 0) return set_error(ADAPTRA_EINVAL, "exec: B before F");
         void* dy = nullptr;
-        if (i < S - 1 && (rc = adaptra_recv(d.in_bwd, mb - 1, epoch, cs, &dy))) return rc;
+        if (i < S - 1 && (rc = inorder ? adaptra_recv_blocking(d.in_bwd, mb - 1, epoch, &dy)
+                                       : adaptra_recv(d.in_bwd, mb - 1, epoch, cs, &dy)))
+          return rc;
         void* dx = (i > 0) ? adaptra_outbox_dst(d.out_bwd, mb - 1) : nullptr;
         ADAPTRA_CUDA_TRY(cudaEventRecord(ev_s[q], cs));
         DBG("  B recv done dy=%p dx=%p", dy, dx);
@@ -123,6 +129,7 @@ struct adaptra_exec {
         }
         ADAPTRA_CUDA_TRY(cudaEventRecord(ev_e[q], cs));
         if (i > 0 && (rc = adaptra_send(d.out_bwd, mb - 1, cs, epoch))) return rc;
+        if (inorder && i > 0 && (rc = adaptra_send_wait(d.out_bwd, mb - 1, epoch))) return rc;
       } else if (o.kind == ADAPTRA_OP_W) {
         int slot = slot_of_mb[mb];
         if (slot < 0) return set_error(ADAPTRA_EINVAL, "exec: W before F");

@@ -239,12 +239,12 @@ class Pipeline:
         if link in self.in_bwd:
             L.check(lib.adaptra_inbox_set_host(self.in_bwd[link], down))
 
-    def run(self, orders, merge_w=False, want_times=False):
+    def run(self, orders, merge_w=False, want_times=False, inorder=False):
         """One iteration.  orders[i] = [(kind, mb), ...] for every stage i (only
         local stages are executed here).  Returns IterResult with local stats."""
         lib = L.lib()
         self.epoch += 1
-        flags = L.MERGE_W if merge_w else 0
+        flags = (L.MERGE_W if merge_w else 0) | (L.EXEC_INORDER if inorder else 0)
         keep = []
         for i in self.local:
             arr = _op_array(orders[i])
@@ -327,6 +327,10 @@ class Arm:
     """Schedule policy for one arm (R18 / R21)."""
 
     def __init__(self, name, S, N, tF, tB, tW, *, x_init=None, ratio=30, x_cap=None):
+        # "<arm>-inorder": same order, executed with blocking sends/receives in
+        # the compute sequence (SURVEY N1: the HOL-blocking baseline)
+        self.inorder = name.endswith("-inorder")
+        name = name[:-len("-inorder")] if self.inorder else name
         self.name, self.S, self.N = name, S, N
         self.tF, self.tB, self.tW = list(tF), list(tB), list(tW)
         self.delta = max(1, max(max(tF), max(tB), max(tW)) // ratio)

@@ -51,7 +51,7 @@ CFGS = [
 ]
 
 
-@pytest.mark.parametrize("arm", ["1f1b", "zb", "adaptive"])
+@pytest.mark.parametrize("arm", ["1f1b", "zb", "adaptive", "zb-inorder", "1f1b-inorder"])
 @pytest.mark.parametrize("kind,dtype,S,N,Lt,d,dff,H,b,T,tol", CFGS)
 def test_pipeline_iteration_matches_full_batch(kind, dtype, S, N, Lt, d, dff, H, b, T, tol, arm):
     pipe, Lref, gref = _setup(kind, dtype, S, N, Lt, d, dff, H, b, T)
@@ -64,7 +64,7 @@ def test_pipeline_iteration_matches_full_batch(kind, dtype, S, N, Lt, d, dff, H,
             pipe.set_latency(S // 2 - 1, c[S // 2 - 1])
         orders = a.plan(c)
         for _ in range(2):                  # twice: epochs / mailbox reuse / zeroed grads
-            res = pipe.run(orders, merge_w=a.merge_w, want_times=True)
+            res = pipe.run(orders, merge_w=a.merge_w, want_times=True, inorder=a.inorder)
         _check(pipe, res, Lref, gref, tol)
         for i, st in res.stats.items():
             assert st["op_cnt"][0] == N
