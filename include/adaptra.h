@@ -264,11 +264,14 @@ int adaptra_stage_zero_grads(adaptra_stage_t s, void* stream);
  *            HOST: D2H into the host ring).
  *   send     enqueues the transfer on the outbox's own stream after the
  *            producing op (never on the compute stream) and posts the flag.
- * Waiting is a one-thread kernel on the consumer stream polling the flag with
- * acquire loads, bounded by $ADAPTRA_TIMEOUT_MS (default 120 s); posting is a
- * one-thread release-store kernel after a system fence.  (Stream memory ops
- * are not used: on this driver a launch behind an unsatisfied stream wait
- * blocks the host.)
+ * Flags live in pinned, device-mapped host memory (POSIX shm, so they can be
+ * mapped by the sender's process); a producer GPU posts a flag with a
+ * one-thread system-scope release-store kernel after its data, the gate and
+ * delegate threads post from the host, and the consuming stage's own host
+ * thread waits on it (bounded by $ADAPTRA_TIMEOUT_MS, default 120 s) before
+ * launching the consuming op -- the paper's busy wait.  Every
+ * stage has its own thread, so a late message delays only the ops that follow
+ * it in that stage's order (no cross-stage head-of-line blocking).
  * Latency injection (R16): with latency c > 0 the flag of each message is
  * posted c ns after its data is in place, by a process-wide gate thread that
  * polls the completion event (no SM use, messages pipeline).  Latency
@@ -288,7 +291,7 @@ typedef struct adaptra_outbox* adaptra_outbox_t;
 /* host_name: NULL = no delegated path for this inbox. */
 int adaptra_inbox_create(int32_t dev, int32_t n_mb, int64_t bytes, const char* host_name, adaptra_inbox_t* out);
 int adaptra_inbox_destroy(adaptra_inbox_t ib);
-/* 128 bytes: CUDA IPC handles of the mailbox and the flags. */
+/* 128 bytes: CUDA IPC handle of the mailbox (64) + name of the flag segment (64). */
 int adaptra_inbox_export(adaptra_inbox_t ib, uint8_t* handle_out);
 void* adaptra_inbox_slot(adaptra_inbox_t ib, int32_t mb);
 /* Enqueue on `consumer` a GPU-side wait (stream memory op, no host blocking,
@@ -365,6 +368,10 @@ int adaptra_exec_destroy(adaptra_exec_t e);
  * head-of-line blocking).  Non-blocking (the stage thread enqueues). */
 #define ADAPTRA_EXEC_INORDER 16u
 int adaptra_run_iteration(adaptra_exec_t e, const adaptra_op_t* ops, int32_t n, uint32_t epoch, uint32_t flags);
+/* Report op times relative to `event` (a cudaEvent_t recorded by the caller on
+ * the stage's device before the iteration; NULL = the stage's own start
+ * event), so that stages sharing a device share one time base. */
+int adaptra_exec_set_time_base(adaptra_exec_t e, void* event);
 /* Wait until the stage thread has enqueued the whole iteration; returns its
  * error, if any (call on every stage before adaptra_exec_wait so that a
  * failed stage can be detected and the others released). */

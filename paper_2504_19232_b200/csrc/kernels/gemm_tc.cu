@@ -41,12 +41,12 @@ constexpr int kWarpProducer = 8, kWarpMma = 9;
 template <int CG, int BN>
 struct TcCfg {
   static constexpr int kBRows = BN / CG;        // B rows held by each CTA
-  static constexpr int kStages = CG == 2 ? 6 : (BN == 256 ? 4 : 6);
+  static constexpr int kStages = CG == 2 ? 5 : (BN == 256 ? 3 : 5);
   static constexpr int kABytes = BM * BK * 2;    // 16 KB
   static constexpr int kBBytes = kBRows * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;       // two accumulators of 128 lanes x BN columns
-  static constexpr int kEpiBytes = kEpiWarps * 4096;  // one 32x32 fp32 staging buffer per epilogue warp
+  static constexpr int kEpiBytes = kEpiWarps * 8192;  // two 32x32 fp32 staging buffers per epilogue warp
   static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int TM = BM * CG;             // tile rows
 };
@@ -112,7 +112,8 @@ __device__ __forceinline__ void epilogue_loop(const adaptra_gemm_desc_t& g, cons
   const int quad = warp & 3;  // TMEM lane quadrant this warp may access
   const int co = (warp >> 2) * (BN / 2);  // first column of this warp's half
   constexpr int NC = BN / 64;            // 32-column chunks per warp
-  uint8_t* stg = sEpi + warp * 4096;
+  uint8_t* stg = sEpi + warp * 8192;
+  int sbuf = 0;
   int acc = 0;
   uint32_t acc_phase = 0;
   const bool f32o = (g.epi == ADAPTRA_EPI_ACC_F32 || g.epi == ADAPTRA_EPI_STORE_F32);
@@ -177,10 +178,11 @@ __device__ __forceinline__ void epilogue_loop(const adaptra_gemm_desc_t& g, cons
           for (int j = 0; j < 32; ++j) bv[j] = (n0 + j < e.N) ? e.bias[n0 + j] : 0.f;
         }
       }
-      // wait until the staging buffer's previous TMA store has read it
-      if (lane == 0) bulk_wait_read<0>();
+      // wait until this staging buffer's previous TMA store has read it
+      if (lane == 0) bulk_wait_read<1>();
       __syncwarp();
-      uint8_t* sb = stg;
+      uint8_t* sb = stg + sbuf * 4096;
+      sbuf ^= 1;
       switch (g.epi) {
         case ADAPTRA_EPI_STORE:
 #pragma unroll

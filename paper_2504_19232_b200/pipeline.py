@@ -153,6 +153,11 @@ class Pipeline:
             h = C.c_void_p()
             L.check(lib.adaptra_exec_create(C.byref(d), C.byref(h)))
             self.execs[i] = h
+        # one time base for all stages of this rank (one device)
+        self._base_stream = torch.cuda.Stream(device=device)
+        self._base_event = torch.cuda.Event(enable_timing=True)
+        for i in self.local:
+            L.check(lib.adaptra_exec_set_time_base(self.execs[i], C.c_void_p(self._base_event.cuda_event)))
         self.epoch = 0
         self.latency = [0] * (S - 1)
         torch.cuda.synchronize(device)
@@ -245,6 +250,7 @@ class Pipeline:
         lib = L.lib()
         self.epoch += 1
         flags = (L.MERGE_W if merge_w else 0) | (L.EXEC_INORDER if inorder else 0)
+        self._base_event.record(self._base_stream)
         keep = []
         for i in self.local:
             arr = _op_array(orders[i])
