@@ -276,6 +276,7 @@ def main():
         return out
 
     # -------- timed arms: headline = adaptive under the trace
+    gem, gem_attn, fused_attn, fused_attn_b = [], [], [], []
     for name in arms:
         results[(name, "trace")] = run_arm(name, True, args.steps, args.warmup, prof=(name == "adaptive"))
         if name == "adaptive":
@@ -285,6 +286,10 @@ def main():
             gem = gather((n.value, ms.value, fl.value, by.value))
             lib.adaptra_prof_collect(2, n, ms, fl, by)
             gem_attn = gather((n.value, ms.value, fl.value, by.value))
+            lib.adaptra_prof_collect(3, n, ms, fl, by)
+            fused_attn = gather((n.value, ms.value, fl.value, by.value))
+            lib.adaptra_prof_collect(4, n, ms, fl, by)
+            fused_attn_b = gather((n.value, ms.value, fl.value, by.value))
         results[(name, "nominal")] = run_arm(name, False, max(3, args.steps // 2), 1)
     e2e = None
     if not args.no_e2e and "adaptive" in arms:
@@ -314,6 +319,20 @@ def main():
             afl = sum(x[2] for x in gem_attn) / na
             attn_line = {"launches": na, "avg_launch_us": round(ams * 1e3, 2),
                          "achieved_tflops": round(afl / (ams / 1e3) / 1e12, 1)}
+        fused_line = {}
+        for nm, src in (("fwd", fused_attn), ("bwd", fused_attn_b)):
+            nf = sum(x[0] for x in src)
+            if nf:
+                fms = sum(x[1] for x in src) / nf
+                ffl = sum(x[2] for x in src) / nf
+                fused_line[nm] = {"launches": nf, "avg_launch_us": round(fms * 1e3, 2),
+                                  "achieved_tflops": round(ffl / (fms / 1e3) / 1e12, 1),
+                                  "frac": round(ffl / (fms / 1e3) / 1e12 / peak, 4)}
+        if fused_line:
+            fused_line["kernel"] = "attn_fwd_kernel / attn_bwd_kernel (+ dq_finalize) (tcgen05, flash-style, causal)"
+            fused_line["flops"] = "algorithmic causal half: fwd 4 T^2 dh H / 2, bwd 8 T^2 dh H / 2 (R28)"
+        else:
+            fused_line = None
         line = {
             "metric": "tokens/sec and bubble rate at 8 stages under injected straggler trace",
             "value": round(head["tokens_per_s"], 1), "unit": "tokens/s", "n_gpus": world,
@@ -341,6 +360,7 @@ def main():
                                  "steps; stages co-located on one GPU run concurrently, which stretches each "
                                  "launch (see profiles/ for serialised ncu shares)",
                          "attention_gemm": attn_line,
+                         "attention_fused": fused_line,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"},
             "clocks": clocks,
             "e2e": e2e,

@@ -2,18 +2,16 @@
 // stage F / B: softmax(Q K^T / sqrt(dh)) V without materialising the
 // T x T scores in HBM.
 //
-// Forward, one CTA per (sequence x head z, 128-query block qb):
-//   pass 1: for key blocks j <= qb: S = Q K_j^T (TMEM) -> row max / sum
-//   pass 2: for key blocks j <= qb: S = Q K_j^T -> P = exp(S/sqrt(dh) - LSE)
-//           (bf16, shared memory) -> O += P V_j (TMEM)
-//   O -> bf16 output, LSE = max + log(sum) (fp32, kept for B).
-// Two passes trade one extra Q K^T per block for exact normalisation without
-// rescaling the TMEM accumulator.
-// Backward, one CTA per (z, 128-key block kb), over query blocks i >= kb:
+// Forward, one CTA per (sequence x head z, 128-query block qb), one pass over
+// key blocks j <= qb: S = Q K_j^T (TMEM) -> online softmax against a lazily
+// moved reference max (P = 2^(S c2 - mref) <= 2^8, bf16, shared memory;
+// O rescaled in TMEM only when mref moves) -> O += P V_j (TMEM);
+// O / l -> bf16 output, LSE = mref + log2(l) (log2 units, kept for B).
+// Backward, one CTA per (z, 128-key block kb), over 64-query blocks i >= 2 kb:
 //   S^T = K Q_i^T, dP^T = V dO_i^T (TMEM) -> P^T = exp(S^T/sqrt(dh) - LSE_i),
 //   dS^T = P^T (dP^T - D_i) (bf16, shared memory) -> dV += P^T dO_i,
-//   dK += dS^T Q_i, dQ_i(partial) = dS K (TMEM) -> TMA reduce-add into an fp32
-//   dQ accumulator.  D_i = rowsum(dO_i o O_i) comes from attn_rowdot.
+//   dK += dS^T Q_i, dQ_i^T(partial) = K^T dS_i^T (TMEM) -> TMA reduce-add into
+//   an fp32 dQ^T accumulator.  D_i = rowsum(dO_i o O_i) comes from attn_rowdot.
 // Warp roles: 0 TMA producer, 1 TMEM allocator + MMA issuer, 2..5 softmax /
 // gradient / epilogue warps (thread = TMEM lane = tile row).
 #include <cuda.h>
@@ -51,20 +49,27 @@ constexpr uint32_t idesc(int a_mn, int b_mn) {
          ((uint32_t)(AT >> 3) << 17) | ((uint32_t)(AT >> 4) << 24);
 }
 
-// store 32 fp32 as bf16 into row r of a K-major SWIZZLE_128B [128 x 128] tile,
-// columns [c0, c0 + 32)
-__device__ __forceinline__ void st_tile_row32(uint8_t* tile, int r, int c0, const float* v) {
-  uint8_t* chunk = tile + (c0 >> 6) * CHUNK + r * 128;
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+// store 32 fp32 as bf16 into row r of a K-major SWIZZLE_128B [128 x 128] tile
+// (shared address `tile`), columns [c0, c0 + 32)
+__device__ __forceinline__ void st_tile_row32(uint32_t tile, int r, int c0, const float* v) {
+  const uint32_t row = tile + (c0 >> 6) * CHUNK + r * 128;
   const int p0 = (c0 & 63) >> 3;  // first 16-byte piece (8 columns) within the 128 B row
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    uint4 u;
-    u.x = pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
-    u.y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
-    u.z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
-    u.w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
-    *reinterpret_cast<uint4*>(chunk + (((p0 + q) ^ (r & 7)) << 4)) = u;
-  }
+  for (int q = 0; q < 4; ++q)
+    sts128(row + (((p0 + q) ^ (r & 7)) << 4), pack_bf16x2(v[8 * q + 0], v[8 * q + 1]),
+           pack_bf16x2(v[8 * q + 2], v[8 * q + 3]), pack_bf16x2(v[8 * q + 4], v[8 * q + 5]),
+           pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
+}
+// same, from 32 values already packed as 16 bf16x2 words
+__device__ __forceinline__ void st_tile_row32_packed(uint32_t tile, int r, int c0, const uint32_t* pk) {
+  const uint32_t row = tile + (c0 >> 6) * CHUNK + r * 128;
+  const int p0 = (c0 & 63) >> 3;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    sts128(row + (((p0 + q) ^ (r & 7)) << 4), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
 }
 
 struct AttnArgs {
@@ -106,17 +111,19 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint8_t* sK = sQ + TILE;                  // 2 stages x 32 KB
   uint8_t* sV = sK + 2 * TILE;              // 2 stages x 32 KB
   uint8_t* sP = sV + 2 * TILE;              // 32 KB
-  float* sStat = (float*)(sP + TILE);       // [2 halves][2 (m, l)][128]
-  uint64_t* bar = (uint64_t*)(sStat + 4 * AT);
+  float* sMax = (float*)(sP + TILE);        // [2 (block parity)][2 halves][128] half-row maxima
+  float* sL = sMax + 4 * AT;                // [2 halves][128] half-row sums
+  uint64_t* bar = (uint64_t*)(sL + 2 * AT);
   uint64_t* q_full = bar + 0;
-  uint64_t* kv_full = bar + 1;   // [2]
-  uint64_t* kv_empty = bar + 3;  // [2]
-  uint64_t* s_full = bar + 5;    // [2]
-  uint64_t* s_empty = bar + 7;   // [2]
-  uint64_t* p_full = bar + 9;
-  uint64_t* p_empty = bar + 10;
-  uint64_t* o_full = bar + 11;
-  uint32_t* tmem_slot = (uint32_t*)(bar + 12);
+  uint64_t* k_full = bar + 1;    // [2]
+  uint64_t* v_full = bar + 3;    // [2]
+  uint64_t* kv_empty = bar + 5;  // [2]
+  uint64_t* s_full = bar + 7;    // [2]
+  uint64_t* s_empty = bar + 9;   // [2]
+  uint64_t* p_full = bar + 11;
+  uint64_t* p_empty = bar + 12;
+  uint64_t* o_full = bar + 13;
+  uint32_t* tmem_slot = (uint32_t*)(bar + 14);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int nqb = a.T / AT, Z = a.b * a.H;
@@ -130,7 +137,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     tma_prefetch(&tm_qkv);
     mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&kv_full[i], 1);
+      mbar_init(&k_full[i], 1);
+      mbar_init(&v_full[i], 1);
       mbar_init(&kv_empty[i], 1);
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], 8);
@@ -151,36 +159,28 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     if (lane == 0) {
       mbar_arrive_expect_tx(q_full, TILE);
       for (int c = 0; c < 2; ++c) tma_load_2d(sQ + c * CHUNK, &tm_qkv, q_full, qcol + 64 * c, row0 + qb * AT);
-      int st = 0;
-      uint32_t ph = 0;
-      for (int pass = 1; pass <= 2; ++pass) {
-        for (int j = 0; j <= qb; ++j) {
-          mbar_wait(&kv_empty[st], ph ^ 1);
-          mbar_arrive_expect_tx(&kv_full[st], pass == 1 ? TILE : 2 * TILE);
-          for (int c = 0; c < 2; ++c)
-            tma_load_2d(sK + st * TILE + c * CHUNK, &tm_qkv, &kv_full[st], kcol + 64 * c, row0 + j * AT);
-          if (pass == 2)
-            for (int c = 0; c < 2; ++c)
-              tma_load_2d(sV + st * TILE + c * CHUNK, &tm_qkv, &kv_full[st], vcol + 64 * c, row0 + j * AT);
-          if (++st == 2) {
-            st = 0;
-            ph ^= 1;
-          }
-        }
+      for (int j = 0; j <= qb; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&k_full[st], TILE);
+        for (int c = 0; c < 2; ++c)
+          tma_load_2d(sK + st * TILE + c * CHUNK, &tm_qkv, &k_full[st], kcol + 64 * c, row0 + j * AT);
+        mbar_arrive_expect_tx(&v_full[st], TILE);
+        for (int c = 0; c < 2; ++c)
+          tma_load_2d(sV + st * TILE + c * CHUNK, &tm_qkv, &v_full[st], vcol + 64 * c, row0 + j * AT);
       }
     }
   } else if (warp == 1) {
-    // Block sequence g = 0..qb (pass 1), qb+1..2qb+1 (pass 2); K/V stage and S
-    // buffer of block g are g & 1, their barrier phase (g >> 1) & 1.  In pass 2
-    // S of block g+1 is issued before waiting for P of block g, so the softmax
-    // warps overlap the tensor pipe.
+    // S of block j+1 is issued before waiting for P of block j, so the softmax
+    // warps overlap the tensor pipe.  K/V stage and S buffer of block j are
+    // j & 1, their barrier phase (j >> 1) & 1.
     mbar_wait(q_full, 0);
     tc_fence_after();
     const uint32_t aQ = smem_u32(sQ), aP = smem_u32(sP);
-    auto issue_s = [&](int gi) {
-      const int st = gi & 1;
-      const uint32_t ph = (gi >> 1) & 1;
-      mbar_wait(&kv_full[st], ph);
+    auto issue_s = [&](int j) {
+      const int st = j & 1;
+      const uint32_t ph = (j >> 1) & 1;
+      mbar_wait(&k_full[st], ph);
       mbar_wait(&s_empty[st], ph ^ 1);
       tc_fence_after();
       if (lane == 0) {
@@ -189,24 +189,21 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         for (int ks = 0; ks < 8; ++ks)
           tc_mma_f16(tmem + st * 128, desc_kmajor(aQ, ks), desc_kmajor(aK, ks), idesc(0, 0), ks > 0 ? 1u : 0u);
         tc_commit(&s_full[st]);
-        if (gi <= qb) tc_commit(&kv_empty[st]);  // pass 1 only needs K
       }
       __syncwarp();
     };
-    for (int gi = 0; gi <= qb; ++gi) issue_s(gi);
-    const int g0 = qb + 1;
-    issue_s(g0);
+    issue_s(0);
     for (int j = 0; j <= qb; ++j) {
-      const int gi = g0 + j;
-      if (j + 1 <= qb) issue_s(gi + 1);
+      if (j + 1 <= qb) issue_s(j + 1);
       mbar_wait(p_full, j & 1);
+      mbar_wait(&v_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
       if (lane == 0) {
-        const uint32_t aV = smem_u32(sV + (gi & 1) * TILE);
+        const uint32_t aV = smem_u32(sV + (j & 1) * TILE);
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
           tc_mma_f16(tO, desc_kmajor(aP, ks), desc_mnmajor(aV, ks), idesc(0, 1), (j > 0 || ks > 0) ? 1u : 0u);
-        tc_commit(&kv_empty[gi & 1]);
+        tc_commit(&kv_empty[j & 1]);
         tc_commit(p_empty);
       }
       __syncwarp();
@@ -214,14 +211,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     if (lane == 0) tc_commit(o_full);
     __syncwarp();
   } else {
-    // softmax warps: lane quadrant quad (rows), column half (64 keys / head dims)
+    // softmax warps: lane quadrant quad (rows), column half (64 keys / head dims).
+    // Online softmax in log2 units against a reference max mref shared by the
+    // two halves of a row (exchanged through sMax every block).  mref moves
+    // only when the running max exceeds it by more than 8, so P <= 2^8 and the
+    // O accumulator in TMEM is rescaled rarely (then by this thread's half).
     const int quad = warp & 3, half = (warp - 2) >> 2;
     const int r = quad * 32 + lane;           // row within the query block
     const int qi = qb * AT + r;               // query position in the sequence
     const uint32_t lanes = ((uint32_t)(quad * 32) << 16) + half * 64;
     const float c2 = a.scale * kLog2e;        // scores in log2 units
-    float m = -INFINITY, l = 0.f;
-    // ---- pass 1: row max and sum (log2 domain) over this half of the keys
+    const int pair_bar = 1 + quad;            // warps quad (half 0) and quad (half 1)
+    float mref = -INFINITY, l = 0.f;
     for (int j = 0; j <= qb; ++j) {
       const int sb = j & 1;
       mbar_wait(&s_full[sb], (j >> 1) & 1);
@@ -234,71 +235,68 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_empty[sb]);
-      float u[64];
-#pragma unroll
-      for (int t = 0; t < 32; ++t) {
-        u[t] = __uint_as_float(r0[t]) * c2;
-        u[32 + t] = __uint_as_float(r1[t]) * c2;
-      }
       if (j == qb) {
-        const int key0 = j * AT + half * 64;
+        const int lim = qi - (j * AT + half * 64);  // last visible column of this half
 #pragma unroll
-        for (int t = 0; t < 64; ++t)
-          if (key0 + t > qi) u[t] = -INFINITY;
+        for (int t = 0; t < 32; ++t) {
+          if (t > lim) r0[t] = __float_as_uint(-INFINITY);
+          if (t + 32 > lim) r1[t] = __float_as_uint(-INFINITY);
+        }
       }
-      float cm = u[0];
+      float cm = fmaxf(__uint_as_float(r0[0]), __uint_as_float(r1[0]));
 #pragma unroll
-      for (int t = 1; t < 64; ++t) cm = fmaxf(cm, u[t]);
-      const float mn = fmaxf(m, cm);
-      if (mn != -INFINITY) {
-        float acc = 0.f;
-#pragma unroll
-        for (int t = 0; t < 64; ++t) acc += ex2(u[t] - mn);
-        l = l * ex2(m - mn) + acc;
-        m = mn;
+      for (int t = 1; t < 32; ++t) cm = fmaxf(cm, fmaxf(__uint_as_float(r0[t]), __uint_as_float(r1[t])));
+      float* mx = sMax + sb * 2 * AT;
+      mx[half * AT + r] = cm;
+      named_sync(pair_bar, 64);
+      // every row has key 0 <= qi in block 0 and key j*128 <= qi in block j: mb is finite
+      const float mb = fmaxf(cm, mx[(half ^ 1) * AT + r]) * c2;
+      const bool resc = mb > mref + 8.f;
+      float alpha = 1.f;
+      if (resc) {
+        alpha = ex2(mref - mb);  // 0 on the first block
+        mref = mb;
       }
-    }
-    // combine the two halves of the row
-    sStat[(half * 2 + 0) * AT + r] = m;
-    sStat[(half * 2 + 1) * AT + r] = l;
-    named_sync(1, 256);
-    const float m0 = sStat[0 * AT + r], l0 = sStat[1 * AT + r];
-    const float m1 = sStat[2 * AT + r], l1 = sStat[3 * AT + r];
-    const float M = fmaxf(m0, m1);
-    const float lse2 = M + __log2f(l0 * ex2(m0 - M) + l1 * ex2(m1 - M));
-    // ---- pass 2: P = 2^(S c2 - lse2) -> shared memory
-    for (int j = 0; j <= qb; ++j) {
-      const int gi = qb + 1 + j, sb = gi & 1;
-      mbar_wait(&s_full[sb], (gi >> 1) & 1);
-      tc_fence_after();
-      uint32_t r0[32], r1[32];
-      tmem_ld32(tmem + sb * 128 + lanes, r0);
-      tmem_ld32(tmem + sb * 128 + lanes + 32, r1);
-      tmem_ld_wait_regs(r0);
-      tmem_ld_wait_regs(r1);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[sb]);
-      float p[64];
+      uint32_t pk[32];  // P row half as bf16x2
+      float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
-      for (int t = 0; t < 32; ++t) {
-        p[t] = ex2(fmaf(__uint_as_float(r0[t]), c2, -lse2));
-        p[32 + t] = ex2(fmaf(__uint_as_float(r1[t]), c2, -lse2));
+      for (int t = 0; t < 32; t += 2) {
+        const float e0 = ex2(fmaf(__uint_as_float(r0[t]), c2, -mref));
+        const float e1 = ex2(fmaf(__uint_as_float(r0[t + 1]), c2, -mref));
+        const float e2 = ex2(fmaf(__uint_as_float(r1[t]), c2, -mref));
+        const float e3 = ex2(fmaf(__uint_as_float(r1[t + 1]), c2, -mref));
+        acc0 += e0 + e1;
+        acc1 += e2 + e3;
+        pk[t >> 1] = pack_bf16x2(e0, e1);
+        pk[16 + (t >> 1)] = pack_bf16x2(e2, e3);
       }
-      if (j == qb) {
-        const int key0 = j * AT + half * 64;
+      l = l * alpha + (acc0 + acc1);
+      mbar_wait(p_empty, (j & 1) ^ 1);  // P V of block j-1 done: O stable, P buffer free
+      if (j > 0 && __any_sync(0xffffffffu, resc)) {
+        tc_fence_after();
 #pragma unroll
-        for (int t = 0; t < 64; ++t)
-          if (key0 + t > qi) p[t] = 0.f;
+        for (int c = 0; c < 2; ++c) {
+          uint32_t o[32];
+          tmem_ld32(tO + lanes + 32 * c, o);
+          tmem_ld_wait_regs(o);
+#pragma unroll
+          for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * alpha);
+          tmem_st32(tO + lanes + 32 * c, o);
+        }
+        tmem_st_wait();
       }
-      mbar_wait(p_empty, (j & 1) ^ 1);  // previous P V has read the P buffer
-      st_tile_row32(sP, r, half * 64, p);
-      st_tile_row32(sP, r, half * 64 + 32, p + 32);
+      st_tile_row32_packed(smem_u32(sP), r, half * 64, pk);
+      st_tile_row32_packed(smem_u32(sP), r, half * 64 + 32, pk + 16);
       fence_proxy_async_smem();
+      tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
     }
-    // ---- epilogue: O -> bf16 (this half of the head dims), LSE (log2 units)
+    // ---- epilogue: O / l -> bf16 (this half of the head dims), LSE (log2 units)
+    sL[half * AT + r] = l;
+    named_sync(pair_bar, 64);
+    const float ltot = sL[r] + sL[AT + r];
+    const float inv = 1.f / ltot;
     mbar_wait(o_full, 0);
     tc_fence_after();
     bf16* orow = a.o + (size_t)(row0 + qi) * a.d + h * AT + half * 64;
@@ -310,12 +308,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     float v[64];
 #pragma unroll
     for (int t = 0; t < 32; ++t) {
-      v[t] = __uint_as_float(r0[t]);
-      v[32 + t] = __uint_as_float(r1[t]);
+      v[t] = __uint_as_float(r0[t]) * inv;
+      v[32 + t] = __uint_as_float(r1[t]) * inv;
     }
 #pragma unroll
     for (int t = 0; t < 64; t += 8) st_bf16x8(orow + t, v + t);
-    if (half == 0) a.lse[(size_t)z * a.T + qi] = lse2;
+    if (half == 0) a.lse[(size_t)z * a.T + qi] = mref + __log2f(ltot);
   }
   tc_fence_before();
   __syncthreads();
@@ -324,31 +322,55 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 }
 
 // ============================================================== backward
+// One CTA per (z, 128-key block kb), over 64-query blocks i >= 2 kb.  TMEM
+// columns: dK [0,128), dV [128,256), S^T x2 [256,384), dP^T [384,448),
+// dQ^T [448,512) -- no aliasing, so S^T / dP^T of block i+1 run on the tensor
+// pipe while the gradient warps turn block i into P^T, dS^T and while
+// dV, dK, dQ^T of block i accumulate.  dQ^T = K^T dS^T (M = head dims) keeps
+// every MMA at M = 128; it is reduce-added into an fp32 accumulator laid out
+// [z][head dim][T] that dq_finalize transposes into dqkv.
+constexpr int QB = 64;                 // queries per backward step
+constexpr int QCHUNK = QB * 128;       // [64 rows x 64 cols] bf16 SWIZZLE_128B chunk (8 KB)
+constexpr int QTILE = 2 * QCHUNK;      // [64 x 128] bf16
+
+__device__ __forceinline__ uint64_t desc_kmajor_c(uint32_t base, int ks, int chunk) {
+  return umma_desc_sw128(base + (ks >> 2) * chunk + (ks & 3) * 32, 16, 1024);
+}
+__device__ __forceinline__ uint64_t desc_mnmajor_c(uint32_t base, int ks, int chunk) {
+  return umma_desc_sw128(base + ks * 2048, chunk, 1024);
+}
+constexpr uint32_t idesc_n(int a_mn, int b_mn, int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(n >> 3) << 17) | ((uint32_t)(AT >> 4) << 24);
+}
+
 __global__ void __launch_bounds__(kAttnThreads, 1)
-    attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-                    const __grid_constant__ CUtensorMap tm_dq, const AttnArgs a) {
+    attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
+                    const __grid_constant__ CUtensorMap tm_do, const __grid_constant__ CUtensorMap tm_dq,
+                    const AttnArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* sK = smem;            // 32 KB
-  uint8_t* sV = sK + TILE;       // 32 KB
-  uint8_t* sQ = sV + TILE;       // 32 KB (query block i)
-  uint8_t* sdO = sQ + TILE;      // 32 KB
-  uint8_t* sPT = sdO + TILE;     // 32 KB  P^T  [keys x queries]
-  uint8_t* sdST = sPT + TILE;    // 32 KB  dS^T [keys x queries]
-  uint8_t* sStg = sdST + TILE;   // 8 warps x 4 KB dQ staging
-  float* sLse = (float*)(sStg + 8 * 4096);  // [128] (log2 units)
-  float* sD = sLse + AT;                    // [128]
-  uint64_t* bar = (uint64_t*)(sD + AT);
+  uint8_t* sK = smem;               // 32 KB
+  uint8_t* sV = sK + TILE;          // 32 KB
+  uint8_t* sQ = sV + TILE;          // 2 stages x 16 KB  (query block i)
+  uint8_t* sdO = sQ + 2 * QTILE;    // 2 stages x 16 KB
+  uint8_t* sPT = sdO + 2 * QTILE;   // 2 buffers x 16 KB  P^T  [128 keys x 64 queries]
+  uint8_t* sdST = sPT + 2 * QTILE;  // 2 buffers x 16 KB  dS^T [128 keys x 64 queries]
+  uint8_t* sStg = sdST + 2 * QTILE; // 8 warps x 4 KB dQ^T staging
+  float* sLse = (float*)(sStg + 8 * 4096);  // [2 stages][64] (log2 units)
+  float* sD = sLse + 2 * QB;                // [2 stages][64]
+  uint64_t* bar = (uint64_t*)(sD + 2 * QB);
   uint64_t* kv_full = bar + 0;
-  uint64_t* qd_full = bar + 1;
-  uint64_t* qd_empty = bar + 2;
-  uint64_t* sd_full = bar + 3;   // S^T and dP^T in TMEM
-  uint64_t* pd_full = bar + 4;   // P^T, dS^T in smem (8 warps)
-  uint64_t* pd_empty = bar + 5;  // MMAs done reading P^T, dS^T
-  uint64_t* dq_full = bar + 6;   // dQ partial in TMEM
-  uint64_t* dq_empty = bar + 7;  // dQ drained (8 warps)
-  uint64_t* kv_done = bar + 8;   // dK, dV final
-  uint32_t* tmem_slot = (uint32_t*)(bar + 9);
+  uint64_t* qd_full = bar + 1;   // [2] Q_i, dO_i, LSE_i, D_i landed
+  uint64_t* qd_empty = bar + 3;  // [2] dV, dK of block i done
+  uint64_t* s_full = bar + 5;    // [2] S^T in TMEM
+  uint64_t* dp_full = bar + 7;   // dP^T in TMEM
+  uint64_t* pd_full = bar + 8;   // [2] P^T, dS^T in smem; S^T and dP^T read (8 warps)
+  uint64_t* pd_empty = bar + 10; // [2] dV, dK, dQ^T done reading P^T / dS^T
+  uint64_t* dq_full = bar + 12;  // dQ^T in TMEM
+  uint64_t* dq_empty = bar + 13; // dQ^T read (8 warps)
+  uint64_t* kv_done = bar + 14;  // dK, dV final
+  uint32_t* tmem_slot = (uint32_t*)(bar + 15);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int nb = a.T / AT, Z = a.b * a.H;
@@ -357,17 +379,22 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   const int s = z / a.H, h = z % a.H;
   const int row0 = s * a.T;
   const int qcol = h * AT, kcol = a.d + h * AT, vcol = 2 * a.d + h * AT;
+  const int i0 = 2 * kb, n_it = 2 * (nb - kb);  // 64-query blocks i0 .. i0 + n_it - 1
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch(&tm_qkv);
+    tma_prefetch(&tm_kv);
+    tma_prefetch(&tm_q);
     tma_prefetch(&tm_do);
     tma_prefetch(&tm_dq);
     mbar_init(kv_full, 1);
-    mbar_init(qd_full, 1);
-    mbar_init(qd_empty, 1);
-    mbar_init(sd_full, 1);
-    mbar_init(pd_full, 8);
-    mbar_init(pd_empty, 1);
+    for (int k = 0; k < 2; ++k) {
+      mbar_init(&qd_full[k], 1);
+      mbar_init(&qd_empty[k], 1);
+      mbar_init(&s_full[k], 1);
+      mbar_init(&pd_full[k], 8);
+      mbar_init(&pd_empty[k], 1);
+    }
+    mbar_init(dp_full, 1);
     mbar_init(dq_full, 1);
     mbar_init(dq_empty, 8);
     mbar_init(kv_done, 1);
@@ -378,155 +405,174 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS = tmem, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 384;
-  const uint32_t tdQ = tmem;  // reuses the S^T columns once they are consumed
+  const uint32_t tdK = tmem, tdV = tmem + 128, tS = tmem + 256, tdP = tmem + 384, tdQ = tmem + 448;
 
   if (warp == 0) {
     if (lane == 0) {
       mbar_arrive_expect_tx(kv_full, 2 * TILE);
       for (int c = 0; c < 2; ++c) {
-        tma_load_2d(sK + c * CHUNK, &tm_qkv, kv_full, kcol + 64 * c, row0 + kb * AT);
-        tma_load_2d(sV + c * CHUNK, &tm_qkv, kv_full, vcol + 64 * c, row0 + kb * AT);
+        tma_load_2d(sK + c * CHUNK, &tm_kv, kv_full, kcol + 64 * c, row0 + kb * AT);
+        tma_load_2d(sV + c * CHUNK, &tm_kv, kv_full, vcol + 64 * c, row0 + kb * AT);
       }
-      uint32_t ph = 0;
-      for (int i = kb; i < nb; ++i) {
-        mbar_wait(qd_empty, ph ^ 1);
-        mbar_arrive_expect_tx(qd_full, 2 * TILE + 2 * AT * 4);
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it & 1, i = i0 + it;
+        mbar_wait(&qd_empty[st], ((it >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&qd_full[st], 2 * QTILE + 2 * QB * 4);
         for (int c = 0; c < 2; ++c) {
-          tma_load_2d(sQ + c * CHUNK, &tm_qkv, qd_full, qcol + 64 * c, row0 + i * AT);
-          tma_load_2d(sdO + c * CHUNK, &tm_do, qd_full, h * AT + 64 * c, row0 + i * AT);
+          tma_load_2d(sQ + st * QTILE + c * QCHUNK, &tm_q, &qd_full[st], qcol + 64 * c, row0 + i * QB);
+          tma_load_2d(sdO + st * QTILE + c * QCHUNK, &tm_do, &qd_full[st], h * AT + 64 * c, row0 + i * QB);
         }
-        bulk_g2s(sLse, a.lse + (size_t)z * a.T + i * AT, AT * 4, qd_full);
-        bulk_g2s(sD, a.D + (size_t)z * a.T + i * AT, AT * 4, qd_full);
-        ph ^= 1;
+        bulk_g2s(sLse + st * QB, a.lse + (size_t)z * a.T + i * QB, QB * 4, &qd_full[st]);
+        bulk_g2s(sD + st * QB, a.D + (size_t)z * a.T + i * QB, QB * 4, &qd_full[st]);
       }
     }
   } else if (warp == 1) {
     mbar_wait(kv_full, 0);
     tc_fence_after();
-    const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aQ = smem_u32(sQ), adO = smem_u32(sdO);
-    const uint32_t aPT = smem_u32(sPT), adST = smem_u32(sdST);
-    uint32_t ph = 0;
-    for (int i = kb; i < nb; ++i) {
-      mbar_wait(qd_full, ph);
-      mbar_wait(dq_empty, ph ^ 1);  // S^T / dQ columns free
+    const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
+    auto issue_s = [&](int it) {  // S^T = K Q_i^T  -> buffer it & 1
+      const int st = it & 1;
+      mbar_wait(&qd_full[st], (it >> 1) & 1);
       tc_fence_after();
       if (lane == 0) {
+        const uint32_t aQ = smem_u32(sQ + st * QTILE);
 #pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {
-          tc_mma_f16(tS, desc_kmajor(aK, ks), desc_kmajor(aQ, ks), idesc(0, 0), ks > 0 ? 1u : 0u);
-          tc_mma_f16(tdP, desc_kmajor(aV, ks), desc_kmajor(adO, ks), idesc(0, 0), ks > 0 ? 1u : 0u);
-        }
-        tc_commit(sd_full);
+        for (int ks = 0; ks < 8; ++ks)
+          tc_mma_f16(tS + st * QB, desc_kmajor(aK, ks), desc_kmajor_c(aQ, ks, QCHUNK), idesc_n(0, 0, QB),
+                     ks > 0 ? 1u : 0u);
+        tc_commit(&s_full[st]);
       }
       __syncwarp();
-      mbar_wait(pd_full, ph);
+    };
+    auto issue_dp = [&](int it) {  // dP^T = V dO_i^T (Q_i / dO_i stage already waited on)
+      if (lane == 0) {
+        const uint32_t adO = smem_u32(sdO + (it & 1) * QTILE);
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+          tc_mma_f16(tdP, desc_kmajor(aV, ks), desc_kmajor_c(adO, ks, QCHUNK), idesc_n(0, 0, QB),
+                     ks > 0 ? 1u : 0u);
+        tc_commit(dp_full);
+      }
+      __syncwarp();
+    };
+    issue_s(0);
+    issue_dp(0);
+    for (int it = 0; it < n_it; ++it) {
+      const int st = it & 1;
+      const uint32_t ph = (it >> 1) & 1;
+      if (it + 1 < n_it) issue_s(it + 1);  // S^T buffer (it+1)&1 was released by pd_full(it-1)
+      mbar_wait(&pd_full[st], ph);         // P^T, dS^T of block it in smem; dP^T read
+      tc_fence_after();
+      if (it + 1 < n_it) issue_dp(it + 1);
+      if (lane == 0) {
+        const uint32_t acc = it > 0 ? 1u : 0u;
+        const uint32_t aQ = smem_u32(sQ + st * QTILE), adO = smem_u32(sdO + st * QTILE);
+        const uint32_t aPT = smem_u32(sPT + st * QTILE), adST = smem_u32(sdST + st * QTILE);
+#pragma unroll
+        for (int ks = 0; ks < QB / 16; ++ks) {
+          // dV += P^T dO_i ; dK += dS^T Q_i  (K = 64 queries; B operands read MN-major)
+          tc_mma_f16(tdV, desc_kmajor(aPT, ks), desc_mnmajor_c(adO, ks, QCHUNK), idesc_n(0, 1, AT),
+                     (acc || ks > 0) ? 1u : 0u);
+          tc_mma_f16(tdK, desc_kmajor(adST, ks), desc_mnmajor_c(aQ, ks, QCHUNK), idesc_n(0, 1, AT),
+                     (acc || ks > 0) ? 1u : 0u);
+        }
+        tc_commit(&qd_empty[st]);
+      }
+      __syncwarp();
+      mbar_wait(dq_empty, (it & 1) ^ 1);  // dQ^T of block it-1 drained
       tc_fence_after();
       if (lane == 0) {
-        const uint32_t acc = (i > kb) ? 1u : 0u;
+        const uint32_t adST = smem_u32(sdST + st * QTILE);
 #pragma unroll
-        for (int ks = 0; ks < 8; ++ks)  // dQ_i = dS K first: its drain overlaps dV, dK
-          tc_mma_f16(tdQ, desc_mnmajor(adST, ks), desc_mnmajor(aK, ks), idesc(1, 1), ks > 0 ? 1u : 0u);
+        for (int ks = 0; ks < 8; ++ks)  // dQ_i^T = K^T dS_i^T  (both operands MN-major, K = 128 keys)
+          tc_mma_f16(tdQ, desc_mnmajor(aK, ks), desc_mnmajor_c(adST, ks, QCHUNK), idesc_n(1, 1, QB),
+                     ks > 0 ? 1u : 0u);
         tc_commit(dq_full);
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {
-          // dV += P^T dO_i ; dK += dS^T Q_i  (B operands read MN-major)
-          tc_mma_f16(tdV, desc_kmajor(aPT, ks), desc_mnmajor(adO, ks), idesc(0, 1), (acc || ks > 0) ? 1u : 0u);
-          tc_mma_f16(tdK, desc_kmajor(adST, ks), desc_mnmajor(aQ, ks), idesc(0, 1), (acc || ks > 0) ? 1u : 0u);
-        }
-        tc_commit(pd_empty);
-        tc_commit(qd_empty);
+        tc_commit(&pd_empty[st]);
       }
       __syncwarp();
-      ph ^= 1;
     }
     if (lane == 0) tc_commit(kv_done);
     __syncwarp();
   } else {
     const int quad = warp & 3, half = (warp - 2) >> 2;
-    const int r = quad * 32 + lane;  // key row (S^T, dP^T, dK, dV) / query row (dQ)
+    const int r = quad * 32 + lane;  // key row (S^T, dP^T, dK, dV) / head-dim row (dQ^T)
     const int kj = kb * AT + r;      // key position
-    const uint32_t lanes = ((uint32_t)(quad * 32) << 16) + half * 64;
+    const uint32_t lanes = (uint32_t)(quad * 32) << 16;
     const float c2 = a.scale * kLog2e;
     uint8_t* stg = sStg + (warp - 2) * 4096;
-    uint32_t ph = 0;
-    for (int i = kb; i < nb; ++i) {
-      mbar_wait(sd_full, ph);
+    auto drain = [&](int it) {  // dQ^T of block it: 32 head-dim rows x 32 queries per warp
+      mbar_wait(dq_full, it & 1);
       tc_fence_after();
-      uint32_t rs0[32], rs1[32];
-      tmem_ld32(tS + lanes, rs0);
-      tmem_ld32(tS + lanes + 32, rs1);
-      tmem_ld_wait_regs(rs0);
-      tmem_ld_wait_regs(rs1);
-      float p[64], ds[64];
-      const int q0 = i * AT + half * 64;
-      const float* lse = sLse + half * 64;
-      const float* Dq = sD + half * 64;
-#pragma unroll
-      for (int t = 0; t < 32; ++t) {
-        p[t] = ex2(fmaf(__uint_as_float(rs0[t]), c2, -lse[t]));
-        p[32 + t] = ex2(fmaf(__uint_as_float(rs1[t]), c2, -lse[32 + t]));
-      }
-      if (i == kb) {
-#pragma unroll
-        for (int t = 0; t < 64; ++t)
-          if (q0 + t < kj) p[t] = 0.f;
-      }
-      tmem_ld32(tdP + lanes, rs0);
-      tmem_ld32(tdP + lanes + 32, rs1);
-      tmem_ld_wait_regs(rs0);
-      tmem_ld_wait_regs(rs1);
-#pragma unroll
-      for (int t = 0; t < 32; ++t) {
-        ds[t] = p[t] * (__uint_as_float(rs0[t]) - Dq[t]);
-        ds[32 + t] = p[32 + t] * (__uint_as_float(rs1[t]) - Dq[32 + t]);
-      }
-      mbar_wait(pd_empty, ph ^ 1);  // previous MMAs done reading P^T / dS^T
-      st_tile_row32(sPT, r, half * 64, p);
-      st_tile_row32(sPT, r, half * 64 + 32, p + 32);
-      st_tile_row32(sdST, r, half * 64, ds);
-      st_tile_row32(sdST, r, half * 64 + 32, ds + 32);
-      tc_fence_before();
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(pd_full);
-      // dQ partial (thread = query row, this half of the head dims) -> TMA reduce-add
-      mbar_wait(dq_full, ph);
-      tc_fence_after();
-      uint32_t rq0[32], rq1[32];
-      tmem_ld32(tdQ + lanes, rq0);
-      tmem_ld32(tdQ + lanes + 32, rq1);
-      tmem_ld_wait_regs(rq0);
-      tmem_ld_wait_regs(rq1);
+      uint32_t rq[32];
+      tmem_ld32(tdQ + lanes + half * 32, rq);
+      tmem_ld_wait_regs(rq);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(dq_empty);
-      auto drain = [&](const uint32_t(&rq)[32], int c) {
-        if (lane == 0) bulk_wait_read<0>();
-        __syncwarp();
-        uint8_t* frow = stg + lane * 128;
+      if (lane == 0) bulk_wait_read<0>();
+      __syncwarp();
+      const uint32_t frow = smem_u32(stg) + lane * 128;
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          *reinterpret_cast<float4*>(frow + ((q ^ (lane & 7)) << 4)) =
-              make_float4(__uint_as_float(rq[4 * q]) * a.scale, __uint_as_float(rq[4 * q + 1]) * a.scale,
-                          __uint_as_float(rq[4 * q + 2]) * a.scale, __uint_as_float(rq[4 * q + 3]) * a.scale);
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          tma_reduce_add_2d(&tm_dq, stg, h * AT + half * 64 + c * 32, row0 + i * AT + quad * 32);
-          bulk_commit();
-        }
-      };
-      drain(rq0, 0);
-      drain(rq1, 1);
-      ph ^= 1;
+      for (int q = 0; q < 8; ++q)
+        sts128(frow + ((q ^ (lane & 7)) << 4), __float_as_uint(__uint_as_float(rq[4 * q]) * a.scale),
+               __float_as_uint(__uint_as_float(rq[4 * q + 1]) * a.scale),
+               __float_as_uint(__uint_as_float(rq[4 * q + 2]) * a.scale),
+               __float_as_uint(__uint_as_float(rq[4 * q + 3]) * a.scale));
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_reduce_add_2d(&tm_dq, stg, (i0 + it) * QB + half * 32, z * AT + quad * 32);
+        bulk_commit();
+      }
+    };
+    for (int it = 0; it < n_it; ++it) {
+      const int st = it & 1, i = i0 + it;
+      const uint32_t ph = (it >> 1) & 1;
+      mbar_wait(&s_full[st], ph);
+      tc_fence_after();
+      uint32_t rs[32];
+      tmem_ld32(tS + st * QB + lanes + half * 32, rs);
+      tmem_ld_wait_regs(rs);
+      const float* lse = sLse + st * QB + half * 32;
+      const float* Dq = sD + st * QB + half * 32;
+      float p[32];
+#pragma unroll
+      for (int t = 0; t < 32; ++t) p[t] = ex2(fmaf(__uint_as_float(rs[t]), c2, -lse[t]));
+      if (it < 2) {  // diagonal: queries before this key are masked
+        const int lim = kj - (i * QB + half * 32);
+#pragma unroll
+        for (int t = 0; t < 32; ++t)
+          if (t < lim) p[t] = 0.f;
+      }
+      mbar_wait(dp_full, it & 1);
+      tc_fence_after();
+      tmem_ld32(tdP + lanes + half * 32, rs);
+      tmem_ld_wait_regs(rs);
+      uint32_t pkp[16], pkd[16];  // P^T, dS^T row pieces as bf16x2
+#pragma unroll
+      for (int t = 0; t < 32; t += 2) {
+        const float d0 = p[t] * (__uint_as_float(rs[t]) - Dq[t]);
+        const float d1 = p[t + 1] * (__uint_as_float(rs[t + 1]) - Dq[t + 1]);
+        pkp[t >> 1] = pack_bf16x2(p[t], p[t + 1]);
+        pkd[t >> 1] = pack_bf16x2(d0, d1);
+      }
+      mbar_wait(&pd_empty[st], ph ^ 1);  // MMAs of block it-2 done with this buffer
+      st_tile_row32_packed(smem_u32(sPT + st * QTILE), r, half * 32, pkp);
+      st_tile_row32_packed(smem_u32(sdST + st * QTILE), r, half * 32, pkd);
+      tc_fence_before();
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pd_full[st]);
+      if (it > 0) drain(it - 1);
     }
+    drain(n_it - 1);
     if (lane == 0) bulk_wait<0>();
     // dK (scaled), dV -> bf16 into dqkv (k and v sections), thread = key row
     mbar_wait(kv_done, 0);
     tc_fence_after();
     for (int which = 0; which < 2; ++which) {
-      const uint32_t tb = (which == 0 ? tdK : tdV) + lanes;
+      const uint32_t tb = (which == 0 ? tdK : tdV) + lanes + half * 64;
       bf16* out = a.dqkv + (size_t)(row0 + kj) * 3 * a.d + (which == 0 ? a.d : 2 * a.d) + h * AT + half * 64;
       const float sc = which == 0 ? a.scale : 1.f;
       uint32_t r0[32], r1[32];
@@ -550,25 +596,39 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
-// dQ (fp32 accumulator) -> bf16 q section of dqkv; clears the accumulator.
-// One thread per 8 consecutive elements of a row (32-bit index math, 16 B
-// stores).
-__global__ void __launch_bounds__(256) dq_finalize_kernel(float* __restrict__ acc, bf16* __restrict__ dqkv, int rows,
-                                                          int d) {
-  const int per_row = d / 8;
-  const int n = rows * per_row;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    const int r = k / per_row, c = (k - r * per_row) * 8;
-    float4* src = reinterpret_cast<float4*>(acc + (size_t)r * d + c);
-    float4 v0 = src[0], v1 = src[1];
-    src[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-    src[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+// dQ^T (fp32 accumulator [z][head dim][T]) -> bf16 q section of dqkv
+// ([b*T, 3d], row s*T + t, column h*128 + c); clears the accumulator.  One
+// block per (z, 64 positions): all 16 loads per thread are issued before any
+// store (coalesced 256 B row pieces along t), then 16 B writes along c.
+constexpr int kFinT = 64;
+__global__ void __launch_bounds__(256) dq_finalize_kernel(float* __restrict__ acc, bf16* __restrict__ dqkv, int H,
+                                                          int T, int d) {
+  __shared__ float tile[AT][kFinT + 1];
+  const int z = blockIdx.y, t0 = blockIdx.x * kFinT;
+  const int s = z / H, h = z % H;
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  float2* src = reinterpret_cast<float2*>(acc + (size_t)z * AT * T + t0) + lane;
+  const int T2 = T / 2;
+  float2 v[AT / 8];
+#pragma unroll
+  for (int k = 0; k < AT / 8; ++k) v[k] = src[(size_t)(w + 8 * k) * T2];
+#pragma unroll
+  for (int k = 0; k < AT / 8; ++k) {
+    tile[w + 8 * k][2 * lane] = v[k].x;
+    tile[w + 8 * k][2 * lane + 1] = v[k].y;
+  }
+#pragma unroll
+  for (int k = 0; k < AT / 8; ++k) src[(size_t)(w + 8 * k) * T2] = make_float2(0.f, 0.f);
+  __syncthreads();
+#pragma unroll
+  for (int k = threadIdx.x; k < kFinT * (AT / 8); k += 256) {
+    const int t = k / (AT / 8), c0 = (k % (AT / 8)) * 8;
     uint4 u;
-    u.x = pack_bf16x2(v0.x, v0.y);
-    u.y = pack_bf16x2(v0.z, v0.w);
-    u.z = pack_bf16x2(v1.x, v1.y);
-    u.w = pack_bf16x2(v1.z, v1.w);
-    *reinterpret_cast<uint4*>(dqkv + (size_t)r * 3 * d + c) = u;
+    u.x = pack_bf16x2(tile[c0 + 0][t], tile[c0 + 1][t]);
+    u.y = pack_bf16x2(tile[c0 + 2][t], tile[c0 + 3][t]);
+    u.z = pack_bf16x2(tile[c0 + 4][t], tile[c0 + 5][t]);
+    u.w = pack_bf16x2(tile[c0 + 6][t], tile[c0 + 7][t]);
+    *reinterpret_cast<uint4*>(dqkv + (size_t)(s * T + t0 + t) * 3 * d + h * AT + c0) = u;
   }
 }
 
@@ -606,8 +666,8 @@ static int check_launch(const char* w) {
   return ADAPTRA_OK;
 }
 
-constexpr int kFwdSmem = 6 * TILE + 4 * AT * 4 + 1024 + 256;
-constexpr int kBwdSmem = 6 * TILE + 8 * 4096 + 2 * AT * 4 + 1024 + 256;
+constexpr int kFwdSmem = 6 * TILE + 6 * AT * 4 + 1024 + 256;
+constexpr int kBwdSmem = 2 * TILE + 8 * QTILE + 8 * 4096 + 4 * QB * 4 + 1024 + 256;
 
 int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d, cudaStream_t st) {
   if (d != H * AT || T % AT) return set_error(ADAPTRA_EINVAL, "attn_fwd_tc: head dim 128 and T % 128 required");
@@ -638,10 +698,11 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
 int attn_bwd_tc(const bf16* qkv, const bf16* dO, const float* lse, const float* D, bf16* dqkv, float* dq_acc, int b,
                 int H, int T, int d, cudaStream_t st) {
   if (d != H * AT || T % AT) return set_error(ADAPTRA_EINVAL, "attn_bwd_tc: head dim 128 and T % 128 required");
-  CUtensorMap mq, mdo, mdq;
-  int rc = map2d(&mq, qkv, (int64_t)b * T, 3LL * d, 3LL * d, 2, 64, AT, CU_TENSOR_MAP_SWIZZLE_128B);
-  if (!rc) rc = map2d(&mdo, dO, (int64_t)b * T, d, d, 2, 64, AT, CU_TENSOR_MAP_SWIZZLE_128B);
-  if (!rc) rc = map2d(&mdq, dq_acc, (int64_t)b * T, d, d, 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+  CUtensorMap mkv, mq, mdo, mdq;
+  int rc = map2d(&mkv, qkv, (int64_t)b * T, 3LL * d, 3LL * d, 2, 64, AT, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!rc) rc = map2d(&mq, qkv, (int64_t)b * T, 3LL * d, 3LL * d, 2, 64, QB, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!rc) rc = map2d(&mdo, dO, (int64_t)b * T, d, d, 2, 64, QB, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!rc) rc = map2d(&mdq, dq_acc, (int64_t)b * H * AT, T, T, 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   static unsigned attr = 0;
   int dev = 0;
@@ -658,15 +719,14 @@ int attn_bwd_tc(const bf16* qkv, const bf16* dO, const float* lse, const float* 
   a.dqkv = dqkv;
   a.dq_acc = dq_acc;
   void* pb = prof_on() ? prof_begin(st) : nullptr;
-  attn_bwd_kernel<<<b * H * (T / AT), kAttnThreads, kBwdSmem, st>>>(mq, mdo, mdq, a);
+  attn_bwd_kernel<<<b * H * (T / AT), kAttnThreads, kBwdSmem, st>>>(mkv, mq, mdo, mdq, a);
   if (pb) {
     double fl = 8.0 * (double)T * T * AT * b * H * 0.5;  // dP, dV, dK, dQ (causal half)
-    prof_end(pb, st, PROF_ATTN, fl, 0);
+    prof_end(pb, st, PROF_ATTN_BWD, fl, 0);
   }
   rc = check_launch("attn_bwd_tc");
   if (rc) return rc;
-  const int n8 = b * T * (d / 8);
-  dq_finalize_kernel<<<std::min(148 * 8, (n8 + 255) / 256), 256, 0, st>>>(dq_acc, dqkv, b * T, d);
+  dq_finalize_kernel<<<dim3(T / kFinT, b * H), 256, 0, st>>>(dq_acc, dqkv, H, T, d);
   return check_launch("dq_finalize");
 }
 

@@ -2,7 +2,7 @@
 #include <cuda_runtime.h>
 
 namespace adaptra {
-enum { PROF_GEMM_TC = 0, PROF_GEMM_SIMT = 1, PROF_GEMM_ATTN = 2, PROF_ATTN = 3 };
+enum { PROF_GEMM_TC = 0, PROF_GEMM_SIMT = 1, PROF_GEMM_ATTN = 2, PROF_ATTN = 3, PROF_ATTN_BWD = 4 };
 bool prof_on();
 void count_launch();
 long long launch_count();

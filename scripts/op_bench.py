@@ -20,8 +20,11 @@ x = [torch.randn(T, d, device="cuda").to(torch.bfloat16) for _ in range(4)]
 y = [st.act() for _ in range(4)]
 dy = [torch.randn(T, d, device="cuda").to(torch.bfloat16) * 0.01 for _ in range(4)]
 dx = [st.act() for _ in range(4)]
+import ctypes  # noqa: E402
+
 res = {}
 for rep in range(3):
+    L.lib().adaptra_prof_enable(1 if rep == 2 else 0)
     ev = {k: (torch.cuda.Event(True), torch.cuda.Event(True)) for k in "FBW"}
     ev["F"][0].record()
     for j in range(4):
@@ -42,4 +45,12 @@ af = 2 * T * T * d * nl / 1e9
 res.update({"layers": nl, "attn": os.environ.get("ADAPTRA_ATTN", "fused"),
             "F_tflops": round((gf + af) / res["F"] / 1e3, 1), "B_tflops": round((gf + 2 * af) / res["B"] / 1e3, 1),
             "W_tflops": round(gf / res["W"] / 1e3, 1)})
+L.lib().adaptra_prof_enable(0)
+names = {0: "gemm_tc", 2: "gemm_attn", 3: "attn_fwd", 4: "attn_bwd"}
+for kind, nm in names.items():
+    n, ms, fl, by = ctypes.c_int64(), ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    L.lib().adaptra_prof_collect(kind, n, ms, fl, by)
+    if n.value:
+        res[nm] = {"launches": n.value, "avg_us": round(ms.value * 1e3 / n.value, 2),
+                   "tflops": round(fl.value / (ms.value / 1e3) / 1e12, 1)}
 print(json.dumps(res))
