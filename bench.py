@@ -119,6 +119,53 @@ def trace_c(event, S, t_ref_ns, host_c_ns):
     return c, down
 
 
+def isolated_kernels(model, lib):
+    """Per-kernel speed of the step's GEMM and attention kernels run alone
+    (serialised, warm) on the timed workload's shapes: one 1-layer stage,
+    F/B/W of two microbatches, prof kinds 0 (linear GEMM), 3 / 4 (attention
+    fwd / bwd, algorithmic causal flops)."""
+    import ctypes
+    import torch
+    from paper_2504_19232_b200 import _lib as L
+    from paper_2504_19232_b200.stage import Stage
+
+    st = Stage(L.BLOCK_GPT, model.dtype, 1, model.d, model.d_ff, model.n_heads, model.b, model.T, False, False,
+               2, 2, "cuda")
+    g = torch.Generator(device="cuda").manual_seed(0)
+    st.wts.copy_((torch.randn(st.wts.numel(), device="cuda", generator=g) * 0.02).to(st.tdt))
+    st.vecs.fill_(1.0)
+    rows = model.b * model.T
+    x = [torch.randn(rows, model.d, device="cuda", generator=g).to(st.tdt) for _ in range(2)]
+    dy = [torch.randn(rows, model.d, device="cuda", generator=g).to(st.tdt) * 0.01 for _ in range(2)]
+    y = [st.act() for _ in range(2)]
+    dx = [st.act() for _ in range(2)]
+    out = {}
+    for rep in range(4):
+        lib.adaptra_prof_enable(1 if rep == 3 else 0)
+        for j in range(2):
+            st.F(j, x[j], y[j])
+        for j in range(2):
+            st.B(j, dy[j], dx[j])
+            st.W(j)
+        torch.cuda.synchronize()
+    lib.adaptra_prof_enable(0)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak_burst = peaks.get("bf16_tflops", 1600.0)
+    for kind, name in ((0, "gemm_tc"), (3, "attn_fwd"), (4, "attn_bwd")):
+        n, ms, fl, by = ctypes.c_int64(), ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        lib.adaptra_prof_collect(kind, n, ms, fl, by)
+        if n.value:
+            tf = fl.value / (ms.value / 1e3) / 1e12
+            out[name] = {"launches": n.value, "avg_launch_us": round(ms.value * 1e3 / n.value, 2),
+                         "achieved_tflops": round(tf, 1), "frac_of_burst_peak": round(tf / peak_burst, 4)}
+    out["peak_burst"] = peak_burst
+    out["how"] = ("1-layer stage of the timed model alone, F/B/W of 2 microbatches on one stream, warm; "
+                  "CUDA events per launch; burst peak (kernel timed alone)")
+    st.close()
+    return out
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -302,6 +349,15 @@ def main():
         clocked = run_arm("adaptive", True, max(3, args.steps // 2), 1)
     clocks = clk.summary()
 
+    # -------- the same kernels alone: one 1-layer stage, F/B/W of 2 microbatches
+    # serialised on one stream, warm (after every timed region; rank 0 only).
+    # With several stages co-located on a GPU the timed-region launches overlap
+    # each other, which stretches their per-launch durations; this pass gives
+    # each kernel's own speed on the same shapes.
+    isolated = None
+    if rank == 0 and model.block == "gpt":
+        isolated = isolated_kernels(model, lib)
+
     if rank == 0:
         head = results[("adaptive", "trace")] if "adaptive" in arms else results[(arms[0], "trace")]
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
@@ -361,6 +417,7 @@ def main():
                                  "launch (see profiles/ for serialised ncu shares)",
                          "attention_gemm": attn_line,
                          "attention_fused": fused_line,
+                         "isolated": isolated,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"},
             "clocks": clocks,
             "e2e": e2e,

@@ -18,6 +18,8 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -82,11 +84,15 @@ struct AttnArgs {
   const float* D;        // [b*H*T] rowsum(dO o O)
   bf16* dqkv;            // [b*T, 3d] (k and v sections written here)
   float* dq_acc;         // [b*T, d] fp32 accumulator of dQ (zeroed by the caller)
+  long long* trace;      // diag 0x200: per-iteration clock64 stamps of CTA 0 ([it][16])
+  int diag;              // ADAPTRA_ATTN_DIAG bit mask, timing experiments only (0 = normal): 1 no dQ
+                         // reduce, 2 no gradient math, 4 no MMAs, 8 no Q/dO loads, 0x10/0x20/0x40/0x80/0x100 no S/dP/dV/dK/dQ MMA
 };
 }  // namespace
 
 // ============================================================== forward
 constexpr int kAttnThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 softmax
+constexpr int kFwdRing = 5;        // forward K/V tile ring (~2.5 key blocks of TMA lead)
 constexpr float kLog2e = 1.4426950408889634f;
 
 __device__ __forceinline__ float ex2(float x) {
@@ -106,24 +112,22 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __global__ void __launch_bounds__(kAttnThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const AttnArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* smem = smem_raw;  // no static shared memory: the window starts 1024-aligned (checked)
+  if (threadIdx.x == 0 && (smem_u32(smem) & 1023)) __trap();
   uint8_t* sQ = smem;                       // 32 KB
-  uint8_t* sK = sQ + TILE;                  // 2 stages x 32 KB
-  uint8_t* sV = sK + 2 * TILE;              // 2 stages x 32 KB
-  uint8_t* sP = sV + 2 * TILE;              // 32 KB
+  uint8_t* sRing = sQ + TILE;               // kFwdRing x 32 KB: K_0 V_0 K_1 V_1 ... (tile n in slot n % kFwdRing)
+  uint8_t* sP = sRing + kFwdRing * TILE;    // 32 KB
   float* sMax = (float*)(sP + TILE);        // [2 (block parity)][2 halves][128] half-row maxima
-  float* sL = sMax + 4 * AT;                // [2 halves][128] half-row sums
-  uint64_t* bar = (uint64_t*)(sL + 2 * AT);
+  uint64_t* bar = (uint64_t*)(sMax + 4 * AT);
   uint64_t* q_full = bar + 0;
-  uint64_t* k_full = bar + 1;    // [2]
-  uint64_t* v_full = bar + 3;    // [2]
-  uint64_t* kv_empty = bar + 5;  // [2]
-  uint64_t* s_full = bar + 7;    // [2]
-  uint64_t* s_empty = bar + 9;   // [2]
-  uint64_t* p_full = bar + 11;
-  uint64_t* p_empty = bar + 12;
-  uint64_t* o_full = bar + 13;
-  uint32_t* tmem_slot = (uint32_t*)(bar + 14);
+  uint64_t* t_full = bar + 1;               // [kFwdRing] tile landed
+  uint64_t* t_empty = t_full + kFwdRing;    // [kFwdRing] tile consumed by its MMA
+  uint64_t* s_full = t_empty + kFwdRing;    // [2]
+  uint64_t* s_empty = s_full + 2;           // [2]
+  uint64_t* p_full = s_empty + 2;
+  uint64_t* p_empty = p_full + 1;
+  uint64_t* o_full = p_empty + 1;
+  uint32_t* tmem_slot = (uint32_t*)(o_full + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int nqb = a.T / AT, Z = a.b * a.H;
@@ -136,10 +140,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm_qkv);
     mbar_init(q_full, 1);
+    for (int i = 0; i < kFwdRing; ++i) {
+      mbar_init(&t_full[i], 1);
+      mbar_init(&t_empty[i], 1);
+    }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&k_full[i], 1);
-      mbar_init(&v_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], 8);
     }
@@ -159,51 +164,54 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     if (lane == 0) {
       mbar_arrive_expect_tx(q_full, TILE);
       for (int c = 0; c < 2; ++c) tma_load_2d(sQ + c * CHUNK, &tm_qkv, q_full, qcol + 64 * c, row0 + qb * AT);
-      for (int j = 0; j <= qb; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&k_full[st], TILE);
+      for (int n = 0, slot = 0, ph = 0; n < 2 * (qb + 1); ++n) {  // K_j (n = 2j), V_j (n = 2j+1)
+        mbar_wait(&t_empty[slot], ph ^ 1);
+        mbar_arrive_expect_tx(&t_full[slot], TILE);
+        const int col = (n & 1) ? vcol : kcol;
         for (int c = 0; c < 2; ++c)
-          tma_load_2d(sK + st * TILE + c * CHUNK, &tm_qkv, &k_full[st], kcol + 64 * c, row0 + j * AT);
-        mbar_arrive_expect_tx(&v_full[st], TILE);
-        for (int c = 0; c < 2; ++c)
-          tma_load_2d(sV + st * TILE + c * CHUNK, &tm_qkv, &v_full[st], vcol + 64 * c, row0 + j * AT);
+          tma_load_2d(sRing + slot * TILE + c * CHUNK, &tm_qkv, &t_full[slot], col + 64 * c, row0 + (n >> 1) * AT);
+        if (++slot == kFwdRing) {
+          slot = 0;
+          ph ^= 1;
+        }
       }
     }
   } else if (warp == 1) {
     // S of block j+1 is issued before waiting for P of block j, so the softmax
-    // warps overlap the tensor pipe.  K/V stage and S buffer of block j are
-    // j & 1, their barrier phase (j >> 1) & 1.
+    // warps overlap the tensor pipe.  S buffer of block j is j & 1; tile n of
+    // the ring sits in slot n % kFwdRing with barrier phase (n / kFwdRing) & 1.
     mbar_wait(q_full, 0);
     tc_fence_after();
     const uint32_t aQ = smem_u32(sQ), aP = smem_u32(sP);
     auto issue_s = [&](int j) {
       const int st = j & 1;
-      const uint32_t ph = (j >> 1) & 1;
-      mbar_wait(&k_full[st], ph);
-      mbar_wait(&s_empty[st], ph ^ 1);
+      const int slot = (2 * j) % kFwdRing;
+      mbar_wait(&t_full[slot], ((2 * j) / kFwdRing) & 1);
+      mbar_wait(&s_empty[st], ((j >> 1) & 1) ^ 1);
       tc_fence_after();
       if (lane == 0) {
-        const uint32_t aK = smem_u32(sK + st * TILE);
+        const uint32_t aK = smem_u32(sRing + slot * TILE);
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
           tc_mma_f16(tmem + st * 128, desc_kmajor(aQ, ks), desc_kmajor(aK, ks), idesc(0, 0), ks > 0 ? 1u : 0u);
         tc_commit(&s_full[st]);
+        tc_commit(&t_empty[slot]);
       }
       __syncwarp();
     };
     issue_s(0);
     for (int j = 0; j <= qb; ++j) {
       if (j + 1 <= qb) issue_s(j + 1);
+      const int vslot = (2 * j + 1) % kFwdRing;
       mbar_wait(p_full, j & 1);
-      mbar_wait(&v_full[j & 1], (j >> 1) & 1);
+      mbar_wait(&t_full[vslot], ((2 * j + 1) / kFwdRing) & 1);
       tc_fence_after();
       if (lane == 0) {
-        const uint32_t aV = smem_u32(sV + (j & 1) * TILE);
+        const uint32_t aV = smem_u32(sRing + vslot * TILE);
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
           tc_mma_f16(tO, desc_kmajor(aP, ks), desc_mnmajor(aV, ks), idesc(0, 1), (j > 0 || ks > 0) ? 1u : 0u);
-        tc_commit(&kv_empty[j & 1]);
+        tc_commit(&t_empty[vslot]);
         tc_commit(p_empty);
       }
       __syncwarp();
@@ -292,7 +300,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
     }
-    // ---- epilogue: O / l -> bf16 (this half of the head dims), LSE (log2 units)
+    // ---- epilogue: O / l -> bf16 (this half of the head dims), LSE (log2 units).
+    // The row sums are exchanged through the sMax buffer of parity qb ^ 1,
+    // which both halves finished reading before the last block's barrier.
+    float* sL = sMax + ((qb & 1) ^ 1) * 2 * AT;
     sL[half * AT + r] = l;
     named_sync(pair_bar, 64);
     const float ltot = sL[r] + sL[AT + r];
@@ -322,16 +333,20 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 }
 
 // ============================================================== backward
-// One CTA per (z, 128-key block kb), over 64-query blocks i >= 2 kb.  TMEM
-// columns: dK [0,128), dV [128,256), S^T x2 [256,384), dP^T [384,448),
-// dQ^T [448,512) -- no aliasing, so S^T / dP^T of block i+1 run on the tensor
-// pipe while the gradient warps turn block i into P^T, dS^T and while
-// dV, dK, dQ^T of block i accumulate.  dQ^T = K^T dS^T (M = head dims) keeps
-// every MMA at M = 128; it is reduce-added into an fp32 accumulator laid out
-// [z][head dim][T] that dq_finalize transposes into dqkv.
+// One CTA per (z, 128-key block kb), over 64-query blocks i >= 2 kb.
+// TMEM columns: dK [0,128), dV [128,256), SP[2] [256,384) (S^T of block i,
+// then P^T in bf16 pairs written over the columns each thread has read:
+// k-step ks of dV += P^T dO_i reads columns [16 ks, 16 ks + 8)), DQ[2]
+// [384,512) (dP^T of block i, then dQ_i^T = K^T dS_i^T once dP^T is read).
+// With both double-buffered, the MMA warp issues S^T / dP^T of block i+1
+// before it waits for the gradient warps to finish block i; four drain warps
+// reduce-add dQ^T into an fp32 accumulator [z][head dim][T] (dq_finalize
+// transposes it into dqkv) off the gradient warps' path.  Every MMA is
+// M = 128.  Q_i / dO_i stream through 3 stages, dS^T is double-buffered.
 constexpr int QB = 64;                 // queries per backward step
 constexpr int QCHUNK = QB * 128;       // [64 rows x 64 cols] bf16 SWIZZLE_128B chunk (8 KB)
 constexpr int QTILE = 2 * QCHUNK;      // [64 x 128] bf16
+constexpr int NQS = 3;                 // Q_i / dO_i stages
 
 __device__ __forceinline__ uint64_t desc_kmajor_c(uint32_t base, int ks, int chunk) {
   return umma_desc_sw128(base + (ks >> 2) * chunk + (ks & 3) * 32, 16, 1024);
@@ -344,33 +359,38 @@ constexpr uint32_t idesc_n(int a_mn, int b_mn, int n) {
          ((uint32_t)(n >> 3) << 17) | ((uint32_t)(AT >> 4) << 24);
 }
 
-__global__ void __launch_bounds__(kAttnThreads, 1)
+// warp 0 TMA, warp 1 MMA, warps 2..17 gradient (4 per TMEM lane quadrant,
+// 16 query columns each), warps 18..21 dQ^T drain (one per quadrant)
+constexpr int kBwdThreads = 704;
+constexpr int kBwdCols = QB / 4;
+
+__global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
                     const __grid_constant__ CUtensorMap tm_do, const __grid_constant__ CUtensorMap tm_dq,
                     const AttnArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* sK = smem;               // 32 KB
-  uint8_t* sV = sK + TILE;          // 32 KB
-  uint8_t* sQ = sV + TILE;          // 2 stages x 16 KB  (query block i)
-  uint8_t* sdO = sQ + 2 * QTILE;    // 2 stages x 16 KB
-  uint8_t* sPT = sdO + 2 * QTILE;   // 2 buffers x 16 KB  P^T  [128 keys x 64 queries]
-  uint8_t* sdST = sPT + 2 * QTILE;  // 2 buffers x 16 KB  dS^T [128 keys x 64 queries]
-  uint8_t* sStg = sdST + 2 * QTILE; // 8 warps x 4 KB dQ^T staging
-  float* sLse = (float*)(sStg + 8 * 4096);  // [2 stages][64] (log2 units)
-  float* sD = sLse + 2 * QB;                // [2 stages][64]
-  uint64_t* bar = (uint64_t*)(sD + 2 * QB);
+  uint8_t* smem = smem_raw;  // no static shared memory: the window starts 1024-aligned (checked)
+  if (threadIdx.x == 0 && (smem_u32(smem) & 1023)) __trap();
+  uint8_t* sK = smem;                  // 32 KB
+  uint8_t* sV = sK + TILE;             // 32 KB
+  uint8_t* sQ = sV + TILE;             // NQS stages x 16 KB  (query block i)
+  uint8_t* sdO = sQ + NQS * QTILE;     // NQS stages x 16 KB
+  uint8_t* sdST = sdO + NQS * QTILE;   // 2 buffers x 16 KB  dS^T [128 keys x 64 queries]
+  uint8_t* sStg = sdST + 2 * QTILE;    // 4 drain warps x 4 KB dQ^T staging
+  float* sLse = (float*)(sStg + 4 * 4096);  // [NQS][64] (log2 units)
+  float* sD = sLse + NQS * QB;              // [NQS][64]
+  uint64_t* bar = (uint64_t*)(sD + NQS * QB);
   uint64_t* kv_full = bar + 0;
-  uint64_t* qd_full = bar + 1;   // [2] Q_i, dO_i, LSE_i, D_i landed
-  uint64_t* qd_empty = bar + 3;  // [2] dV, dK of block i done
-  uint64_t* s_full = bar + 5;    // [2] S^T in TMEM
-  uint64_t* dp_full = bar + 7;   // dP^T in TMEM
-  uint64_t* pd_full = bar + 8;   // [2] P^T, dS^T in smem; S^T and dP^T read (8 warps)
-  uint64_t* pd_empty = bar + 10; // [2] dV, dK, dQ^T done reading P^T / dS^T
-  uint64_t* dq_full = bar + 12;  // dQ^T in TMEM
-  uint64_t* dq_empty = bar + 13; // dQ^T read (8 warps)
-  uint64_t* kv_done = bar + 14;  // dK, dV final
-  uint32_t* tmem_slot = (uint32_t*)(bar + 15);
+  uint64_t* qd_full = bar + 1;    // [NQS] Q_i, dO_i, LSE_i, D_i landed
+  uint64_t* qd_empty = bar + 1 + NQS;   // [NQS] dV, dK of block i done
+  uint64_t* s_full = bar + 1 + 2 * NQS;  // [2] S^T in SP[b]
+  uint64_t* dp_full = s_full + 2;        // [2] dP^T in DQ[b]
+  uint64_t* pd_full = dp_full + 2;       // [2] P^T (SP[b]), dS^T (smem) written; S^T, dP^T read (16 warps)
+  uint64_t* pd_empty = pd_full + 2;      // [2] dK, dQ^T done reading dS^T (smem buffer b)
+  uint64_t* dq_full = pd_empty + 2;      // [2] dQ^T in DQ[b]
+  uint64_t* dq_empty = dq_full + 2;      // [2] dQ^T read (4 drain warps)
+  uint64_t* kv_done = dq_empty + 2;      // dK, dV final
+  uint32_t* tmem_slot = (uint32_t*)(kv_done + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int nb = a.T / AT, Z = a.b * a.H;
@@ -380,6 +400,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   const int row0 = s * a.T;
   const int qcol = h * AT, kcol = a.d + h * AT, vcol = 2 * a.d + h * AT;
   const int i0 = 2 * kb, n_it = 2 * (nb - kb);  // 64-query blocks i0 .. i0 + n_it - 1
+  const bool tr = (a.diag & 0x200) && blockIdx.x == 0 && lane == 0;
+#define TRACE(it, ev) \
+  if (tr && (it) < 64) a.trace[(it) * 16 + (ev)] = clock64();
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm_kv);
@@ -387,16 +410,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     tma_prefetch(&tm_do);
     tma_prefetch(&tm_dq);
     mbar_init(kv_full, 1);
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < NQS; ++k) {
       mbar_init(&qd_full[k], 1);
       mbar_init(&qd_empty[k], 1);
+    }
+    for (int k = 0; k < 2; ++k) {
       mbar_init(&s_full[k], 1);
-      mbar_init(&pd_full[k], 8);
+      mbar_init(&dp_full[k], 1);
+      mbar_init(&pd_full[k], 16);
+      mbar_init(&dq_full[k], 1);
+      mbar_init(&dq_empty[k], 4);
       mbar_init(&pd_empty[k], 1);
     }
-    mbar_init(dp_full, 1);
-    mbar_init(dq_full, 1);
-    mbar_init(dq_empty, 8);
     mbar_init(kv_done, 1);
     fence_barrier_init();
   }
@@ -405,7 +430,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tdK = tmem, tdV = tmem + 128, tS = tmem + 256, tdP = tmem + 384, tdQ = tmem + 448;
+  const uint32_t tdK = tmem, tdV = tmem + 128, tSP = tmem + 256, tDQ = tmem + 384;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -414,9 +439,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         tma_load_2d(sK + c * CHUNK, &tm_kv, kv_full, kcol + 64 * c, row0 + kb * AT);
         tma_load_2d(sV + c * CHUNK, &tm_kv, kv_full, vcol + 64 * c, row0 + kb * AT);
       }
-      for (int it = 0; it < n_it; ++it) {
-        const int st = it & 1, i = i0 + it;
-        mbar_wait(&qd_empty[st], ((it >> 1) & 1) ^ 1);
+      for (int it = 0, st = 0, ph = 0; it < n_it; ++it) {
+        const int i = i0 + it;
+        mbar_wait(&qd_empty[st], ph ^ 1);
+        TRACE(it, 0)
+        if (a.diag & 8) {
+          mbar_arrive(&qd_full[st]);
+          if (++st == NQS) {
+            st = 0;
+            ph ^= 1;
+          }
+          continue;
+        }
         mbar_arrive_expect_tx(&qd_full[st], 2 * QTILE + 2 * QB * 4);
         for (int c = 0; c < 2; ++c) {
           tma_load_2d(sQ + st * QTILE + c * QCHUNK, &tm_q, &qd_full[st], qcol + 64 * c, row0 + i * QB);
@@ -424,176 +458,244 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         }
         bulk_g2s(sLse + st * QB, a.lse + (size_t)z * a.T + i * QB, QB * 4, &qd_full[st]);
         bulk_g2s(sD + st * QB, a.D + (size_t)z * a.T + i * QB, QB * 4, &qd_full[st]);
+        if (++st == NQS) {
+          st = 0;
+          ph ^= 1;
+        }
       }
     }
   } else if (warp == 1) {
     mbar_wait(kv_full, 0);
     tc_fence_after();
     const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
-    auto issue_s = [&](int it) {  // S^T = K Q_i^T  -> buffer it & 1
-      const int st = it & 1;
-      mbar_wait(&qd_full[st], (it >> 1) & 1);
-      tc_fence_after();
+    // S^T = K Q_i^T -> SP[b], dP^T = V dO_i^T -> DQ[b] (stage st landed)
+    auto issue_sdp = [&](int b, int st, bool do_dp) {
       if (lane == 0) {
-        const uint32_t aQ = smem_u32(sQ + st * QTILE);
+        const uint32_t aQ = smem_u32(sQ + st * QTILE), adO = smem_u32(sdO + st * QTILE);
+        if (!(a.diag & 0x14)) {
 #pragma unroll
-        for (int ks = 0; ks < 8; ++ks)
-          tc_mma_f16(tS + st * QB, desc_kmajor(aK, ks), desc_kmajor_c(aQ, ks, QCHUNK), idesc_n(0, 0, QB),
-                     ks > 0 ? 1u : 0u);
-        tc_commit(&s_full[st]);
+          for (int ks = 0; ks < 8; ++ks)
+            tc_mma_f16(tSP + b * QB, desc_kmajor(aK, ks), desc_kmajor_c(aQ, ks, QCHUNK), idesc_n(0, 0, QB),
+                       ks > 0 ? 1u : 0u);
+        }
+        tc_commit(&s_full[b]);
+        if (do_dp) {
+          if (!(a.diag & 0x24)) {
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks)
+              tc_mma_f16(tDQ + b * QB, desc_kmajor(aV, ks), desc_kmajor_c(adO, ks, QCHUNK), idesc_n(0, 0, QB),
+                         ks > 0 ? 1u : 0u);
+          }
+          tc_commit(&dp_full[b]);
+        }
       }
       __syncwarp();
     };
-    auto issue_dp = [&](int it) {  // dP^T = V dO_i^T (Q_i / dO_i stage already waited on)
+    auto issue_dp = [&](int b, int st) {
       if (lane == 0) {
-        const uint32_t adO = smem_u32(sdO + (it & 1) * QTILE);
+        const uint32_t adO = smem_u32(sdO + st * QTILE);
+        if (!(a.diag & 0x24)) {
 #pragma unroll
-        for (int ks = 0; ks < 8; ++ks)
-          tc_mma_f16(tdP, desc_kmajor(aV, ks), desc_kmajor_c(adO, ks, QCHUNK), idesc_n(0, 0, QB),
-                     ks > 0 ? 1u : 0u);
-        tc_commit(dp_full);
+          for (int ks = 0; ks < 8; ++ks)
+            tc_mma_f16(tDQ + b * QB, desc_kmajor(aV, ks), desc_kmajor_c(adO, ks, QCHUNK), idesc_n(0, 0, QB),
+                       ks > 0 ? 1u : 0u);
+        }
+        tc_commit(&dp_full[b]);
       }
       __syncwarp();
     };
-    issue_s(0);
-    issue_dp(0);
-    for (int it = 0; it < n_it; ++it) {
-      const int st = it & 1;
-      const uint32_t ph = (it >> 1) & 1;
-      if (it + 1 < n_it) issue_s(it + 1);  // S^T buffer (it+1)&1 was released by pd_full(it-1)
-      mbar_wait(&pd_full[st], ph);         // P^T, dS^T of block it in smem; dP^T read
+    mbar_wait(&qd_full[0], 0);
+    tc_fence_after();
+    issue_sdp(0, 0, true);
+    for (int it = 0, st = 0, ph = 0; it < n_it; ++it) {
+      const int nst = st + 1 == NQS ? 0 : st + 1, nph = st + 1 == NQS ? ph ^ 1 : ph;
+      const int b = it & 1, nbuf = b ^ 1;
+      if (it + 1 < n_it) {
+        // SP[nbuf]: S^T(it-1) read and P^T(it-1) consumed by dV(it-1), issued earlier (in-order pipe)
+        mbar_wait(&qd_full[nst], nph);
+        TRACE(it, 1)
+        tc_fence_after();
+        issue_sdp(nbuf, nst, false);
+        // DQ[nbuf]: dP^T(it-1) read (pd_full(it-1) seen) and dQ^T(it-1) drained
+        if (it >= 1) mbar_wait(&dq_empty[nbuf], ((it - 1) >> 1) & 1);
+        TRACE(it, 2)
+        tc_fence_after();
+        issue_dp(nbuf, nst);
+      }
+      mbar_wait(&pd_full[b], (it >> 1) & 1);  // P^T, dS^T of block it written; S^T, dP^T read
+      TRACE(it, 3)
       tc_fence_after();
-      if (it + 1 < n_it) issue_dp(it + 1);
       if (lane == 0) {
         const uint32_t acc = it > 0 ? 1u : 0u;
         const uint32_t aQ = smem_u32(sQ + st * QTILE), adO = smem_u32(sdO + st * QTILE);
-        const uint32_t aPT = smem_u32(sPT + st * QTILE), adST = smem_u32(sdST + st * QTILE);
+        const uint32_t adST = smem_u32(sdST + b * QTILE);
 #pragma unroll
         for (int ks = 0; ks < QB / 16; ++ks) {
-          // dV += P^T dO_i ; dK += dS^T Q_i  (K = 64 queries; B operands read MN-major)
-          tc_mma_f16(tdV, desc_kmajor(aPT, ks), desc_mnmajor_c(adO, ks, QCHUNK), idesc_n(0, 1, AT),
-                     (acc || ks > 0) ? 1u : 0u);
-          tc_mma_f16(tdK, desc_kmajor(adST, ks), desc_mnmajor_c(aQ, ks, QCHUNK), idesc_n(0, 1, AT),
-                     (acc || ks > 0) ? 1u : 0u);
+          // dV += P^T dO_i (A from TMEM) ; dK += dS^T Q_i  (K = 64 queries; B read MN-major)
+          if (!(a.diag & 0x44))
+            tc_mma_f16_ts(tdV, tSP + b * QB + 16 * ks, desc_mnmajor_c(adO, ks, QCHUNK), idesc_n(0, 1, AT),
+                          (acc || ks > 0) ? 1u : 0u);
+          if (!(a.diag & 0x84))
+            tc_mma_f16(tdK, desc_kmajor(adST, ks), desc_mnmajor_c(aQ, ks, QCHUNK), idesc_n(0, 1, AT),
+                       (acc || ks > 0) ? 1u : 0u);
         }
         tc_commit(&qd_empty[st]);
-      }
-      __syncwarp();
-      mbar_wait(dq_empty, (it & 1) ^ 1);  // dQ^T of block it-1 drained
-      tc_fence_after();
-      if (lane == 0) {
-        const uint32_t adST = smem_u32(sdST + st * QTILE);
+        if (!(a.diag & 0x104)) {
 #pragma unroll
-        for (int ks = 0; ks < 8; ++ks)  // dQ_i^T = K^T dS_i^T  (both operands MN-major, K = 128 keys)
-          tc_mma_f16(tdQ, desc_mnmajor(aK, ks), desc_mnmajor_c(adST, ks, QCHUNK), idesc_n(1, 1, QB),
-                     ks > 0 ? 1u : 0u);
-        tc_commit(dq_full);
-        tc_commit(&pd_empty[st]);
+          for (int ks = 0; ks < 8; ++ks)  // dQ_i^T = K^T dS_i^T  (both operands MN-major, K = 128 keys)
+            tc_mma_f16(tDQ + b * QB, desc_mnmajor(aK, ks), desc_mnmajor_c(adST, ks, QCHUNK), idesc_n(1, 1, QB),
+                       ks > 0 ? 1u : 0u);
+        }
+        tc_commit(&dq_full[b]);
+        tc_commit(&pd_empty[b]);
       }
       __syncwarp();
+      st = nst;
+      ph = nph;
     }
     if (lane == 0) tc_commit(kv_done);
     __syncwarp();
-  } else {
-    const int quad = warp & 3, half = (warp - 2) >> 2;
-    const int r = quad * 32 + lane;  // key row (S^T, dP^T, dK, dV) / head-dim row (dQ^T)
+  } else if (warp < 18) {
+    // gradient warps: lane quadrant quad, query-column group cg (16 of the 64)
+    const int quad = warp & 3, cg = (warp - 2) >> 2;
+    const int r = quad * 32 + lane;  // key row (S^T, dP^T, P^T, dK, dV)
     const int kj = kb * AT + r;      // key position
     const uint32_t lanes = (uint32_t)(quad * 32) << 16;
     const float c2 = a.scale * kLog2e;
-    uint8_t* stg = sStg + (warp - 2) * 4096;
-    auto drain = [&](int it) {  // dQ^T of block it: 32 head-dim rows x 32 queries per warp
-      mbar_wait(dq_full, it & 1);
+    for (int it = 0, st = 0, ph = 0; it < n_it; ++it) {
+      const int i = i0 + it, b = it & 1;
+      const uint32_t bph = (it >> 1) & 1;
+      const uint32_t tS = tSP + b * QB + lanes + cg * kBwdCols;
+      mbar_wait(&s_full[b], bph);
+      if (warp == 2) TRACE(it, 4)
       tc_fence_after();
-      uint32_t rq[32];
-      tmem_ld32(tdQ + lanes + half * 32, rq);
-      tmem_ld_wait_regs(rq);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(dq_empty);
-      if (lane == 0) bulk_wait_read<0>();
-      __syncwarp();
-      const uint32_t frow = smem_u32(stg) + lane * 128;
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        sts128(frow + ((q ^ (lane & 7)) << 4), __float_as_uint(__uint_as_float(rq[4 * q]) * a.scale),
-               __float_as_uint(__uint_as_float(rq[4 * q + 1]) * a.scale),
-               __float_as_uint(__uint_as_float(rq[4 * q + 2]) * a.scale),
-               __float_as_uint(__uint_as_float(rq[4 * q + 3]) * a.scale));
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) {
-        tma_reduce_add_2d(&tm_dq, stg, (i0 + it) * QB + half * 32, z * AT + quad * 32);
-        bulk_commit();
+      uint32_t rs[16];
+      tmem_ld16(tS, rs);
+      tmem_ld_wait_regs16(rs);
+      if (a.diag & 2) {
+        mbar_wait(&dp_full[b], bph);
+        if (warp == 2) TRACE(it, 5)
+        mbar_wait(&pd_empty[b], bph ^ 1);
+        if (warp == 2) TRACE(it, 6)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pd_full[b]);
+        if (++st == NQS) {
+          st = 0;
+          ph ^= 1;
+        }
+        continue;
       }
-    };
-    for (int it = 0; it < n_it; ++it) {
-      const int st = it & 1, i = i0 + it;
-      const uint32_t ph = (it >> 1) & 1;
-      mbar_wait(&s_full[st], ph);
-      tc_fence_after();
-      uint32_t rs[32];
-      tmem_ld32(tS + st * QB + lanes + half * 32, rs);
-      tmem_ld_wait_regs(rs);
-      const float* lse = sLse + st * QB + half * 32;
-      const float* Dq = sD + st * QB + half * 32;
-      float p[32];
+      mbar_wait(&qd_full[st], ph);  // LSE_i, D_i landed (the MMA warp saw it before S^T)
+      const float* lse = sLse + st * QB + cg * kBwdCols;
+      const float* Dq = sD + st * QB + cg * kBwdCols;
+      float p[16];
 #pragma unroll
-      for (int t = 0; t < 32; ++t) p[t] = ex2(fmaf(__uint_as_float(rs[t]), c2, -lse[t]));
+      for (int t = 0; t < 16; ++t) p[t] = ex2(fmaf(__uint_as_float(rs[t]), c2, -lse[t]));
       if (it < 2) {  // diagonal: queries before this key are masked
-        const int lim = kj - (i * QB + half * 32);
+        const int lim = kj - (i * QB + cg * kBwdCols);
 #pragma unroll
-        for (int t = 0; t < 32; ++t)
+        for (int t = 0; t < 16; ++t)
           if (t < lim) p[t] = 0.f;
       }
-      mbar_wait(dp_full, it & 1);
+      if (warp == 2) TRACE(it, 10)
+      mbar_wait(&dp_full[b], bph);
+      if (warp == 2) TRACE(it, 5)
       tc_fence_after();
-      tmem_ld32(tdP + lanes + half * 32, rs);
-      tmem_ld_wait_regs(rs);
-      uint32_t pkp[16], pkd[16];  // P^T, dS^T row pieces as bf16x2
+      tmem_ld16(tDQ + b * QB + lanes + cg * kBwdCols, rs);
+      tmem_ld_wait_regs16(rs);
+      uint32_t pkp[8], pkd[8];  // P^T, dS^T row pieces as bf16x2
 #pragma unroll
-      for (int t = 0; t < 32; t += 2) {
+      for (int t = 0; t < 16; t += 2) {
         const float d0 = p[t] * (__uint_as_float(rs[t]) - Dq[t]);
         const float d1 = p[t + 1] * (__uint_as_float(rs[t + 1]) - Dq[t + 1]);
         pkp[t >> 1] = pack_bf16x2(p[t], p[t + 1]);
         pkd[t >> 1] = pack_bf16x2(d0, d1);
       }
-      mbar_wait(&pd_empty[st], ph ^ 1);  // MMAs of block it-2 done with this buffer
-      st_tile_row32_packed(smem_u32(sPT + st * QTILE), r, half * 32, pkp);
-      st_tile_row32_packed(smem_u32(sdST + st * QTILE), r, half * 32, pkd);
+      // P^T over this thread's own S^T columns (k-step cg of dV); dS^T to smem
+      tmem_st8(tS, pkp);
+      if (warp == 2) TRACE(it, 11)
+      mbar_wait(&pd_empty[b], bph ^ 1);  // dK, dQ^T of block it-2 done with dS^T buffer b
+      if (warp == 2) TRACE(it, 6)
+      {
+        const uint32_t row = smem_u32(sdST + b * QTILE) + r * 128;
+        const int p0 = cg * 2;  // first 16-byte piece (8 queries) of this column group
+        sts128(row + ((p0 ^ (r & 7)) << 4), pkd[0], pkd[1], pkd[2], pkd[3]);
+        sts128(row + (((p0 + 1) ^ (r & 7)) << 4), pkd[4], pkd[5], pkd[6], pkd[7]);
+      }
+      tmem_st_wait();
       tc_fence_before();
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&pd_full[st]);
-      if (it > 0) drain(it - 1);
+      if (warp == 2) TRACE(it, 7)
+      if (lane == 0) mbar_arrive(&pd_full[b]);
+      if (++st == NQS) {
+        st = 0;
+        ph ^= 1;
+      }
     }
-    drain(n_it - 1);
-    if (lane == 0) bulk_wait<0>();
-    // dK (scaled), dV -> bf16 into dqkv (k and v sections), thread = key row
+    // dK (scaled), dV -> bf16 into dqkv (k and v sections), thread = key row, 32 columns
     mbar_wait(kv_done, 0);
     tc_fence_after();
     for (int which = 0; which < 2; ++which) {
-      const uint32_t tb = (which == 0 ? tdK : tdV) + lanes + half * 64;
-      bf16* out = a.dqkv + (size_t)(row0 + kj) * 3 * a.d + (which == 0 ? a.d : 2 * a.d) + h * AT + half * 64;
+      const uint32_t tb = (which == 0 ? tdK : tdV) + lanes + cg * 32;
+      bf16* out = a.dqkv + (size_t)(row0 + kj) * 3 * a.d + (which == 0 ? a.d : 2 * a.d) + h * AT + cg * 32;
       const float sc = which == 0 ? a.scale : 1.f;
-      uint32_t r0[32], r1[32];
+      uint32_t r0[32];
       tmem_ld32(tb, r0);
-      tmem_ld32(tb + 32, r1);
+      tmem_ld_wait_regs(r0);
+      float v[32];
+#pragma unroll
+      for (int t = 0; t < 32; ++t) v[t] = __uint_as_float(r0[t]) * sc;
+#pragma unroll
+      for (int t = 0; t < 32; t += 8) st_bf16x8(out + t, v + t);
+    }
+  } else {
+    // drain warps: dQ^T rows of lane quadrant quad (head dims), 64 queries in 2 chunks of 32
+    const int quad = warp & 3;
+    const uint32_t lanes = (uint32_t)(quad * 32) << 16;
+    uint8_t* stg = sStg + (warp - 18) * 4096;
+    for (int it = 0; it < n_it; ++it) {
+      const int b = it & 1;
+      mbar_wait(&dq_full[b], (it >> 1) & 1);
+      if (warp == 18) TRACE(it, 8)
+      tc_fence_after();
+      uint32_t r0[32], r1[32];
+      tmem_ld32(tDQ + b * QB + lanes, r0);
+      tmem_ld32(tDQ + b * QB + lanes + 32, r1);
       tmem_ld_wait_regs(r0);
       tmem_ld_wait_regs(r1);
-      float v[64];
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&dq_empty[b]);
+      if (warp == 18) TRACE(it, 9)
+      auto stage = [&](const uint32_t(&rq)[32], int c) {
+        if (lane == 0) bulk_wait_read<0>();  // the previous reduce has read the staging buffer
+        __syncwarp();
+        const uint32_t frow = smem_u32(stg) + lane * 128;
 #pragma unroll
-      for (int t = 0; t < 32; ++t) {
-        v[t] = __uint_as_float(r0[t]) * sc;
-        v[32 + t] = __uint_as_float(r1[t]) * sc;
-      }
-#pragma unroll
-      for (int t = 0; t < 64; t += 8) st_bf16x8(out + t, v + t);
+        for (int q = 0; q < 8; ++q)
+          sts128(frow + ((q ^ (lane & 7)) << 4), __float_as_uint(__uint_as_float(rq[4 * q]) * a.scale),
+                 __float_as_uint(__uint_as_float(rq[4 * q + 1]) * a.scale),
+                 __float_as_uint(__uint_as_float(rq[4 * q + 2]) * a.scale),
+                 __float_as_uint(__uint_as_float(rq[4 * q + 3]) * a.scale));
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (!(a.diag & 3)) tma_reduce_add_2d(&tm_dq, stg, (i0 + it) * QB + c * 32, z * AT + quad * 32);
+          bulk_commit();
+        }
+      };
+      stage(r0, 0);
+      stage(r1, 1);
     }
+    if (lane == 0) bulk_wait<0>();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 1) tmem_dealloc(tmem, 512);
+#undef TRACE
 }
 
 // dQ^T (fp32 accumulator [z][head dim][T]) -> bf16 q section of dqkv
@@ -666,8 +768,10 @@ static int check_launch(const char* w) {
   return ADAPTRA_OK;
 }
 
-constexpr int kFwdSmem = 6 * TILE + 6 * AT * 4 + 1024 + 256;
-constexpr int kBwdSmem = 2 * TILE + 8 * QTILE + 8 * 4096 + 4 * QB * 4 + 1024 + 256;
+constexpr int kFwdSmem = (kFwdRing + 2) * TILE + 4 * AT * 4 + 256;
+static_assert(kFwdSmem <= 232448, "attn fwd shared memory");
+constexpr int kBwdSmem = 2 * TILE + (2 * NQS + 2) * QTILE + 4 * 4096 + 2 * NQS * QB * 4 + 256;
+static_assert(kBwdSmem <= 232448, "attn bwd shared memory");
 
 int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d, cudaStream_t st) {
   if (d != H * AT || T % AT) return set_error(ADAPTRA_EINVAL, "attn_fwd_tc: head dim 128 and T % 128 required");
@@ -719,7 +823,25 @@ int attn_bwd_tc(const bf16* qkv, const bf16* dO, const float* lse, const float* 
   a.dqkv = dqkv;
   a.dq_acc = dq_acc;
   void* pb = prof_on() ? prof_begin(st) : nullptr;
-  attn_bwd_kernel<<<b * H * (T / AT), kAttnThreads, kBwdSmem, st>>>(mkv, mq, mdo, mdq, a);
+  static const int diag = getenv("ADAPTRA_ATTN_DIAG") ? atoi(getenv("ADAPTRA_ATTN_DIAG")) : 0;
+  a.diag = diag;
+  static long long* trace = nullptr;
+  if ((diag & 0x200) && !trace) cudaMalloc(&trace, 64 * 16 * sizeof(long long));
+  a.trace = trace;
+  attn_bwd_kernel<<<b * H * (T / AT), kBwdThreads, kBwdSmem, st>>>(mkv, mq, mdo, mdq, a);
+  if (diag & 0x200) {
+    static int dumped = 0;
+    long long h[64 * 16];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
+    if (dumped++ == 2) {
+      for (int it = 0; it < 32; ++it) {
+        fprintf(stderr, "it %2d", it);
+        for (int e = 0; e < 12; ++e) fprintf(stderr, " %7lld", h[it * 16 + e] - h[0]);
+        fprintf(stderr, "\n");
+      }
+    }
+  }
   if (pb) {
     double fl = 8.0 * (double)T * T * AT * b * H * 0.5;  // dP, dV, dK, dQ (causal half)
     prof_end(pb, st, PROF_ATTN_BWD, fl, 0);
