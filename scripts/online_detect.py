@@ -26,7 +26,7 @@ def main():
     ap.add_argument("--S", type=int, default=4)
     ap.add_argument("--N", type=int, default=16)
     ap.add_argument("--layers", type=int, default=24)
-    ap.add_argument("--d", type=int, default=2048)
+    ap.add_argument("--width", type=int, default=2048)
     ap.add_argument("--hold", type=int, default=4)
     ap.add_argument("--events", type=int, default=10)
     args = ap.parse_args()
@@ -57,7 +57,7 @@ def main():
         return out
 
     S, N = args.S, args.N
-    m = ModelCfg(block="gpt", n_layers=args.layers, d=args.d, d_ff=4 * args.d, n_heads=args.d // 128, b=1,
+    m = ModelCfg(block="gpt", n_layers=args.layers, d=args.width, d_ff=4 * args.width, n_heads=args.width // 128, b=1,
                  T=2048, dtype=L.BF16)
     pipe = Pipeline(m, S, N, rank=rank, world=world, device=local, group=group, host_links=True)
     prof = Arm("zb", S, N, [1000] * S, [1000] * S, [1000] * S)
