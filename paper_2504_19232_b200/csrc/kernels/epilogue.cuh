@@ -103,7 +103,7 @@ __device__ __forceinline__ void epi_row(const EpiCtx& e, int m, int n0, float (&
   }
 }
 
-// Vectorised bf16 variant for a full run of 32 in-range, 16B-aligned columns.
+// Vectorised bf16 variant for a full run of NV (multiple of 8) in-range, 16B-aligned columns.
 __device__ __forceinline__ void st_bf16x8(bf16* p, const float* v) {
   uint4 u;
   u.x = pack_bf16x2(v[0], v[1]);
@@ -121,75 +121,76 @@ __device__ __forceinline__ void ld_bf16x8(const bf16* p, float* v) {
   f = unpack_bf16x2(u.w); v[6] = f.x; v[7] = f.y;
 }
 
-__device__ __forceinline__ void epi_row32_bf16_fast(const EpiCtx& e, int m, int n0, float (&v)[32]) {
+template <int NV>
+__device__ __forceinline__ void epi_rowN_bf16_fast(const EpiCtx& e, int m, int n0, float (&v)[NV]) {
   switch (e.epi) {
     case ADAPTRA_EPI_STORE: {
       bf16* c = (bf16*)e.C + (long)m * e.ldc + n0;
       if (e.bias) {
 #pragma unroll
-        for (int j = 0; j < 32; j += 4) {
+        for (int j = 0; j < NV; j += 4) {
           float4 b = *reinterpret_cast<const float4*>(e.bias + n0 + j);
           v[j] = e.alpha * v[j] + b.x; v[j + 1] = e.alpha * v[j + 1] + b.y;
           v[j + 2] = e.alpha * v[j + 2] + b.z; v[j + 3] = e.alpha * v[j + 3] + b.w;
         }
       } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] *= e.alpha;
+        for (int j = 0; j < NV; ++j) v[j] *= e.alpha;
       }
 #pragma unroll
-      for (int j = 0; j < 32; j += 8) st_bf16x8(c + j, v + j);
+      for (int j = 0; j < NV; j += 8) st_bf16x8(c + j, v + j);
     } break;
     case ADAPTRA_EPI_GELU: {
       bf16* c = (bf16*)e.C + (long)m * e.ldc + n0;
       bf16* a = (bf16*)e.aux + (long)m * e.ldaux + n0;
       if (e.bias) {
 #pragma unroll
-        for (int j = 0; j < 32; j += 4) {
+        for (int j = 0; j < NV; j += 4) {
           float4 b = *reinterpret_cast<const float4*>(e.bias + n0 + j);
           v[j] += b.x; v[j + 1] += b.y; v[j + 2] += b.z; v[j + 3] += b.w;
         }
       }
 #pragma unroll
-      for (int j = 0; j < 32; j += 8) st_bf16x8(a + j, v + j);
-      float gv[32];
+      for (int j = 0; j < NV; j += 8) st_bf16x8(a + j, v + j);
+      float gv[NV];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) gv[j] = gelu_f(__bfloat162float(__float2bfloat16_rn(v[j])));
+      for (int j = 0; j < NV; ++j) gv[j] = gelu_f(__bfloat162float(__float2bfloat16_rn(v[j])));
 #pragma unroll
-      for (int j = 0; j < 32; j += 8) st_bf16x8(c + j, gv + j);
+      for (int j = 0; j < NV; j += 8) st_bf16x8(c + j, gv + j);
     } break;
     case ADAPTRA_EPI_RESID: {
       bf16* c = (bf16*)e.C + (long)m * e.ldc + n0;
       const bf16* r = (const bf16*)e.R + (long)m * e.ldr + n0;
-      float rv[32];
+      float rv[NV];
 #pragma unroll
-      for (int j = 0; j < 32; j += 8) ld_bf16x8(r + j, rv + j);
+      for (int j = 0; j < NV; j += 8) ld_bf16x8(r + j, rv + j);
       if (e.bias) {
 #pragma unroll
-        for (int j = 0; j < 32; j += 4) {
+        for (int j = 0; j < NV; j += 4) {
           float4 b = *reinterpret_cast<const float4*>(e.bias + n0 + j);
           v[j] += b.x; v[j + 1] += b.y; v[j + 2] += b.z; v[j + 3] += b.w;
         }
       }
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] += rv[j];
+      for (int j = 0; j < NV; ++j) v[j] += rv[j];
 #pragma unroll
-      for (int j = 0; j < 32; j += 8) st_bf16x8(c + j, v + j);
+      for (int j = 0; j < NV; j += 8) st_bf16x8(c + j, v + j);
     } break;
     case ADAPTRA_EPI_DGELU: {
       bf16* c = (bf16*)e.C + (long)m * e.ldc + n0;
       const bf16* a = (const bf16*)e.aux + (long)m * e.ldaux + n0;
-      float av[32];
+      float av[NV];
 #pragma unroll
-      for (int j = 0; j < 32; j += 8) ld_bf16x8(a + j, av + j);
+      for (int j = 0; j < NV; j += 8) ld_bf16x8(a + j, av + j);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] *= gelu_grad_f(av[j]);
+      for (int j = 0; j < NV; ++j) v[j] *= gelu_grad_f(av[j]);
 #pragma unroll
-      for (int j = 0; j < 32; j += 8) st_bf16x8(c + j, v + j);
+      for (int j = 0; j < NV; j += 8) st_bf16x8(c + j, v + j);
     } break;
     case ADAPTRA_EPI_ACC_F32: {
       float* c = (float*)e.C + (long)m * e.ldc + n0;
 #pragma unroll
-      for (int j = 0; j < 32; j += 4) {
+      for (int j = 0; j < NV; j += 4) {
         float4 o = *reinterpret_cast<float4*>(c + j);
         o.x += e.alpha * v[j]; o.y += e.alpha * v[j + 1]; o.z += e.alpha * v[j + 2]; o.w += e.alpha * v[j + 3];
         *reinterpret_cast<float4*>(c + j) = o;
@@ -198,23 +199,27 @@ __device__ __forceinline__ void epi_row32_bf16_fast(const EpiCtx& e, int m, int 
     case ADAPTRA_EPI_STORE_F32: {
       float* c = (float*)e.C + (long)m * e.ldc + n0;
 #pragma unroll
-      for (int j = 0; j < 32; j += 4)
+      for (int j = 0; j < NV; j += 4)
         *reinterpret_cast<float4*>(c + j) = make_float4(e.alpha * v[j], e.alpha * v[j + 1], e.alpha * v[j + 2],
                                                         e.alpha * v[j + 3]);
     } break;
     case ADAPTRA_EPI_DSOFTMAX: {
       bf16* c = (bf16*)e.C + (long)m * e.ldc + n0;
       const bf16* p = (const bf16*)e.aux + (long)m * e.ldaux + n0;
-      float pv[32];
+      float pv[NV];
 #pragma unroll
-      for (int j = 0; j < 32; j += 8) ld_bf16x8(p + j, pv + j);
+      for (int j = 0; j < NV; j += 8) ld_bf16x8(p + j, pv + j);
       float D = e.rowv[m];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = pv[j] * (v[j] - D) * e.alpha;
+      for (int j = 0; j < NV; ++j) v[j] = pv[j] * (v[j] - D) * e.alpha;
 #pragma unroll
-      for (int j = 0; j < 32; j += 8) st_bf16x8(c + j, v + j);
+      for (int j = 0; j < NV; j += 8) st_bf16x8(c + j, v + j);
     } break;
   }
+}
+
+__device__ __forceinline__ void epi_row32_bf16_fast(const EpiCtx& e, int m, int n0, float (&v)[32]) {
+  epi_rowN_bf16_fast<32>(e, m, n0, v);
 }
 
 }  // namespace adaptra
