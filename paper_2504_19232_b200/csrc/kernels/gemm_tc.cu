@@ -60,6 +60,7 @@ struct TileInfo {
 // (aux) as (row, col) coordinates of their 2-D tensor maps.
 struct EpiTma {
   int on;
+  int in_tma;  // RESID / DGELU / DSOFTMAX: the input tile (R or aux) arrives by TMA through tmX
   int c_r1, c_r2, c_q1, c_q2;
   int x_r1, x_r2, x_q1, x_q2;
 };
@@ -106,7 +107,7 @@ template <int CG, int BN>
 __device__ __forceinline__ void epilogue_loop(const adaptra_gemm_desc_t& g, const TileInfo& ti, const EpiTma& et,
                                               const CUtensorMap* tmC, const CUtensorMap* tmX, int vec_ok,
                                               uint8_t* sEpi, uint32_t tmem_base, uint64_t* tfull, uint64_t* tempty,
-                                              int warp, int lane, int cid, int ncl, int rank) {
+                                              uint64_t* inbar, int warp, int lane, int cid, int ncl, int rank) {
   constexpr int TM = TcCfg<CG, BN>::TM;
   const int n_tiles = ti.m_blocks * ti.n_blocks * ti.Z;
   const int quad = warp & 3;  // TMEM lane quadrant this warp may access
@@ -116,6 +117,12 @@ __device__ __forceinline__ void epilogue_loop(const adaptra_gemm_desc_t& g, cons
   int sbuf = 0;
   int acc = 0;
   uint32_t acc_phase = 0;
+  uint32_t in_phase = 0;
+  // With in_tma the warp's 8 KB staging holds the input tile's NC chunks
+  // (2 KB each, bf16, SWIZZLE_64B = the bf16 output staging layout); each
+  // chunk's output is written over its input and TMA-stored from there.  No
+  // global load is then in flight at the fence.proxy.async of a chunk (it
+  // compiles to MEMBAR.ALL.CTA, which would wait for it).
   const bool f32o = (g.epi == ADAPTRA_EPI_ACC_F32 || g.epi == ADAPTRA_EPI_STORE_F32);
   const bool has_in = (g.epi == ADAPTRA_EPI_RESID || g.epi == ADAPTRA_EPI_DGELU || g.epi == ADAPTRA_EPI_DSOFTMAX);
   for (int t = cid; t < n_tiles; t += ncl) {
@@ -131,11 +138,18 @@ __device__ __forceinline__ void epilogue_loop(const adaptra_gemm_desc_t& g, cons
     const int ccol = z1 * et.c_q1 + z2 * et.c_q2 + nb * BN + co;
     const int xrow = z1 * et.x_r1 + z2 * et.x_r2 + rbase;
     const int xcol = z1 * et.x_q1 + z2 * et.x_q2 + nb * BN + co;
+    const bool in_tma = has_in && et.in_tma && et.on == 1;
     const bf16* in_row = nullptr;
-    if (has_in && row_ok)
+    if (has_in && row_ok && !in_tma)
       in_row = g.epi == ADAPTRA_EPI_RESID ? (const bf16*)e.R + (long)m * e.ldr : (const bf16*)e.aux + (long)m * e.ldaux;
     float nxt[32];
     if (in_row) ld_row32(in_row + nb * BN + co, nb * BN + co, e.N, vec_ok, nxt);
+    if (in_tma && lane == 0) {
+      bulk_wait_read<0>();  // the previous tile's stores have read the staging
+      mbar_arrive_expect_tx(inbar, NC * 2048);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) tma_load_2d(stg + c * 2048, tmX, inbar, xcol + c * 32, xrow);
+    }
     const float Dm = (g.epi == ADAPTRA_EPI_DSOFTMAX && row_ok) ? e.rowv[m] : 0.f;
     mbar_wait(&tfull[acc], acc_phase);
     tc_fence_after();
@@ -178,11 +192,20 @@ __device__ __forceinline__ void epilogue_loop(const adaptra_gemm_desc_t& g, cons
           for (int j = 0; j < 32; ++j) bv[j] = (n0 + j < e.N) ? e.bias[n0 + j] : 0.f;
         }
       }
-      // wait until this staging buffer's previous TMA store has read it
-      if (lane == 0) bulk_wait_read<1>();
-      __syncwarp();
-      uint8_t* sb = stg + sbuf * 4096;
-      sbuf ^= 1;
+      uint8_t* sb;
+      if (in_tma) {
+        if (c == 0) mbar_wait(inbar, in_phase);
+        sb = stg + c * 2048;
+        const uint8_t* irow = sb + lane * 64;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ld_bf16x8((const bf16*)(irow + ((j ^ ((lane >> 1) & 3)) << 4)), in + 8 * j);
+      } else {
+        // wait until this staging buffer's previous TMA store has read it
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+        sb = stg + sbuf * 4096;
+        sbuf ^= 1;
+      }
       switch (g.epi) {
         case ADAPTRA_EPI_STORE:
 #pragma unroll
@@ -239,6 +262,7 @@ __device__ __forceinline__ void epilogue_loop(const adaptra_gemm_desc_t& g, cons
         bulk_commit();
       }
     }
+    if (in_tma) in_phase ^= 1;
     tc_fence_before();
     __syncwarp();
     if (lane == 0) {
@@ -272,7 +296,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + Cfg::kStages;
   uint64_t* tfull = empty + Cfg::kStages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  uint64_t* inbar = tempty + 2;  // [kEpiWarps] epilogue input tiles (in_tma)
+  uint32_t* tmem_slot = (uint32_t*)(inbar + kEpiWarps);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -292,6 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], kEpiWarps * CG);
     }
+    for (int w = 0; w < kEpiWarps; ++w) mbar_init(&inbar[w], 1);
     fence_barrier_init();
   }
   if (warp == kWarpMma) {
@@ -433,7 +459,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
-    epilogue_loop<CG, BN>(g, ti, et, &tmC, &tmX, vec_ok, sEpi, tmem_base, tfull, tempty, warp, lane, cid, ncl, rank);
+    epilogue_loop<CG, BN>(g, ti, et, &tmC, &tmX, vec_ok, sEpi, tmem_base, tfull, tempty, &inbar[warp], warp, lane, cid,
+                          ncl, rank);
   }
   tc_fence_before();
   if (CG == 2)
@@ -572,6 +599,18 @@ static int launch_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
            decomp(g.aux_1, g.aux_2, g.ldaux, et.x_r1, et.x_r2, et.x_q1, et.x_q2, xr, xc) &&
            make_map(&mx, g.aux, xr, g.Z == 1 ? g.N : xc, g.ldaux, 32, 32, false, 64) == ADAPTRA_OK;
     }
+    if (ok && (g.epi == ADAPTRA_EPI_DGELU || g.epi == ADAPTRA_EPI_DSOFTMAX) && g.aux && (uintptr_t)g.aux % 16 == 0 &&
+        (g.ldaux * 2) % 16 == 0) {
+      int64_t xr = 0, xc = 0;
+      et.in_tma = decomp(g.aux_1, g.aux_2, g.ldaux, et.x_r1, et.x_r2, et.x_q1, et.x_q2, xr, xc) &&
+                  make_map(&mx, g.aux, xr, g.Z == 1 ? g.N : xc, g.ldaux, 32, 32, false, 64) == ADAPTRA_OK;
+    } else if (ok && g.epi == ADAPTRA_EPI_RESID && g.R && (uintptr_t)g.R % 16 == 0 && (g.ldr * 2) % 16 == 0 &&
+               g.Z == 1) {
+      et.x_r1 = et.x_r2 = et.x_q1 = et.x_q2 = 0;
+      et.in_tma = make_map(&mx, g.R, g.M, g.N, g.ldr, 32, 32, false, 64) == ADAPTRA_OK;
+    }
+    static const bool no_in_tma = getenv("ADAPTRA_EPI_IN_LDG") != nullptr;  // timing comparison only
+    if (no_in_tma) et.in_tma = 0;
     et.on = ok ? 1 : 0;
     // timing experiments only: 1 = skip all epilogue work, 2 = skip the TMA store
     static const int diag = getenv("ADAPTRA_DIAG_NOEPI") ? atoi(getenv("ADAPTRA_DIAG_NOEPI")) : 0;
