@@ -334,8 +334,9 @@ def main():
         if name == "adaptive":
             n, ms, fl, by = (__import__("ctypes").c_int64(), __import__("ctypes").c_double(),
                              __import__("ctypes").c_double(), __import__("ctypes").c_double())
-            lib.adaptra_prof_collect(0, n, ms, fl, by)
-            gem = gather((n.value, ms.value, fl.value, by.value))
+            um = __import__("ctypes").c_double()
+            lib.adaptra_prof_collect_ex(0, n, ms, um, fl, by)
+            gem = gather((n.value, ms.value, fl.value, by.value, um.value))
             lib.adaptra_prof_collect(2, n, ms, fl, by)
             gem_attn = gather((n.value, ms.value, fl.value, by.value))
             lib.adaptra_prof_collect(3, n, ms, fl, by)
@@ -373,6 +374,9 @@ def main():
         fl_l = sum(x[2] for x in gem)
         avg_ms = ms_l / max(1, n_l)
         achieved = (fl_l / max(1, n_l)) / (avg_ms / 1e3) / 1e12 if n_l else None
+        # the GEMM class over the time any GEMM was running (per rank: union of
+        # its launches' intervals across stage streams), summed over ranks
+        union_tf = sum(x[2] / (x[4] / 1e3) / 1e12 for x in gem if x[4] > 0) if n_l else None
         na = sum(x[0] for x in gem_attn)
         attn_line = None
         if na:
@@ -422,6 +426,11 @@ def main():
                                  "launch (see profiles/ for serialised ncu shares)",
                          "attention_gemm": attn_line,
                          "attention_fused": fused_line,
+                         "class_union": {"achieved": round(union_tf, 1) if union_tf else None,
+                                         "frac": round(union_tf / (world * peak), 4) if union_tf else None,
+                                         "how": "algorithmic GEMM FLOPs of the timed steps / union of the GEMM "
+                                                "launch intervals across a GPU's stage streams (time any GEMM ran), "
+                                                "summed over GPUs; peak x n_gpus"},
                          "isolated": isolated,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"},
             "clocks": clocks,

@@ -164,7 +164,8 @@ int adaptra_gemm(const adaptra_gemm_desc_t* g, void* stream);
 
 /* Live kernel timing (bench roofline): when enabled, every tcgen05 GEMM launch
  * is bracketed by CUDA events on its own stream; kind 0 = the stage's linear
- * layers (unbatched), kind 2 = the batched attention products.  collect() waits for
+ * layers (unbatched), kind 2 = the batched attention products (materialised
+ * fp32 path), kind 3 / 4 = the fused attention forward / backward.  collect() waits for
  * the recorded launches of `kind`, returns their count, summed duration (ms),
  * algorithmic FLOPs (2MNK per batch, causal products counted at 1/2, R28) and
  * operand/result bytes, and forgets them. */
@@ -172,6 +173,12 @@ int adaptra_prof_enable(int32_t on);
 /* Number of this library's kernel launches in this process so far. */
 int64_t adaptra_launch_count(void);
 int adaptra_prof_collect(int32_t kind, int64_t* n_launches, double* sum_ms, double* flops, double* bytes);
+/* Same, plus the union of the collected launches' [start, end) intervals
+ * across all streams of the device (ms): the wall time during which at least
+ * one launch of this kind was running.  With several stage streams on one GPU
+ * launches overlap, so sum_ms / n overstates a launch's own duration. */
+int adaptra_prof_collect_ex(int32_t kind, int64_t* n_launches, double* sum_ms, double* union_ms, double* flops,
+                            double* bytes);
 
 /* ================================================================ stage compute
  * One pipeline stage = n_layers identical blocks (R24/R19: uniform stages).

@@ -95,6 +95,8 @@ _SIGS = {
     "adaptra_prof_enable": (_i32, [_i32]),
     "adaptra_launch_count": (_i64, []),
     "adaptra_prof_collect": (_i32, [_i32, _P(_i64), _P(C.c_double), _P(C.c_double), _P(C.c_double)]),
+    "adaptra_prof_collect_ex": (_i32, [_i32, _P(_i64), _P(C.c_double), _P(C.c_double), _P(C.c_double),
+                                       _P(C.c_double)]),
     "adaptra_stage_slot_bytes": (_i64, [_P(StageDesc)]),
     "adaptra_stage_slot_fb_bytes": (_i64, [_P(StageDesc)]),
     "adaptra_stage_work_bytes": (_i64, [_P(StageDesc)]),
