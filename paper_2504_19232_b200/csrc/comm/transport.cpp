@@ -17,6 +17,7 @@
 #include <chrono>
 #include <condition_variable>
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <functional>
@@ -253,6 +254,7 @@ struct adaptra_inbox {
   bool has_ring = false;
   std::atomic<int> host_on{0};
   cudaStream_t dstream = nullptr;     // delegate H2D stream
+  bool own_dstream = false;           // dstream created for this inbox (multi-queue)
   std::vector<uint32_t> delivered;    // host path: epoch delivered per mb
 };
 
@@ -364,10 +366,24 @@ extern "C" int adaptra_inbox_create(int32_t dev, int32_t n_mb, int64_t bytes, co
       return rc;
     }
   }
-  ib->dstream = signal_stream(dev);
+  // Multi-queue delegated path: every inbox (one
+  // link direction) gets its own H2D stream, so host-path deliveries of
+  // different links proceed on separate copy queues instead of one.
+  // ADAPTRA_DELEGATE_SHARED_STREAM=1 restores the single shared queue.
+  static const bool shared_q = getenv("ADAPTRA_DELEGATE_SHARED_STREAM") != nullptr;
+  if (shared_q) {
+    ib->dstream = signal_stream(dev);
+  } else if (cudaStreamCreateWithFlags(&ib->dstream, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaFree(ib->mbox);
+    flags_close(ib->fl);
+    delete ib;
+    return set_error(ADAPTRA_ECUDA, "inbox_create: stream");
+  }
+  ib->own_dstream = !shared_q;
   if (host_name && host_name[0]) {
     int rc = ring_open(ib->ring, host_name, n_mb, bytes, true);
     if (rc) {
+      if (ib->own_dstream) cudaStreamDestroy(ib->dstream);
       cudaFree(ib->mbox);
       flags_close(ib->fl);
       delete ib;
@@ -389,6 +405,7 @@ extern "C" int adaptra_inbox_destroy(adaptra_inbox_t ib) {
   }
   cudaSetDevice(ib->dev);
   cudaStreamSynchronize(ib->dstream);
+  if (ib->own_dstream) cudaStreamDestroy(ib->dstream);
   cudaFree(ib->mbox);
   flags_close(ib->fl);
   delete ib;
