@@ -529,7 +529,8 @@ def reference_arm(args, rank, world):
             "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"C1 (oracle sample) S={S} N={N} seq={T} d={d}"},
+            "config": {"workload": f"{'C3, 8 stages, 1.3B-shaped blocks' if S == 8 else 'C1'} (oracle sample) "
+                                     f"S={S} N={N} seq={T} d={d}"},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
