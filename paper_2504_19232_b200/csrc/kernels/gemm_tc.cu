@@ -649,6 +649,279 @@ static int launch_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
   return ADAPTRA_OK;
 }
 
+// ------------------------------------------------------------------ grouped dW
+// All weight-gradient products of a W op (dW += X^T dY for every
+// linear layer of the stage) are independent, so they run as one persistent
+// launch over the union of their tiles instead of one launch each: the waves
+// are filled across problems and only the launch's last tiles expose an
+// epilogue.  Specialised to what W needs: CTA pairs, 256 x 256 tiles, both
+// operands MN-major, fp32 TMA reduce-add into the gradient.  Each tile runs
+// the same MMA sequence and reduce-add as in gemm_tc_kernel, so the result is
+// the same bit for bit.
+constexpr int kMaxGroup = 24;
+struct GroupArgs {
+  CUtensorMap tmA[kMaxGroup], tmB[kMaxGroup], tmC[kMaxGroup];
+  int n, total_tiles;
+  int tile_start[kMaxGroup + 1];
+  int m_blocks[kMaxGroup], k_blocks[kMaxGroup], N[kMaxGroup];
+  float alpha[kMaxGroup];
+};
+
+__device__ __forceinline__ void group_tile(const GroupArgs& ga, int t, int TM_, int& q, int& mb, int& nb) {
+  q = 0;
+  while (q + 1 < ga.n && t >= ga.tile_start[q + 1]) ++q;
+  const int lt = t - ga.tile_start[q];
+  mb = lt % ga.m_blocks[q];
+  nb = lt / ga.m_blocks[q];
+  (void)TM_;
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1) gemm_tc_grouped_kernel(const __grid_constant__ GroupArgs ga) {
+  constexpr int CG = 2;
+  using Cfg = TcCfg<CG, BN>;
+  constexpr int TM = Cfg::TM;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + Cfg::kStages * Cfg::kABytes;
+  uint8_t* sEpi = smem + Cfg::kStages * Cfg::kStageBytes;
+  uint64_t* full = (uint64_t*)(smem + Cfg::kStages * Cfg::kStageBytes + Cfg::kEpiBytes);
+  uint64_t* empty = full + Cfg::kStages;
+  uint64_t* tfull = empty + Cfg::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2 + kEpiWarps);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int rank = (int)cluster_ctarank();
+  const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
+
+  if (warp == kWarpProducer && lane == 0) {
+    for (int s = 0; s < Cfg::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], kEpiWarps * CG);
+    }
+    fence_barrier_init();
+  }
+  if (warp == kWarpMma) tmem_alloc2(tmem_slot, Cfg::kTmemCols);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp >= kEpiWarps) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory");
+  if (warp == kWarpProducer) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cid; t < ga.total_tiles; t += ncl) {
+        int q, mb, nb;
+        group_tile(ga, t, TM, q, mb, nb);
+        const int m0 = mb * TM + rank * BM, n0 = nb * BN + rank * Cfg::kBRows;
+        for (int kb = 0; kb < ga.k_blocks[q]; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes * CG);
+          uint8_t* a_dst = sA + stage * Cfg::kABytes;
+          uint8_t* b_dst = sB + stage * Cfg::kBBytes;
+          const int k0 = kb * BK;
+#pragma unroll
+          for (int j = 0; j < BM / 64; ++j)
+            tma_load_2d_2sm(a_dst + j * (BK * 128), &ga.tmA[q], &full[stage], m0 + 64 * j, k0);
+#pragma unroll
+          for (int j = 0; j < Cfg::kBRows / 64; ++j)
+            tma_load_2d_2sm(b_dst + j * (BK * 128), &ga.tmB[q], &full[stage], n0 + 64 * j, k0);
+          if (++stage == Cfg::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == kWarpMma) {
+    if (rank == 0) {
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) |
+                             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = cid; t < ga.total_tiles; t += ncl) {
+        int q, mb, nb;
+        group_tile(ga, t, TM, q, mb, nb);
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        const int kb1 = ga.k_blocks[q];
+        for (int kb = 0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a_addr = smem_u32(sA + stage * Cfg::kABytes);
+            const uint32_t b_addr = smem_u32(sB + stage * Cfg::kBBytes);
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              tc_mma_f16_2sm(d_tmem, umma_desc_sw128(a_addr + k * 2048, BK * 128, 1024),
+                             umma_desc_sw128(b_addr + k * 2048, BK * 128, 1024), idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            tc_commit_2sm_mc(&empty[stage]);
+          }
+          __syncwarp();
+          if (++stage == Cfg::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (lane == 0) tc_commit_2sm_mc(&tfull[acc]);
+        __syncwarp();
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
+    // epilogue: fp32 TMA reduce-add of the accumulator (as gemm_tc_kernel's ACC_F32 path)
+    const int quad = warp & 3;
+    const int co = (warp >> 2) * (BN / 2);
+    constexpr int NC = BN / 64;
+    uint8_t* stg = sEpi + warp * 8192;
+    int sbuf = 0, acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = cid; t < ga.total_tiles; t += ncl) {
+      int q, mb, nb;
+      group_tile(ga, t, TM, q, mb, nb);
+      const int crow = mb * TM + rank * BM + quad * 32;
+      const int ccol = nb * BN + co;
+      const float alpha = ga.alpha[q];
+      const int Nq = ga.N[q];
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + co;
+      uint32_t r[32];
+      tmem_ld32(tbase, r);
+#pragma unroll 1
+      for (int c = 0; c < NC; ++c) {
+        tmem_ld_wait_regs(r);
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * alpha;
+        if (c + 1 < NC) tmem_ld32(tbase + (c + 1) * 32, r);
+        if (ccol + c * 32 >= Nq) continue;
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+        uint8_t* sb = stg + sbuf * 4096;
+        sbuf ^= 1;
+        uint8_t* frow = sb + lane * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<float4*>(frow + ((j ^ (lane & 7)) << 4)) =
+              make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_reduce_add_2d(&ga.tmC[q], sb, ccol + c * 32, crow);
+          bulk_commit();
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(&tempty[acc], 0);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+    if (lane == 0) bulk_wait<0>();
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == kWarpMma) tmem_dealloc2(tmem_base, Cfg::kTmemCols);
+}
+
+int gemm_tc(const adaptra_gemm_desc_t& g, cudaStream_t st);
+
+// Grouped dW products (see above).  Falls back to one gemm_tc launch per
+// product when a product does not fit the specialisation.
+int gemm_tc_grouped(const adaptra_gemm_desc_t* gs, int n, cudaStream_t st) {
+  constexpr int BN = 256;
+  using Cfg = TcCfg<2, BN>;
+  static const bool off = getenv("ADAPTRA_GEMM_GROUPED") && atoi(getenv("ADAPTRA_GEMM_GROUPED")) == 0;
+  bool ok = !off && n > 0 && n <= kMaxGroup;
+  for (int i = 0; ok && i < n; ++i) {
+    const auto& g = gs[i];
+    ok = g.dtype == ADAPTRA_BF16 && g.Z == 1 && g.epi == ADAPTRA_EPI_ACC_F32 && g.a_mn == 1 && g.b_mn == 1 &&
+         !g.causal && g.N >= 2048 && g.M >= 256 && (g.ldc % 4) == 0 && ((uintptr_t)g.C % 16) == 0 &&
+         (g.lda * 2) % 16 == 0 && (g.ldb * 2) % 16 == 0;
+  }
+  if (!ok) {
+    for (int i = 0; i < n; ++i) {
+      int rc = gemm_tc(gs[i], st);
+      if (rc) return rc;
+    }
+    return ADAPTRA_OK;
+  }
+  static GroupArgs ga;  // host staging of the kernel parameter (9 KB); launches are serialised per process
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  memset(&ga, 0, sizeof(ga));
+  ga.n = n;
+  int tiles = 0;
+  double fl = 0;
+  for (int i = 0; i < n; ++i) {
+    const auto& g = gs[i];
+    int rc = make_map(&ga.tmA[i], g.A, g.a_rows, g.a_cols, g.lda, 64, BK);
+    if (!rc) rc = make_map(&ga.tmB[i], g.B, g.b_rows, g.b_cols, g.ldb, 64, BK);
+    if (!rc) rc = make_map(&ga.tmC[i], g.C, g.M, g.N, g.ldc, 32, 32, true, 128);
+    if (rc) return rc;
+    ga.m_blocks[i] = (g.M + Cfg::TM - 1) / Cfg::TM;
+    ga.k_blocks[i] = (g.K + BK - 1) / BK;
+    ga.N[i] = g.N;
+    ga.alpha[i] = g.alpha;
+    ga.tile_start[i] = tiles;
+    tiles += ga.m_blocks[i] * ((g.N + BN - 1) / BN);
+    fl += 2.0 * g.M * (double)g.N * g.K;
+  }
+  ga.tile_start[n] = tiles;
+  ga.total_tiles = tiles;
+  auto kern = gemm_tc_grouped_kernel<BN>;
+  static unsigned attr_mask = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(attr_mask & (1u << dev))) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+    attr_mask |= 1u << dev;
+  }
+  const int slots = num_sms() / 2;
+  const int grid = (tiles < slots ? tiles : slots) * 2;
+  void* pb = prof_on() ? prof_begin(st) : nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Cfg::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, ga);
+  count_launch();
+  if (pb) prof_end(pb, st, PROF_GEMM_TC, fl, 0);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(ADAPTRA_ECUDA, std::string("gemm_tc_grouped launch: ") + cudaGetErrorString(e));
+  return ADAPTRA_OK;
+}
+
 int gemm_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
   // BN = 256 for large unbatched N, else 128 (batched attention tiles must not
   // cross a batch boundary: require tile-aligned extents when Z > 1).

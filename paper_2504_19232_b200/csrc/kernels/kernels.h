@@ -9,6 +9,9 @@ namespace adaptra {
 typedef __nv_bfloat16 bf16;
 
 int gemm_tc(const adaptra_gemm_desc_t& g, cudaStream_t st);
+// Independent products in one persistent launch (W op's dW += X^T dY);
+// falls back to one gemm_tc per product outside its specialisation.
+int gemm_tc_grouped(const adaptra_gemm_desc_t* gs, int n, cudaStream_t st);
 int gemm_simt(const adaptra_gemm_desc_t& g, cudaStream_t st);
 
 template <typename T>

@@ -5,6 +5,7 @@
 // accumulating into fp32 buffers (deferred).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <string>
@@ -399,6 +400,10 @@ struct StageOps {
   int Wop(int slot) {
     const auto& D = d();
     const long R = s->R, Dm = D.d, Ff = D.d_ff;
+    // every dW += X^T dY product of the op is independent: collect them and run
+    // them as grouped persistent launches (bias / LN parameter sums inline)
+    std::vector<adaptra_gemm_desc_t> dw;
+    dw.reserve(4 * D.n_layers);
     for (int l = D.n_layers - 1; l >= 0; --l) {
       ParamOff p = param_off(D, l);
       const T* dy = layer_dy(slot, l);
@@ -406,12 +411,12 @@ struct StageOps {
       T* g = buf(slot, l, s->L.g);
       T* da = buf(slot, l, s->L.da);
       // dW2 += dy^T g ; db2 += sum dy
-      TRY(GB(dt()).shape(Dm, Ff, R).A(dy, Dm, R, Dm, 1).B(g, Ff, R, Ff, 1).C(GW(p.W2), Ff)
-              .epi(ADAPTRA_EPI_ACC_F32).run(st));
+      dw.push_back(GB(dt()).shape(Dm, Ff, R).A(dy, Dm, R, Dm, 1).B(g, Ff, R, Ff, 1).C(GW(p.W2), Ff)
+              .epi(ADAPTRA_EPI_ACC_F32).g);
       TRY(col_sum<T>(dy, GV(p.b2), R, Dm, st));
       if (D.block == ADAPTRA_BLOCK_MLP) {
-        TRY(GB(dt()).shape(Ff, Dm, R).A(da, Ff, R, Ff, 1).B(x, Dm, R, Dm, 1).C(GW(p.W1), Dm)
-                .epi(ADAPTRA_EPI_ACC_F32).run(st));
+        dw.push_back(GB(dt()).shape(Ff, Dm, R).A(da, Ff, R, Ff, 1).B(x, Dm, R, Dm, 1).C(GW(p.W1), Dm)
+                .epi(ADAPTRA_EPI_ACC_F32).g);
         TRY(col_sum<T>(da, GV(p.b1), R, Ff, st));
         continue;
       }
@@ -423,19 +428,27 @@ struct StageOps {
       T* dy1 = buf(slot, l, s->L.dy1);
       T* dh2 = buf(slot, l, s->L.dh2);
       T* dh1 = buf(slot, l, s->L.dh1);
-      TRY(GB(dt()).shape(Ff, Dm, R).A(da, Ff, R, Ff, 1).B(h2, Dm, R, Dm, 1).C(GW(p.W1), Dm)
-              .epi(ADAPTRA_EPI_ACC_F32).run(st));
+      dw.push_back(GB(dt()).shape(Ff, Dm, R).A(da, Ff, R, Ff, 1).B(h2, Dm, R, Dm, 1).C(GW(p.W1), Dm)
+              .epi(ADAPTRA_EPI_ACC_F32).g);
       TRY(col_sum<T>(da, GV(p.b1), R, Ff, st));
       TRY(ln_param_grad<T>(dh2, y1, fbuf(slot, l, s->L.mean2), fbuf(slot, l, s->L.rstd2), GV(p.ln2_g), GV(p.ln2_b), R,
                            Dm, st));
-      TRY(GB(dt()).shape(Dm, Dm, R).A(dy1, Dm, R, Dm, 1).B(o, Dm, R, Dm, 1).C(GW(p.Wo), Dm)
-              .epi(ADAPTRA_EPI_ACC_F32).run(st));
+      dw.push_back(GB(dt()).shape(Dm, Dm, R).A(dy1, Dm, R, Dm, 1).B(o, Dm, R, Dm, 1).C(GW(p.Wo), Dm)
+              .epi(ADAPTRA_EPI_ACC_F32).g);
       TRY(col_sum<T>(dy1, GV(p.bo), R, Dm, st));
-      TRY(GB(dt()).shape(3 * Dm, Dm, R).A(dqkv, 3 * Dm, R, 3 * Dm, 1).B(h1, Dm, R, Dm, 1).C(GW(p.Wqkv), Dm)
-              .epi(ADAPTRA_EPI_ACC_F32).run(st));
+      dw.push_back(GB(dt()).shape(3 * Dm, Dm, R).A(dqkv, 3 * Dm, R, 3 * Dm, 1).B(h1, Dm, R, Dm, 1).C(GW(p.Wqkv), Dm)
+              .epi(ADAPTRA_EPI_ACC_F32).g);
       TRY(col_sum<T>(dqkv, GV(p.bqkv), R, 3 * Dm, st));
       TRY(ln_param_grad<T>(dh1, x, fbuf(slot, l, s->L.mean1), fbuf(slot, l, s->L.rstd1), GV(p.ln1_g), GV(p.ln1_b), R,
                            Dm, st));
+    }
+    dw.erase(std::remove_if(dw.begin(), dw.end(), [](const adaptra_gemm_desc_t& g) { return g.M == 0 || g.N == 0; }),
+             dw.end());
+    if (dt() == ADAPTRA_BF16) {
+      for (size_t i = 0; i < dw.size(); i += 24)
+        TRY(gemm_tc_grouped(dw.data() + i, (int)std::min<size_t>(24, dw.size() - i), st));
+    } else {
+      for (auto& g : dw) TRY(gemm_simt(g, st));
     }
     return ADAPTRA_OK;
   }
