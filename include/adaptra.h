@@ -322,6 +322,12 @@ int adaptra_outbox_close(adaptra_outbox_t ob);
 void* adaptra_outbox_dst(adaptra_outbox_t ob, int32_t mb);
 /* Injected latency in ns (>= 0), or ADAPTRA_LINK_DOWN (delegated host path). */
 int adaptra_set_link_latency(adaptra_outbox_t ob, int64_t latency_ns);
+/* The P2P link mode's transfer kernel (P:1575-1577 inter-stage activations /
+ * gradients): copies `bytes` from `src` to `dst` (device pointers, either may
+ * be a peer GPU's memory; peer access is enabled on first use) on `stream` with 16-byte
+ * vector loads/stores from 32 CTAs (few SMs taken from compute); falls back to
+ * cudaMemcpyAsync when not 16-byte aligned.  Exposed for transfer benchmarks. */
+int adaptra_p2p_copy(void* dst, const void* src, int64_t bytes, void* stream);
 /* Send message mb of iteration epoch once the work already enqueued on
  * `producer` (the producing op) has completed. */
 int adaptra_send(adaptra_outbox_t ob, int32_t mb, void* producer, uint32_t epoch);

@@ -94,6 +94,7 @@ _SIGS = {
     "adaptra_gemm": (_i32, [_P(GemmDesc), _vp]),
     "adaptra_prof_enable": (_i32, [_i32]),
     "adaptra_launch_count": (_i64, []),
+    "adaptra_p2p_copy": (_i32, [C.c_void_p, C.c_void_p, _i64, C.c_void_p]),
     "adaptra_prof_collect": (_i32, [_i32, _P(_i64), _P(C.c_double), _P(C.c_double), _P(C.c_double)]),
     "adaptra_prof_collect_ex": (_i32, [_i32, _P(_i64), _P(C.c_double), _P(C.c_double), _P(C.c_double),
                                        _P(C.c_double)]),

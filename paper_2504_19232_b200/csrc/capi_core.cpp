@@ -4,6 +4,7 @@
 #include <string>
 
 #include "../../include/adaptra.h"
+#include "kernels/kernels.h"
 #include "util.h"
 
 namespace adaptra {
@@ -30,4 +31,21 @@ extern "C" int adaptra_gemm(const adaptra_gemm_desc_t* g, void* stream) {
   if (g->dtype == ADAPTRA_BF16) return adaptra::gemm_tc(*g, st);
   if (g->dtype == ADAPTRA_F32) return adaptra::gemm_simt(*g, st);
   return adaptra::set_error(ADAPTRA_EINVAL, "adaptra_gemm: bad dtype");
+}
+
+extern "C" int adaptra_p2p_copy(void* dst, const void* src, int64_t bytes, void* stream) {
+  if (!dst || !src || bytes < 0) return adaptra::set_error(ADAPTRA_EINVAL, "adaptra_p2p_copy: bad args");
+  if (bytes == 0) return ADAPTRA_OK;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (const void* p : {(const void*)dst, src}) {  // a peer GPU's buffer: enable peer access once
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) == cudaSuccess && a.type == cudaMemoryTypeDevice && a.device != cur) {
+      cudaError_t e = cudaDeviceEnablePeerAccess(a.device, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+        return adaptra::set_error(ADAPTRA_ECUDA, "adaptra_p2p_copy: no peer access");
+    }
+    cudaGetLastError();
+  }
+  return adaptra::copy_async(dst, src, (long)bytes, (cudaStream_t)stream);
 }
