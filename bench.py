@@ -29,7 +29,18 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
-os.environ["NCCL_DEBUG"] = "WARN"  # keep stdout to the one JSON line (NCCL prints its version otherwise)
+os.environ["NCCL_DEBUG"] = "WARN"
+JSON_OUT = sys.stdout
+
+
+def _isolate_stdout():
+    """stdout carries exactly the one JSON line: the line goes to a duplicate
+    of the original stdout, and file descriptor 1 is pointed at stderr for
+    every library that prints (NCCL reports its version on stdout under
+    torchrun).  Only when run as the bench script, not on import."""
+    global JSON_OUT
+    JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
 
 
 def parse():
@@ -439,7 +450,7 @@ def main():
         }
         if not args.no_cpu and world == 1:  # rank 0 at N = 1 only
             line["cpu_baseline"] = cpu_baseline(model, S, N)
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=JSON_OUT, flush=True)
     pipe.close()
     if world > 1:
         dist.barrier(group=group)
@@ -533,9 +544,10 @@ def reference_arm(args, rank, world):
                                      f"S={S} N={N} seq={T} d={d}"},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line), file=JSON_OUT, flush=True)
     return 0
 
 
 if __name__ == "__main__":
+    _isolate_stdout()
     sys.exit(main() or 0)
