@@ -82,7 +82,7 @@ class Pipeline:
                 self._init_params(st, i, seed)
             self.stages[i] = st
         # ---------------- io
-        tdt = self.stages[self.local[0]].tdt
+        tdt = torch.bfloat16 if model.dtype == L.BF16 else torch.float32  # (a rank may host no stage: S < world)
         R = model.tokens_per_mb
         self.inputs, self.targets = [], []
         if 0 in self.stages:
