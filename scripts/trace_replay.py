@@ -6,6 +6,9 @@ iteration by iteration on 8 stages, compressed `--compress`x in time (1200 ->
   online    planner fed the transport's measured latencies (lag 1)
   zb        fixed ZB order (Alg. 2 plan at c = 0)
   1f1b      fixed 1F1B order
+  zb-inorder / 1f1b-inorder  the same orders with blocking sends / receives
+            in the compute sequence (the paper's NCCL-in-order
+            baselines, head-of-line blocking)
 on the same kernels and transport.  Latencies are scaled per R22 (latency_ms
 in units of the paper's t = 10 ms, times the measured stage t_F); the failed
 link carries its traffic on the delegated host path in every arm (the fixed
@@ -103,7 +106,7 @@ def main():
         mon = LinkMonitor(pipe, gather)
         for l in range(S - 1):
             pipe.set_latency(l, 0)
-        pipe.run(base.plan([0] * (S - 1)), merge_w=base.merge_w)  # warm-up at nominal
+        pipe.run(base.plan([0] * (S - 1)), merge_w=base.merge_w, inorder=base.inorder)  # warm-up at nominal
         mon.sample()
         if world > 1:
             dist.barrier(group=group)
@@ -117,7 +120,7 @@ def main():
             orders = online.orders() if online else base.plan(c)
             ev0, ev1 = torch.cuda.Event(True), torch.cuda.Event(True)
             ev0.record()
-            res = pipe.run(orders, merge_w=base.merge_w)
+            res = pipe.run(orders, merge_w=base.merge_w, inorder=base.inorder)
             ev1.record()
             torch.cuda.synchronize()
             g = gather((ev0.elapsed_time(ev1), sum(st["busy_ns"] for st in res.stats.values())))
