@@ -1,9 +1,11 @@
-"""Parity at BASELINE.json's full C1 sizes: one GPT-2 block of the 1.3B-shaped
-stack (d=2048, 16 heads x 128, d_ff=8192, T=2048 tokens), bf16, run through the
-same C-ABI stage calls and GEMM configurations (2-CTA 256x256 tcgen05 tiles,
-batched causal attention tiles) as bench.py, against the float64 oracle on
-the same inputs: every element of y, dx and every gradient, tolerance 2e-2
-(max relative error, R20)."""
+"""Parity at BASELINE.json's full sizes: GPT-2 blocks of the 1.3B-shaped stack
+(C1: d=2048, 16 heads x 128, d_ff=8192) and of the 7B-shaped stack (C2/C3:
+d=4096, 32 heads x 128, d_ff=16384), T=2048 tokens, bf16, run through the same
+C-ABI stage calls and kernel configurations as bench.py (2-CTA 256x256
+tcgen05 tiles, fused flash attention, the grouped dW launch: 4 products per
+layer, 8 with two layers) against the float64 oracle on the same inputs:
+every element of y, dx and every gradient, tolerance 2e-2 (max relative
+error, R20)."""
 import numpy as np
 import pytest
 import torch
@@ -20,15 +22,20 @@ def rel(a, b):
     return float(np.abs(np.asarray(a, np.float64) - b).max() / max(np.abs(b).max(), 1e-30))
 
 
-@pytest.mark.parametrize("last", [False, True])
-def test_c1_block_fbw(last):
-    d, dff, H, T, b = 2048, 8192, 16, 2048, 1
-    params = sy.gpt_params(0, 1, 1, d, dff, perturb=True, bf16=True)[0]
+@pytest.mark.parametrize("d,dff,H,nl,last", [
+    (2048, 8192, 16, 1, False),     # C1 block
+    (2048, 8192, 16, 1, True),      # C1 block, last stage (loss + dy seed)
+    (2048, 8192, 16, 2, False),     # C1, two layers: 8 grouped dW products
+    (4096, 16384, 32, 1, False),    # C2/C3 7B-shaped block
+])
+def test_full_size_block_fbw(d, dff, H, nl, last):
+    T, b = 2048, 1
+    params = sy.gpt_params(0, 1, nl, d, dff, perturb=True, bf16=True)[0]
     # scale the perturbed projections down to GPT-2 magnitudes at this width
     x = sy.microbatches(1, 1, b, T, d, bf16=True)[0]
     tgt = sy.targets(2, 1, b, T, d)[0]
     dy = sy.microbatches(3, 1, b, T, d, bf16=True)[0]
-    st = Stage(L.BLOCK_GPT, L.BF16, 1, d, dff, H, b, T, False, last, 1, 1, "cuda")
+    st = Stage(L.BLOCK_GPT, L.BF16, nl, d, dff, H, b, T, False, last, 1, 1, "cuda")
     st.load_params(params)
     st.zero_grads()
     xin = torch.from_numpy(x.reshape(T, d)).to("cuda", torch.bfloat16)
@@ -39,7 +46,7 @@ def test_c1_block_fbw(last):
     st.B(0, None if last else torch.from_numpy(dy.reshape(T, d)).to("cuda", torch.bfloat16), dx)
     st.W(0)
     torch.cuda.synchronize()
-    p64 = [{k: np.asarray(v, np.float64) for k, v in params[0].items()}]
+    p64 = [{k: np.asarray(v, np.float64) for k, v in layer.items()} for layer in params]
     yr, caches = nu.stage_F("gpt", p64, x.astype(np.float64), H)
     if last:
         Lr, dyr = nu.mse_loss(yr, tgt.astype(np.float64), 1)
@@ -51,6 +58,7 @@ def test_c1_block_fbw(last):
     assert rel(dx.double().cpu().numpy().reshape(dxr.shape), dxr) < 2e-2
     gw = nu.stage_W("gpt", caches, gc)
     got = st.grads()
-    for k, ref in gw[0].items():
-        e = rel(got[0][k], ref)
-        assert e < 2e-2, (k, e)
+    for l in range(nl):
+        for k, ref in gw[l].items():
+            e = rel(got[l][k], ref)
+            assert e < 2e-2, (l, k, e)
