@@ -101,3 +101,23 @@ def test_latency_injection_and_link_down(mode):
         _check(pipe, res, Lref, gref, 1e-4)
     finally:
         pipe.close()
+
+
+def test_pipeline_full_size_c1_layers():
+    """The whole pipelined iteration at C1 sizes (d=2048, 16 heads, d_ff=8192,
+    T=2048, bf16): 2 stages x 2 layers, N=2, adaptive arm with 2 ms injected on
+    the link -- producer epilogues storing into the peer mailbox, fused
+    attention, grouped dW launches -- vs the fp64 full batch (P12, 2e-2)."""
+    S, N, Lt, d, dff, H, b, T = 2, 2, 4, 2048, 8192, 16, 1, 2048
+    pipe, Lref, gref = _setup("gpt", L.BF16, S, N, Lt, d, dff, H, b, T)
+    try:
+        t = [1_000_000] * S
+        a = Arm("adaptive", S, N, t, t, t)
+        c = [2_000_000]
+        pipe.set_latency(0, c[0])
+        orders = a.plan(c)
+        res = pipe.run(orders, merge_w=a.merge_w, want_times=True)
+        _check(pipe, res, Lref, gref, 2e-2)
+    finally:
+        pipe.set_latency(0, 0)
+        pipe.close()
