@@ -129,6 +129,12 @@ int adaptra_validate(int32_t S, int32_t N, const int64_t* tF, const int64_t* tB,
 #define ADAPTRA_EPI_ACC_F32 4   /* Cf32[m,n] += alpha*acc   (deferred W accumulation)      */
 #define ADAPTRA_EPI_STORE_F32 5 /* Cf32[m,n] = alpha*acc                                   */
 #define ADAPTRA_EPI_DSOFTMAX 6  /* C = aux[m,n] * (acc - rowv[m]) * alpha  (softmax bwd)   */
+/* C = acc (bf16) and, per 128-column head h and row m = s*T + t,
+ * rowv[(s*H + h)*T + t] = sum_c bf16(C[m,c]) * aux[m,c]: the attention
+ * backward's D = rowsum(dO o O) fused into the GEMM that produces dO
+ * (rowv_1 = T tokens per sequence, rowv_2 = H heads; bf16, N % 256 == 0,
+ * unbatched, the 2-CTA 256-wide tile path only). */
+#define ADAPTRA_EPI_STORE_ROWDOT 7
 
 #define ADAPTRA_CAUSAL_NONE 0
 #define ADAPTRA_CAUSAL_TILE 1   /* skip output tiles strictly above the diagonal           */

@@ -29,7 +29,10 @@ extern "C" int adaptra_gemm(const adaptra_gemm_desc_t* g, void* stream) {
   if (g->M == 0 || g->N == 0) return ADAPTRA_OK;
   cudaStream_t st = (cudaStream_t)stream;
   if (g->dtype == ADAPTRA_BF16) return adaptra::gemm_tc(*g, st);
-  if (g->dtype == ADAPTRA_F32) return adaptra::gemm_simt(*g, st);
+  if (g->dtype == ADAPTRA_F32) {
+    if (g->epi == ADAPTRA_EPI_STORE_ROWDOT) return adaptra::set_error(ADAPTRA_EINVAL, "STORE_ROWDOT is bf16-only");
+    return adaptra::gemm_simt(*g, st);
+  }
   return adaptra::set_error(ADAPTRA_EINVAL, "adaptra_gemm: bad dtype");
 }
 

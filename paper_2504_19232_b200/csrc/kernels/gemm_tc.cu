@@ -124,7 +124,8 @@ __device__ __forceinline__ void epilogue_loop(const adaptra_gemm_desc_t& g, cons
   // global load is then in flight at the fence.proxy.async of a chunk (it
   // compiles to MEMBAR.ALL.CTA, which would wait for it).
   const bool f32o = (g.epi == ADAPTRA_EPI_ACC_F32 || g.epi == ADAPTRA_EPI_STORE_F32);
-  const bool has_in = (g.epi == ADAPTRA_EPI_RESID || g.epi == ADAPTRA_EPI_DGELU || g.epi == ADAPTRA_EPI_DSOFTMAX);
+  const bool has_in = (g.epi == ADAPTRA_EPI_RESID || g.epi == ADAPTRA_EPI_DGELU || g.epi == ADAPTRA_EPI_DSOFTMAX ||
+                       g.epi == ADAPTRA_EPI_STORE_ROWDOT);
   for (int t = cid; t < n_tiles; t += ncl) {
     int mb, nb, z, kb0, kb1;
     tile_coords(t, ti, mb, nb, z);
@@ -151,6 +152,7 @@ __device__ __forceinline__ void epilogue_loop(const adaptra_gemm_desc_t& g, cons
       for (int c = 0; c < NC; ++c) tma_load_2d(stg + c * 2048, tmX, inbar, xcol + c * 32, xrow);
     }
     const float Dm = (g.epi == ADAPTRA_EPI_DSOFTMAX && row_ok) ? e.rowv[m] : 0.f;
+    float rdot = 0.f;  // EPI_STORE_ROWDOT: this warp's 128 columns are one head
     mbar_wait(&tfull[acc], acc_phase);
     tc_fence_after();
     const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + co;
@@ -232,6 +234,13 @@ __device__ __forceinline__ void epilogue_loop(const adaptra_gemm_desc_t& g, cons
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = in[j] * (v[j] - Dm) * e.alpha;
           break;
+        case ADAPTRA_EPI_STORE_ROWDOT:
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            v[j] = __bfloat162float(__float2bfloat16_rn(v[j]));  // the stored dO
+            rdot = fmaf(v[j], in[j], rdot);
+          }
+          break;
         default:  // ACC_F32, STORE_F32
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] *= e.alpha;
@@ -263,6 +272,11 @@ __device__ __forceinline__ void epilogue_loop(const adaptra_gemm_desc_t& g, cons
       }
     }
     if (in_tma) in_phase ^= 1;
+    if (g.epi == ADAPTRA_EPI_STORE_ROWDOT && row_ok && et.on == 1) {
+      const int Tn = (int)g.rowv_1, Hn = (int)g.rowv_2;
+      const int head = (nb * BN + co) / 128, sq = m / Tn, t = m - sq * Tn;
+      const_cast<float*>(g.rowv)[((size_t)sq * Hn + head) * Tn + t] = rdot;
+    }
     tc_fence_before();
     __syncwarp();
     if (lane == 0) {
@@ -599,7 +613,8 @@ static int launch_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
            decomp(g.aux_1, g.aux_2, g.ldaux, et.x_r1, et.x_r2, et.x_q1, et.x_q2, xr, xc) &&
            make_map(&mx, g.aux, xr, g.Z == 1 ? g.N : xc, g.ldaux, 32, 32, false, 64) == ADAPTRA_OK;
     }
-    if (ok && (g.epi == ADAPTRA_EPI_DGELU || g.epi == ADAPTRA_EPI_DSOFTMAX) && g.aux && (uintptr_t)g.aux % 16 == 0 &&
+    if (ok && (g.epi == ADAPTRA_EPI_DGELU || g.epi == ADAPTRA_EPI_DSOFTMAX || g.epi == ADAPTRA_EPI_STORE_ROWDOT) &&
+        g.aux && (uintptr_t)g.aux % 16 == 0 &&
         (g.ldaux * 2) % 16 == 0) {
       int64_t xr = 0, xc = 0;
       et.in_tma = decomp(g.aux_1, g.aux_2, g.ldaux, et.x_r1, et.x_r2, et.x_q1, et.x_q2, xr, xc) &&
@@ -610,10 +625,14 @@ static int launch_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
       et.in_tma = make_map(&mx, g.R, g.M, g.N, g.ldr, 32, 32, false, 64) == ADAPTRA_OK;
     }
     static const bool no_in_tma = getenv("ADAPTRA_EPI_IN_LDG") != nullptr;  // timing comparison only
-    if (no_in_tma) et.in_tma = 0;
+    if (no_in_tma && g.epi != ADAPTRA_EPI_STORE_ROWDOT) et.in_tma = 0;
     et.on = ok ? 1 : 0;
     // timing experiments only: 1 = skip all epilogue work, 2 = skip the TMA store
     static const int diag = getenv("ADAPTRA_DIAG_NOEPI") ? atoi(getenv("ADAPTRA_DIAG_NOEPI")) : 0;
+    if (g.epi == ADAPTRA_EPI_STORE_ROWDOT && !(et.on == 1 && et.in_tma && CG == 2 && BN == 256)) {
+      cudaGetLastError();
+      return set_error(ADAPTRA_EINVAL, "STORE_ROWDOT needs the TMA epilogue of the 2-CTA 256-wide path");
+    }
     if (diag == 1 && ok) et.on = 2;
     if (diag == 2 && ok) et.on = 3;
     cudaGetLastError();
@@ -923,6 +942,10 @@ int gemm_tc_grouped(const adaptra_gemm_desc_t* gs, int n, cudaStream_t st) {
 }
 
 int gemm_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
+  if (g.epi == ADAPTRA_EPI_STORE_ROWDOT &&
+      (g.Z != 1 || g.N % 256 || g.N < 2048 || g.M < 256 || g.causal || !g.aux || !g.rowv || g.rowv_1 < 1 ||
+       g.rowv_2 < 1))
+    return set_error(ADAPTRA_EINVAL, "STORE_ROWDOT: unbatched, N % 256 == 0, N >= 2048, aux and rowv required");
   // BN = 256 for large unbatched N, else 128 (batched attention tiles must not
   // cross a batch boundary: require tile-aligned extents when Z > 1).
   if (g.Z > 1 && (g.M % BM || g.K % BK)) return set_error(ADAPTRA_EINVAL, "batched tc gemm needs M%128==0, K%64==0");

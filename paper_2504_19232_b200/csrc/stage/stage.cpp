@@ -356,9 +356,14 @@ struct StageOps {
       // dh2 = da W1 ; dy1 = dy + LN2_bwd(dh2)
       TRY(GB(dt()).shape(R, Dm, Ff).A(da, Ff, R, Ff).B(W(p.W1), Dm, Ff, Dm, 1).C(dh2, Dm).run(st));
       TRY(ln_bwd<T>(dh2, y1, fbuf(slot, l, s->L.mean2), fbuf(slot, l, s->L.rstd2), V(p.ln2_g), dy, dy1, R, Dm, st));
-      // do = dy1 Wo
-      TRY(GB(dt()).shape(R, Dm, Dm).A(dy1, Dm, R, Dm).B(W(p.Wo), Dm, Dm, Dm, 1).C(dO, Dm).run(st));
-      TRY(attn_rowdot<T>(dO, o, Dv, b, H, Tn, dh, Dm, st));
+      // do = dy1 Wo ; D = rowsum(do o o) per head (fused into the GEMM's epilogue on the tcgen05 path)
+      if (s->L.flash && Dm % 256 == 0 && Dm >= 2048) {
+        TRY(GB(dt()).shape(R, Dm, Dm).A(dy1, Dm, R, Dm).B(W(p.Wo), Dm, Dm, Dm, 1).C(dO, Dm)
+                .epi(ADAPTRA_EPI_STORE_ROWDOT).aux(o, Dm).rowv(Dv, Tn, H).run(st));
+      } else {
+        TRY(GB(dt()).shape(R, Dm, Dm).A(dy1, Dm, R, Dm).B(W(p.Wo), Dm, Dm, Dm, 1).C(dO, Dm).run(st));
+        TRY(attn_rowdot<T>(dO, o, Dv, b, H, Tn, dh, Dm, st));
+      }
       if (s->L.flash) {
         float* dq_acc = (float*)((char*)D.work + s->L.w_dq);
         TRY(attn_bwd_tc((const bf16*)qkv, (const bf16*)dO, (const float*)P, Dv, (bf16*)dqkv, dq_acc, b, H, Tn, (int)Dm,
