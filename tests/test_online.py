@@ -71,3 +71,45 @@ def test_online_planner_matches_oracle_on_lagged_quantised_sequence(S, N, seed, 
                 assert q[link] > 0
             elif link not in downs[k - 1]:
                 assert q[link] == 0
+
+
+class _FakePipe:
+    """Stands in for a Pipeline: only the attributes LinkMonitor reads."""
+
+    def __init__(self, S, out_fwd, out_bwd):
+        self.S, self.out_fwd, self.out_bwd = S, out_fwd, out_bwd
+
+
+def test_link_monitor_pools_directions_and_ranks():
+    """Per link: (sum of both directions' delays) / (their message count) over
+    the interval since the previous sample, merged across ranks; max of the
+    maxima; a link without gated messages measures 0 (R32, R16)."""
+    from paper_2504_19232_b200 import online
+
+    # two "ranks": rank A owns stage 0..1 outboxes, rank B stages 2..3 (S = 4)
+    stats = {"A": {("fwd", 0): (0, 0, 0), ("fwd", 1): (0, 0, 0), ("bwd", 0): (0, 0, 0)},
+             "B": {("bwd", 1): (0, 0, 0), ("bwd", 2): (0, 0, 0), ("fwd", 2): (0, 0, 0)}}
+    mons = {}
+    for r in ("A", "B"):
+        m = online.LinkMonitor.__new__(online.LinkMonitor)
+        m.pipe, m.S = _FakePipe(4, {}, {}), 4
+        m._read = (lambda rr: (lambda: dict(stats[rr])))(r)
+        m._last = m._read()
+        mons[r] = m
+    # interval: link 0 fwd 4 msgs x 1000 ns (rank A); link 0 bwd 4 msgs x 3000 ns (rank B's stage 1 outbox)
+    #           link 1 fwd 2 msgs x 500, max 700 (rank A); link 2: nothing gated
+    stats["A"][("fwd", 0)] = (4, 4000, 1000)
+    stats["B"][("bwd", 0)] = (4, 12000, 3000)
+    stats["A"][("fwd", 1)] = (2, 1000, 700)
+    parts = {}
+    for r in ("A", "B"):
+        cur = mons[r]._read()
+        parts[r] = {k: (v[0] - mons[r]._last.get(k, (0, 0, 0))[0], v[1] - mons[r]._last.get(k, (0, 0, 0))[1], v[2])
+                    for k, v in cur.items()}
+    gather = lambda _o: [parts["A"], parts["B"]]
+    m = mons["A"]
+    m.gather = gather
+    m._read = lambda: dict(stats["A"])
+    mean, mx = m.sample()
+    assert mean == [2000, 500, 0]        # (4000 + 12000) / 8 ; 1000 / 2 ; none
+    assert mx == [3000, 700, 0]
