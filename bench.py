@@ -293,7 +293,7 @@ def main():
             res = one_step(warmup + k)
             if res.loss is not None:
                 losses.append(res.loss)   # D2H read of the step's result
-            span = max(st["last_end_ns"] for st in res.stats.values())
+            span = max((st["last_end_ns"] for st in res.stats.values()), default=0)
             busy = sum(st["busy_ns"] for st in res.stats.values())
             # device-level busy: union of this rank's op intervals
             iv = sorted(t for st in res.stats.values() for t in st["op_times"])
