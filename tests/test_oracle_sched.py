@@ -251,3 +251,26 @@ def test_plan_properties(S, N, xmax):
         dl = xa[i] - xa[i + 1]
         # Either Eq. 1 holds or the clip (N-2S, or the R11 cap at N) is active
         assert ok[i] or dl == max(0, N - 2 * S) or xa[i] == N
+
+
+def test_p13_bubble_formula():
+    """R15: utilisation bubble 1 - sum(busy)/(S T).  The ideal ZB schedule
+     has no interior gaps ("zero bubbles") and utilisation
+    bubble 1/13; the paper's three (T, bubble) pairs of the 7B microbenchmark
+    (ZB 703 ms / 57.4 %, Adaptra-CPU 579 / 48.8 %, Adaptra 398 / 25.3 %,
+    S = 4) imply the same total busy time (about 1.19 s) only under this form."""
+    X, T, _ = sc.schedule(4, 12, T10, T10, T10, [0, 0, 0], [7, 5, 3, 1], 1)
+    m = sc.metrics(4, X, T)
+    assert T == 390 and m["interior_bubble"] == 0.0
+    assert abs(m["util_bubble"] - 1 / 13) < 1e-12
+    busy = [4 * t * (1 - b) for t, b in ((703, 0.574), (579, 0.488), (398, 0.253))]
+    assert max(busy) / min(busy) < 1.015 and all(1180 < v < 1200 for v in busy)
+
+
+def test_peak_activations_equal_the_plan():
+    """Peak in-flight forwards per stage (max over time of #F - #B) equals the
+    warm-up plan on the ideal ZB timeline ([7, 5, 3, 1]) and on an adapted
+    plan ([9, 5, 3, 1]) at c = 0 (SPEC peak_activations examples, derived)."""
+    for x in ([7, 5, 3, 1], [9, 5, 3, 1]):
+        X, T, _ = sc.schedule(4, 12, T10, T10, T10, [0, 0, 0], x, 1)
+        assert sc.metrics(4, X, T)["peak_inflight"] == x
