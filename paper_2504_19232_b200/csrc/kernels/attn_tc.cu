@@ -11,7 +11,8 @@
 //   S^T = K Q_i^T, dP^T = V dO_i^T (TMEM) -> P^T = exp(S^T/sqrt(dh) - LSE_i),
 //   dS^T = P^T (dP^T - D_i) (bf16, shared memory) -> dV += P^T dO_i,
 //   dK += dS^T Q_i, dQ_i^T(partial) = K^T dS_i^T (TMEM) -> TMA reduce-add into
-//   an fp32 dQ^T accumulator.  D_i = rowsum(dO_i o O_i) comes from attn_rowdot.
+//   an fp32 dQ^T accumulator.  D_i = rowsum(dO_i o O_i) comes from the epilogue
+//   of the GEMM that produces dO (EPI_STORE_ROWDOT; attn_rowdot elsewhere).
 // Warp roles: 0 TMA producer, 1 TMEM allocator + MMA issuer, 2..5 softmax /
 // gradient / epilogue warps (thread = TMEM lane = tile row).
 #include <cuda.h>
