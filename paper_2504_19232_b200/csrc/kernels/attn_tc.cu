@@ -13,8 +13,10 @@
 //   dK += dS^T Q_i, dQ_i^T(partial) = K^T dS_i^T (TMEM) -> TMA reduce-add into
 //   an fp32 dQ^T accumulator.  D_i = rowsum(dO_i o O_i) comes from the epilogue
 //   of the GEMM that produces dO (EPI_STORE_ROWDOT; attn_rowdot elsewhere).
-// Warp roles: 0 TMA producer, 1 TMEM allocator + MMA issuer, 2..5 softmax /
-// gradient / epilogue warps (thread = TMEM lane = tile row).
+// Warp roles: 0 TMA producer, 1 TMEM allocator + MMA issuer; forward: 2..9
+// softmax / epilogue warps (lane quadrant x column half); backward: 2..17
+// gradient warps (lane quadrant x 16-query column group), 18..21 dQ^T drain
+// warps (thread = TMEM lane = tile row).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
