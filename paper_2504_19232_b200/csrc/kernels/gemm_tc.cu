@@ -4,13 +4,17 @@
 // Persistent warp-specialised kernel, one CTA per SM (CG = 1) or one CTA pair
 // per 2 SMs (CG = 2, tcgen05 cta_group::2: a 256 x BN tile whose A rows and B
 // rows are split over the two CTAs' shared memory, MMA issued by the leader):
-//   warp 0      TMA producer (one elected lane) -> smem ring of kStages stages
-//   warp 1      TMEM allocator + MMA issuer (one elected lane, tcgen05.mma
-//               kind::f16, (128 CG) x BN x 16 per instruction, fp32 accumulate)
-//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> fused epilogue ->
+//   warps 0..7  epilogue (two warpgroups, setmaxnreg 208): tcgen05.ld TMEM ->
+//               registers -> fused epilogue (bias / GeLU / residual / dGeLU /
+//               row-dot; residual and GeLU inputs arrive by TMA) -> swizzled
 //               shared-memory staging -> TMA store / TMA reduce-add
+//   warp 8      TMA producer (one elected lane) -> smem ring of kStages stages
+//   warp 9      TMEM allocator + MMA issuer (one elected lane, tcgen05.mma
+//               kind::f16, (128 CG) x BN x 16 per instruction, fp32 accumulate)
+//   warps 10,11 idle (complete the setmaxnreg-decreased warpgroup)
 // Two TMEM accumulators (2 x BN columns) let the epilogue of tile t overlap
-// the main loop of tile t+1.  Operands may be K-major or MN-major (SWIZZLE_128B
+// the main loop of tile t+1.  gemm_tc_grouped_kernel runs all dW products of
+// a W op as one persistent launch over the union of their tiles.  Operands may be K-major or MN-major (SWIZZLE_128B
 // canonical layouts, selected by the instruction descriptor's major bits), so
 // dX = dY W and dW = dY^T X read the stored activations without transposes.
 #include <cuda.h>
