@@ -418,7 +418,7 @@ def main():
             "bubble_rate": round(head["bubble"], 4), "device_bubble_rate": round(head["device_bubble"], 4),
             "step_tflops": round(head["step_tflops"], 1),
             "step_tflops_frac_of_peak": round(head["step_tflops"] / (world * peaks.get("bf16_tflops_sustained", 1400.0)), 4),
-            "config": {"workload": f"{'C2/C3 (7B-shaped)' if args.model == '7b' else ('C3, 8 stages, 1.3B-shaped blocks' if S == 8 else 'C1 (largest single-GPU config: 8 stages x N=32 need ~166 GB of W stash)')}: GPT-style "
+            "config": {"workload": f"{'C2/C3 (7B-shaped)' if args.model == '7b' else ('C3, 8 stages, 1.3B-shaped blocks' if S == 8 else ('C1 (largest single-GPU config: 8 stages x N=32 need ~166 GB of W stash)' if world == 1 else 'C1'))}: GPT-style "
                                    f"{args.layers}x(d={args.d},h={args.heads},ff={4 * args.d}) "
                                    f"S={S} N={N} seq={args.T} bf16, paper trace compressed 1 event/step",
                        "stages": S, "microbatches": N, "tokens_per_step": N * model.tokens_per_mb,
