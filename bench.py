@@ -409,6 +409,15 @@ def main():
             fused_line["flops"] = "algorithmic causal half: fwd 4 T^2 dh H / 2, bwd 8 T^2 dh H / 2 (R28)"
         else:
             fused_line = None
+        # DRAM bytes per launch of a representative linear-layer GEMM, from the
+        # committed ncu --set full capture (cold cache)
+        traffic, traffic_src = None, None
+        tp = os.path.join(ROOT, "profiles", "r01_ncu_gemm_traffic.json")
+        if os.path.exists(tp):
+            rec = json.load(open(tp))["launches"][0]
+            traffic = rec["dram_bytes"]
+            traffic_src = (f"profiles/r01_ncu_gemm_traffic.json: {rec['shape']}, {rec['dram_bytes']} B per launch "
+                           f"vs {rec['algorithmic_bytes']} B algorithmic")
         line = {
             "metric": "tokens/sec and bubble rate at 8 stages under injected straggler trace",
             "value": round(head["tokens_per_s"], 1), "unit": "tokens/s", "n_gpus": world,
@@ -429,7 +438,8 @@ def main():
                      for (a, w), r in results.items()},
             "roofline": {"bound": "tensor", "achieved": round(achieved, 1) if achieved else None,
                          "peak": peak, "unit": "TFLOP/s",
-                         "frac": round(achieved / peak, 4) if achieved else None, "traffic": None,
+                         "frac": round(achieved / peak, 4) if achieved else None, "traffic": traffic,
+                         "traffic_source": traffic_src,
                          "kernel": "gemm_tc_kernel (tcgen05), stage linear layers (Z=1)", "launches": n_l,
                          "avg_launch_us": round(avg_ms * 1e3, 2),
                          "note": "per-launch CUDA-event durations on the launching stream during the timed "
