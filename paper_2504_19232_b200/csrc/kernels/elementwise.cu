@@ -5,6 +5,7 @@
 // is aligned; fp32 arithmetic everywhere.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <string>
 
 #include "../../../include/adaptra.h"
@@ -473,6 +474,84 @@ int copy_async(void* dst, const void* src, long bytes, cudaStream_t st) {
   return launch_check("copy16");
 }
 
+// All column sums of a W op (bias gradients db += sum_rows dY and LN
+// parameter gradients) in one launch: job j owns blocks [start_j, start_j +
+// nbx_j * nby); each block is colsum_vec_kernel's 64 columns x 256 rows.
+template <typename T>
+__global__ void __launch_bounds__(256) colsum_grouped_kernel(const ColsumGroup g) {
+  int j = 0;
+  while (j + 1 < g.n && (int)blockIdx.x >= g.job[j + 1].start) ++j;
+  const ColsumJob& J = g.job[j];
+  const int b = blockIdx.x - J.start, bx = b % J.nbx, by = b / J.nbx;
+  const T* __restrict__ y = (const T*)J.y;
+  const T* __restrict__ x = (const T*)J.x;
+  const int N = J.N, R = g.R;
+  __shared__ float sa[32][65], sb[32][65];
+  const int cg = threadIdx.x & 7, rl = threadIdx.x >> 3;
+  const int c0 = bx * 64 + cg * 8;
+  const int r0 = by * 256;
+  float a[8] = {}, bsum[8] = {};
+  if (c0 < N) {
+    for (int r = r0 + rl; r < min(R, r0 + 256); r += 32) {
+      float v[8];
+      load8(y + (long)r * N + c0, v);
+      if (J.ln) {
+        float xv[8];
+        load8(x + (long)r * N + c0, xv);
+        const float mu = J.mean[r], rs = J.rstd[r];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          a[k] += v[k] * (xv[k] - mu) * rs;
+          bsum[k] += v[k];
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a[k] += v[k];
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    sa[rl][cg * 8 + k] = a[k];
+    sb[rl][cg * 8 + k] = bsum[k];
+  }
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    const int c = bx * 64 + threadIdx.x;
+    float ta = 0.f, tb = 0.f;
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) {
+      ta += sa[k][threadIdx.x];
+      tb += sb[k][threadIdx.x];
+    }
+    if (c < N) {
+      atomicAdd(J.out_a + c, ta);
+      if (J.ln) atomicAdd(J.out_b + c, tb);
+    }
+  }
+}
+template <typename T>
+int colsum_grouped(const ColsumJob* jobs, int n, int R, cudaStream_t st) {
+  for (int i0 = 0; i0 < n; i0 += kMaxColsum) {
+    ColsumGroup g{};
+    g.n = std::min(kMaxColsum, n - i0);
+    g.R = R;
+    int blocks = 0;
+    for (int k = 0; k < g.n; ++k) {
+      g.job[k] = jobs[i0 + k];
+      if (g.job[k].N % 8) return set_error(ADAPTRA_EINVAL, "colsum_grouped: N % 8 != 0");
+      g.job[k].nbx = (g.job[k].N + 63) / 64;
+      g.job[k].start = blocks;
+      blocks += g.job[k].nbx * ((R + 255) / 256);
+    }
+    if (blocks == 0) continue;
+    colsum_grouped_kernel<T><<<blocks, 256, 0, st>>>(g);
+    int rc = launch_check("colsum_grouped");
+    if (rc) return rc;
+  }
+  return ADAPTRA_OK;
+}
+
 #define INST(T)                                                                                                   \
   template int ln_fwd<T>(const T*, const float*, const float*, T*, float*, float*, int, int, cudaStream_t);       \
   template int ln_bwd<T>(const T*, const T*, const float*, const float*, const float*, const T*, T*, int, int,    \
@@ -482,6 +561,7 @@ int copy_async(void* dst, const void* src, long bytes, cudaStream_t st) {
   template int col_sum<T>(const T*, float*, int, int, cudaStream_t);                                              \
   template int softmax_causal<T>(const float*, T*, int, int, cudaStream_t);                                       \
   template int attn_rowdot<T>(const T*, const T*, float*, int, int, int, int, int, cudaStream_t);                 \
+  template int colsum_grouped<T>(const ColsumJob*, int, int, cudaStream_t);                                       \
   template int mse_loss<T>(const T*, const float*, T*, float*, long, int, cudaStream_t);
 INST(float)
 INST(bf16)

@@ -24,6 +24,26 @@ int ln_param_grad(const T* dh, const T* x, const float* mean, const float* rstd,
                   cudaStream_t st);
 template <typename T>
 int col_sum(const T* y, float* out, int R, int N, cudaStream_t st);
+// One launch for many column sums (a W op's bias and LN parameter gradients):
+// ln = 0: out_a[c] += sum_r y[r,c];  ln = 1: out_a[c] += sum_r y (x - mean) rstd,
+// out_b[c] += sum_r y.  y, x row-major [R, N], N % 8 == 0.
+struct ColsumJob {
+  const void* y;
+  const void* x;
+  const float* mean;
+  const float* rstd;
+  float* out_a;
+  float* out_b;
+  int N, ln;
+  int start, nbx;  // filled by colsum_grouped
+};
+constexpr int kMaxColsum = 48;
+struct ColsumGroup {
+  int n, R;
+  ColsumJob job[kMaxColsum];
+};
+template <typename T>
+int colsum_grouped(const ColsumJob* jobs, int n, int R, cudaStream_t st);
 template <typename T>
 int softmax_causal(const float* S, T* P, int Z, int Tn, cudaStream_t st);
 template <typename T>

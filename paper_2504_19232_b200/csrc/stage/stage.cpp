@@ -409,6 +409,8 @@ struct StageOps {
     // them as grouped persistent launches (bias / LN parameter sums inline)
     std::vector<adaptra_gemm_desc_t> dw;
     dw.reserve(4 * D.n_layers);
+    std::vector<ColsumJob> cs;  // bias and LN parameter gradients, one grouped launch
+    cs.reserve(6 * D.n_layers);
     for (int l = D.n_layers - 1; l >= 0; --l) {
       ParamOff p = param_off(D, l);
       const T* dy = layer_dy(slot, l);
@@ -418,11 +420,11 @@ struct StageOps {
       // dW2 += dy^T g ; db2 += sum dy
       dw.push_back(GB(dt()).shape(Dm, Ff, R).A(dy, Dm, R, Dm, 1).B(g, Ff, R, Ff, 1).C(GW(p.W2), Ff)
               .epi(ADAPTRA_EPI_ACC_F32).g);
-      TRY(col_sum<T>(dy, GV(p.b2), R, Dm, st));
+      cs.push_back(ColsumJob{dy, nullptr, nullptr, nullptr, GV(p.b2), nullptr, (int)(Dm), 0, 0, 0});
       if (D.block == ADAPTRA_BLOCK_MLP) {
         dw.push_back(GB(dt()).shape(Ff, Dm, R).A(da, Ff, R, Ff, 1).B(x, Dm, R, Dm, 1).C(GW(p.W1), Dm)
                 .epi(ADAPTRA_EPI_ACC_F32).g);
-        TRY(col_sum<T>(da, GV(p.b1), R, Ff, st));
+        cs.push_back(ColsumJob{da, nullptr, nullptr, nullptr, GV(p.b1), nullptr, (int)(Ff), 0, 0, 0});
         continue;
       }
       T* h1 = buf(slot, l, s->L.h1);
@@ -435,17 +437,15 @@ struct StageOps {
       T* dh1 = buf(slot, l, s->L.dh1);
       dw.push_back(GB(dt()).shape(Ff, Dm, R).A(da, Ff, R, Ff, 1).B(h2, Dm, R, Dm, 1).C(GW(p.W1), Dm)
               .epi(ADAPTRA_EPI_ACC_F32).g);
-      TRY(col_sum<T>(da, GV(p.b1), R, Ff, st));
-      TRY(ln_param_grad<T>(dh2, y1, fbuf(slot, l, s->L.mean2), fbuf(slot, l, s->L.rstd2), GV(p.ln2_g), GV(p.ln2_b), R,
-                           Dm, st));
+      cs.push_back(ColsumJob{da, nullptr, nullptr, nullptr, GV(p.b1), nullptr, (int)(Ff), 0, 0, 0});
+      cs.push_back(ColsumJob{dh2, y1, fbuf(slot, l, s->L.mean2), fbuf(slot, l, s->L.rstd2), GV(p.ln2_g), GV(p.ln2_b), (int)Dm, 1, 0, 0});
       dw.push_back(GB(dt()).shape(Dm, Dm, R).A(dy1, Dm, R, Dm, 1).B(o, Dm, R, Dm, 1).C(GW(p.Wo), Dm)
               .epi(ADAPTRA_EPI_ACC_F32).g);
-      TRY(col_sum<T>(dy1, GV(p.bo), R, Dm, st));
+      cs.push_back(ColsumJob{dy1, nullptr, nullptr, nullptr, GV(p.bo), nullptr, (int)(Dm), 0, 0, 0});
       dw.push_back(GB(dt()).shape(3 * Dm, Dm, R).A(dqkv, 3 * Dm, R, 3 * Dm, 1).B(h1, Dm, R, Dm, 1).C(GW(p.Wqkv), Dm)
               .epi(ADAPTRA_EPI_ACC_F32).g);
-      TRY(col_sum<T>(dqkv, GV(p.bqkv), R, 3 * Dm, st));
-      TRY(ln_param_grad<T>(dh1, x, fbuf(slot, l, s->L.mean1), fbuf(slot, l, s->L.rstd1), GV(p.ln1_g), GV(p.ln1_b), R,
-                           Dm, st));
+      cs.push_back(ColsumJob{dqkv, nullptr, nullptr, nullptr, GV(p.bqkv), nullptr, (int)(3 * Dm), 0, 0, 0});
+      cs.push_back(ColsumJob{dh1, x, fbuf(slot, l, s->L.mean1), fbuf(slot, l, s->L.rstd1), GV(p.ln1_g), GV(p.ln1_b), (int)Dm, 1, 0, 0});
     }
     dw.erase(std::remove_if(dw.begin(), dw.end(), [](const adaptra_gemm_desc_t& g) { return g.M == 0 || g.N == 0; }),
              dw.end());
@@ -455,6 +455,7 @@ struct StageOps {
     } else {
       for (auto& g : dw) TRY(gemm_simt(g, st));
     }
+    TRY(colsum_grouped<T>(cs.data(), (int)cs.size(), (int)R, st));
     return ADAPTRA_OK;
   }
 };
