@@ -455,7 +455,21 @@ struct StageOps {
     } else {
       for (auto& g : dw) TRY(gemm_simt(g, st));
     }
-    TRY(colsum_grouped<T>(cs.data(), (int)cs.size(), (int)R, st));
+    // Column sums: one launch per sum by default.  The grouped launch is 13 %
+    // faster on the W op alone but one ~17k-block kernel crowds co-located
+    // stages' streams (1 GPU, 4 stages: -1.4 % step; 1 stage per GPU: within
+    // noise), so it is opt-in (ADAPTRA_COLSUM_GROUPED=1).
+    static const bool cs_grouped = getenv("ADAPTRA_COLSUM_GROUPED") && atoi(getenv("ADAPTRA_COLSUM_GROUPED")) == 1;
+    if (cs_grouped) {
+      TRY(colsum_grouped<T>(cs.data(), (int)cs.size(), (int)R, st));
+    } else {
+      for (const auto& j : cs) {
+        if (j.ln)
+          TRY(ln_param_grad<T>((const T*)j.y, (const T*)j.x, j.mean, j.rstd, j.out_a, j.out_b, (int)R, j.N, st));
+        else
+          TRY(col_sum<T>((const T*)j.y, j.out_a, (int)R, j.N, st));
+      }
+    }
     return ADAPTRA_OK;
   }
 };

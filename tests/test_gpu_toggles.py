@@ -1,0 +1,25 @@
+"""The non-default kernel paths behind environment toggles (read once per
+process by libadaptra) re-run the stage F / B / W parity suites (small and
+full-size) in a fresh process: grouped column sums (opt-in), one dW launch per product instead of
+the grouped GEMM, epilogue inputs by LDG instead of TMA."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("toggle", [{"ADAPTRA_COLSUM_GROUPED": "1"},
+                                    {"ADAPTRA_GEMM_GROUPED": "0"},
+                                    {"ADAPTRA_EPI_IN_LDG": "1"}])
+def test_stage_parity_under_toggle(toggle):
+    env = dict(os.environ, **toggle)
+    cmd = [sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+           os.path.join(ROOT, "tests/test_gpu_stage.py"), os.path.join(ROOT, "tests/test_gpu_fullsize.py")]
+    r = subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    print(r.stdout[-3000:], r.stderr[-3000:])
+    assert r.returncode == 0
+    assert " passed" in r.stdout and "failed" not in r.stdout
