@@ -20,11 +20,13 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../../include/adaptra.h"
 #include "../prof.h"
@@ -88,6 +90,7 @@ struct AttnArgs {
   bf16* dqkv;            // [b*T, 3d] (k and v sections written here)
   float* dq_acc;         // [b*T, d] fp32 accumulator of dQ (zeroed by the caller)
   long long* trace;      // diag 0x200: per-iteration clock64 stamps of CTA 0 ([it][16])
+  long long* cta;        // diag 0x400: per CTA {smid, globaltimer at entry, at exit}
   int diag;              // ADAPTRA_ATTN_DIAG bit mask, timing experiments only (0 = normal): 1 no dQ
                          // reduce, 2 no gradient math, 4 no MMAs, 8 no Q/dO loads, 0x10/0x20/0x40/0x80/0x100 no S/dP/dV/dK/dQ MMA
 };
@@ -98,6 +101,16 @@ constexpr int kAttnThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 softmax
 constexpr int kFwdRing = 5;        // forward K/V tile ring (~2.5 key blocks of TMA lead)
 constexpr float kLog2e = 1.4426950408889634f;
 
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ int smid() {
+  int v;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(v));
+  return v;
+}
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -112,13 +125,22 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
+// Persistent: one CTA per SM walks work items (z, qb) -- heavy (late) query
+// blocks first, dealt to the CTAs in snake order (round r: item r*G + c, then
+// (r+1)*G - 1 - c), so each SM's total key blocks stay close to the mean.  The
+// K/V ring, the S buffers and every barrier phase run on counters global to
+// the CTA, so the next item's Q / K / V loads and its first S MMA overlap this
+// item's last softmax block and epilogue (per-CTA setup and the epilogue were
+// 26 % of the SM time with one CTA per item, diag 0x400).
+__device__ __forceinline__ int fwd_item(int r, int c, int G) { return (r & 1) ? (r + 1) * G - 1 - c : r * G + c; }
+
 __global__ void __launch_bounds__(kAttnThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const AttnArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;  // no static shared memory: the window starts 1024-aligned (checked)
   if (threadIdx.x == 0 && (smem_u32(smem) & 1023)) __trap();
   uint8_t* sQ = smem;                       // 32 KB
-  uint8_t* sRing = sQ + TILE;               // kFwdRing x 32 KB: K_0 V_0 K_1 V_1 ... (tile n in slot n % kFwdRing)
+  uint8_t* sRing = sQ + TILE;               // kFwdRing x 32 KB: K V K V ... (tile n in slot n % kFwdRing)
   uint8_t* sP = sRing + kFwdRing * TILE;    // 32 KB
   float* sMax = (float*)(sP + TILE);        // [2 (block parity)][2 halves][128] half-row maxima
   uint64_t* bar = (uint64_t*)(sMax + 4 * AT);
@@ -130,19 +152,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint64_t* p_full = s_empty + 2;
   uint64_t* p_empty = p_full + 1;
   uint64_t* o_full = p_empty + 1;
-  uint32_t* tmem_slot = (uint32_t*)(o_full + 1);
+  uint64_t* q_empty = o_full + 1;           // the item's last S MMA read Q
+  uint32_t* tmem_slot = (uint32_t*)(q_empty + 1);
 
+  const long long cta_t0 = (a.diag & 0x400) ? gtimer() : 0;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int nqb = a.T / AT, Z = a.b * a.H;
-  const int qb = nqb - 1 - (int)(blockIdx.x / Z);  // heavy (late) query blocks first
-  const int z = blockIdx.x % Z;
-  const int s = z / a.H, h = z % a.H;
-  const int row0 = s * a.T;                       // first row of this sequence in [b*T, .]
-  const int qcol = h * AT, kcol = a.d + h * AT, vcol = 2 * a.d + h * AT;
+  const int nqb = a.T / AT, Z = a.b * a.H, n_items = nqb * Z;
+  const int G = (int)gridDim.x, cta = (int)blockIdx.x;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm_qkv);
     mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
     for (int i = 0; i < kFwdRing; ++i) {
       mbar_init(&t_full[i], 1);
       mbar_init(&t_empty[i], 1);
@@ -165,32 +186,40 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, TILE);
-      for (int c = 0; c < 2; ++c) tma_load_2d(sQ + c * CHUNK, &tm_qkv, q_full, qcol + 64 * c, row0 + qb * AT);
-      for (int n = 0, slot = 0, ph = 0; n < 2 * (qb + 1); ++n) {  // K_j (n = 2j), V_j (n = 2j+1)
-        mbar_wait(&t_empty[slot], ph ^ 1);
-        mbar_arrive_expect_tx(&t_full[slot], TILE);
-        const int col = (n & 1) ? vcol : kcol;
-        for (int c = 0; c < 2; ++c)
-          tma_load_2d(sRing + slot * TILE + c * CHUNK, &tm_qkv, &t_full[slot], col + 64 * c, row0 + (n >> 1) * AT);
-        if (++slot == kFwdRing) {
-          slot = 0;
-          ph ^= 1;
+      int slot = 0, ph = 0;
+      for (int r = 0, it = 0;; ++r, ++it) {
+        const int item = fwd_item(r, cta, G);
+        if (item >= n_items) break;
+        const int qb = nqb - 1 - item / Z, z = item % Z;
+        const int s = z / a.H, h = z % a.H, row0 = s * a.T;
+        const int kcol = a.d + h * AT, vcol = 2 * a.d + h * AT;
+        mbar_wait(q_empty, (it & 1) ^ 1);
+        mbar_arrive_expect_tx(q_full, TILE);
+        for (int c = 0; c < 2; ++c) tma_load_2d(sQ + c * CHUNK, &tm_qkv, q_full, h * AT + 64 * c, row0 + qb * AT);
+        for (int n = 0; n < 2 * (qb + 1); ++n) {  // K_j (n = 2j), V_j (n = 2j+1)
+          mbar_wait(&t_empty[slot], ph ^ 1);
+          mbar_arrive_expect_tx(&t_full[slot], TILE);
+          const int col = (n & 1) ? vcol : kcol;
+          for (int c = 0; c < 2; ++c)
+            tma_load_2d(sRing + slot * TILE + c * CHUNK, &tm_qkv, &t_full[slot], col + 64 * c, row0 + (n >> 1) * AT);
+          if (++slot == kFwdRing) {
+            slot = 0;
+            ph ^= 1;
+          }
         }
       }
     }
   } else if (warp == 1) {
     // S of block j+1 is issued before waiting for P of block j, so the softmax
-    // warps overlap the tensor pipe.  S buffer of block j is j & 1; tile n of
-    // the ring sits in slot n % kFwdRing with barrier phase (n / kFwdRing) & 1.
-    mbar_wait(q_full, 0);
-    tc_fence_after();
+    // warps overlap the tensor pipe; across items, S of the next item's first
+    // block follows this item's last P V.  Global block g: S buffer
+    // g & 1, K tile 2g and V tile 2g+1 of the ring.
     const uint32_t aQ = smem_u32(sQ), aP = smem_u32(sP);
-    auto issue_s = [&](int j) {
-      const int st = j & 1;
-      const int slot = (2 * j) % kFwdRing;
-      mbar_wait(&t_full[slot], ((2 * j) / kFwdRing) & 1);
-      mbar_wait(&s_empty[st], ((j >> 1) & 1) ^ 1);
+    auto issue_s = [&](int g) {
+      const int st = g & 1;
+      const int slot = (2 * g) % kFwdRing;
+      mbar_wait(&t_full[slot], ((2 * g) / kFwdRing) & 1);
+      mbar_wait(&s_empty[st], ((g >> 1) & 1) ^ 1);
       tc_fence_after();
       if (lane == 0) {
         const uint32_t aK = smem_u32(sRing + slot * TILE);
@@ -202,137 +231,183 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       }
       __syncwarp();
     };
-    issue_s(0);
-    for (int j = 0; j <= qb; ++j) {
-      if (j + 1 <= qb) issue_s(j + 1);
-      const int vslot = (2 * j + 1) % kFwdRing;
-      mbar_wait(p_full, j & 1);
-      mbar_wait(&t_full[vslot], ((2 * j + 1) / kFwdRing) & 1);
+    int g0 = 0;  // global index of the item's first block
+    int it = 0;
+    int item = fwd_item(0, cta, G);
+    if (item < n_items) {
+      mbar_wait(q_full, 0);
       tc_fence_after();
-      if (lane == 0) {
-        const uint32_t aV = smem_u32(sRing + vslot * TILE);
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks)
-          tc_mma_f16(tO, desc_kmajor(aP, ks), desc_mnmajor(aV, ks), idesc(0, 1), (j > 0 || ks > 0) ? 1u : 0u);
-        tc_commit(&t_empty[vslot]);
-        tc_commit(p_empty);
-      }
-      __syncwarp();
+      issue_s(0);
     }
-    if (lane == 0) tc_commit(o_full);
-    __syncwarp();
+    while (item < n_items) {
+      const int nb = nqb - item / Z;  // key blocks of this item
+      const int next = fwd_item(it + 1, cta, G);
+      for (int j = 0; j < nb; ++j) {
+        const int g = g0 + j;
+        if (j + 1 < nb) {
+          issue_s(g + 1);
+        } else {
+          if (lane == 0) tc_commit(q_empty);  // after the item's last S: Q may be replaced
+          __syncwarp();
+        }
+        const int vslot = (2 * g + 1) % kFwdRing;
+        mbar_wait(p_full, g & 1);
+        mbar_wait(&t_full[vslot], ((2 * g + 1) / kFwdRing) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t aV = smem_u32(sRing + vslot * TILE);
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks)
+            tc_mma_f16(tO, desc_kmajor(aP, ks), desc_mnmajor(aV, ks), idesc(0, 1), (j > 0 || ks > 0) ? 1u : 0u);
+          tc_commit(&t_empty[vslot]);
+          tc_commit(p_empty);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) tc_commit(o_full);
+      __syncwarp();
+      // the next item's first S: its Q load started when this item's last S
+      // finished, so it lands while the softmax warps run the last block and
+      // the epilogue (waiting here before the last P V would put it on the path)
+      if (next < n_items) {
+        mbar_wait(q_full, (it + 1) & 1);
+        tc_fence_after();
+        issue_s(g0 + nb);
+      }
+      g0 += nb;
+      ++it;
+      item = next;
+    }
   } else {
     // softmax warps: lane quadrant quad (rows), column half (64 keys / head dims).
     // Online softmax in log2 units against a reference max mref shared by the
     // two halves of a row (exchanged through sMax every block).  mref moves
     // only when the running max exceeds it by more than 8, so P <= 2^8 and the
     // O accumulator in TMEM is rescaled rarely (then by this thread's half).
+    // The next item's first P V (which overwrites O) waits for p_full, which
+    // these warps arrive only after reading O in the epilogue.
     const int quad = warp & 3, half = (warp - 2) >> 2;
     const int r = quad * 32 + lane;           // row within the query block
-    const int qi = qb * AT + r;               // query position in the sequence
     const uint32_t lanes = ((uint32_t)(quad * 32) << 16) + half * 64;
     const float c2 = a.scale * kLog2e;        // scores in log2 units
     const int pair_bar = 1 + quad;            // warps quad (half 0) and quad (half 1)
-    float mref = -INFINITY, l = 0.f;
-    for (int j = 0; j <= qb; ++j) {
-      const int sb = j & 1;
-      mbar_wait(&s_full[sb], (j >> 1) & 1);
+    int g = 0;
+    for (int rr = 0, it = 0;; ++rr, ++it) {
+      const int item = fwd_item(rr, cta, G);
+      if (item >= n_items) break;
+      const int qb = nqb - 1 - item / Z, z = item % Z;
+      const int s = z / a.H, h = z % a.H, row0 = s * a.T;
+      const int qi = qb * AT + r;             // query position in the sequence
+      float mref = -INFINITY, l = 0.f;
+      for (int j = 0; j <= qb; ++j, ++g) {
+        const int sb = g & 1;
+        mbar_wait(&s_full[sb], (g >> 1) & 1);
+        tc_fence_after();
+        uint32_t r0[32], r1[32];
+        tmem_ld32(tmem + sb * 128 + lanes, r0);
+        tmem_ld32(tmem + sb * 128 + lanes + 32, r1);
+        tmem_ld_wait_regs(r0);
+        tmem_ld_wait_regs(r1);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[sb]);
+        if (j == qb) {
+          const int lim = qi - (j * AT + half * 64);  // last visible column of this half
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            if (t > lim) r0[t] = __float_as_uint(-INFINITY);
+            if (t + 32 > lim) r1[t] = __float_as_uint(-INFINITY);
+          }
+        }
+        float cm = fmaxf(__uint_as_float(r0[0]), __uint_as_float(r1[0]));
+#pragma unroll
+        for (int t = 1; t < 32; ++t) cm = fmaxf(cm, fmaxf(__uint_as_float(r0[t]), __uint_as_float(r1[t])));
+        float* mx = sMax + sb * 2 * AT;
+        mx[half * AT + r] = cm;
+        named_sync(pair_bar, 64);
+        // every row has key 0 <= qi in block 0 and key j*128 <= qi in block j: mb is finite
+        const float mb = fmaxf(cm, mx[(half ^ 1) * AT + r]) * c2;
+        const bool resc = mb > mref + 8.f;
+        float alpha = 1.f;
+        if (resc) {
+          alpha = ex2(mref - mb);  // 0 on the first block
+          mref = mb;
+        }
+        uint32_t pk[32];  // P row half as bf16x2
+        float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+        for (int t = 0; t < 32; t += 2) {
+          const float e0 = ex2(fmaf(__uint_as_float(r0[t]), c2, -mref));
+          const float e1 = ex2(fmaf(__uint_as_float(r0[t + 1]), c2, -mref));
+          const float e2 = ex2(fmaf(__uint_as_float(r1[t]), c2, -mref));
+          const float e3 = ex2(fmaf(__uint_as_float(r1[t + 1]), c2, -mref));
+          acc0 += e0 + e1;
+          acc1 += e2 + e3;
+          pk[t >> 1] = pack_bf16x2(e0, e1);
+          pk[16 + (t >> 1)] = pack_bf16x2(e2, e3);
+        }
+        l = l * alpha + (acc0 + acc1);
+        mbar_wait(p_empty, (g & 1) ^ 1);  // P V of the previous block done: O stable, P buffer free
+        if (j > 0 && __any_sync(0xffffffffu, resc)) {
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            uint32_t o[32];
+            tmem_ld32(tO + lanes + 32 * c, o);
+            tmem_ld_wait_regs(o);
+#pragma unroll
+            for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * alpha);
+            tmem_st32(tO + lanes + 32 * c, o);
+          }
+          tmem_st_wait();
+        }
+        st_tile_row32_packed(smem_u32(sP), r, half * 64, pk);
+        st_tile_row32_packed(smem_u32(sP), r, half * 64 + 32, pk + 16);
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full);
+      }
+      // ---- epilogue: O / l -> bf16 (this half of the head dims), LSE (log2 units).
+      // The row sums are exchanged through the sMax buffer of the parity the
+      // last block did not use (both halves finished reading it before the last
+      // block's barrier); the second barrier keeps the next item's first block,
+      // which writes that buffer, behind both reads.
+      float* sL = sMax + (g & 1) * 2 * AT;
+      sL[half * AT + r] = l;
+      named_sync(pair_bar, 64);
+      const float ltot = sL[r] + sL[AT + r];
+      named_sync(pair_bar, 64);
+      const float inv = 1.f / ltot;
+      mbar_wait(o_full, it & 1);
       tc_fence_after();
       uint32_t r0[32], r1[32];
-      tmem_ld32(tmem + sb * 128 + lanes, r0);
-      tmem_ld32(tmem + sb * 128 + lanes + 32, r1);
+      tmem_ld32(tO + lanes, r0);
+      tmem_ld32(tO + lanes + 32, r1);
       tmem_ld_wait_regs(r0);
       tmem_ld_wait_regs(r1);
       tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[sb]);
-      if (j == qb) {
-        const int lim = qi - (j * AT + half * 64);  // last visible column of this half
+      bf16* orow = a.o + (size_t)(row0 + qi) * a.d + h * AT + half * 64;
+      float v[64];
 #pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          if (t > lim) r0[t] = __float_as_uint(-INFINITY);
-          if (t + 32 > lim) r1[t] = __float_as_uint(-INFINITY);
-        }
+      for (int t = 0; t < 32; ++t) {
+        v[t] = __uint_as_float(r0[t]) * inv;
+        v[32 + t] = __uint_as_float(r1[t]) * inv;
       }
-      float cm = fmaxf(__uint_as_float(r0[0]), __uint_as_float(r1[0]));
 #pragma unroll
-      for (int t = 1; t < 32; ++t) cm = fmaxf(cm, fmaxf(__uint_as_float(r0[t]), __uint_as_float(r1[t])));
-      float* mx = sMax + sb * 2 * AT;
-      mx[half * AT + r] = cm;
-      named_sync(pair_bar, 64);
-      // every row has key 0 <= qi in block 0 and key j*128 <= qi in block j: mb is finite
-      const float mb = fmaxf(cm, mx[(half ^ 1) * AT + r]) * c2;
-      const bool resc = mb > mref + 8.f;
-      float alpha = 1.f;
-      if (resc) {
-        alpha = ex2(mref - mb);  // 0 on the first block
-        mref = mb;
-      }
-      uint32_t pk[32];  // P row half as bf16x2
-      float acc0 = 0.f, acc1 = 0.f;
-#pragma unroll
-      for (int t = 0; t < 32; t += 2) {
-        const float e0 = ex2(fmaf(__uint_as_float(r0[t]), c2, -mref));
-        const float e1 = ex2(fmaf(__uint_as_float(r0[t + 1]), c2, -mref));
-        const float e2 = ex2(fmaf(__uint_as_float(r1[t]), c2, -mref));
-        const float e3 = ex2(fmaf(__uint_as_float(r1[t + 1]), c2, -mref));
-        acc0 += e0 + e1;
-        acc1 += e2 + e3;
-        pk[t >> 1] = pack_bf16x2(e0, e1);
-        pk[16 + (t >> 1)] = pack_bf16x2(e2, e3);
-      }
-      l = l * alpha + (acc0 + acc1);
-      mbar_wait(p_empty, (j & 1) ^ 1);  // P V of block j-1 done: O stable, P buffer free
-      if (j > 0 && __any_sync(0xffffffffu, resc)) {
-        tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t o[32];
-          tmem_ld32(tO + lanes + 32 * c, o);
-          tmem_ld_wait_regs(o);
-#pragma unroll
-          for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * alpha);
-          tmem_st32(tO + lanes + 32 * c, o);
-        }
-        tmem_st_wait();
-      }
-      st_tile_row32_packed(smem_u32(sP), r, half * 64, pk);
-      st_tile_row32_packed(smem_u32(sP), r, half * 64 + 32, pk + 16);
-      fence_proxy_async_smem();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      for (int t = 0; t < 64; t += 8) st_bf16x8(orow + t, v + t);
+      if (half == 0) a.lse[(size_t)z * a.T + qi] = mref + __log2f(ltot);
     }
-    // ---- epilogue: O / l -> bf16 (this half of the head dims), LSE (log2 units).
-    // The row sums are exchanged through the sMax buffer of parity qb ^ 1,
-    // which both halves finished reading before the last block's barrier.
-    float* sL = sMax + ((qb & 1) ^ 1) * 2 * AT;
-    sL[half * AT + r] = l;
-    named_sync(pair_bar, 64);
-    const float ltot = sL[r] + sL[AT + r];
-    const float inv = 1.f / ltot;
-    mbar_wait(o_full, 0);
-    tc_fence_after();
-    bf16* orow = a.o + (size_t)(row0 + qi) * a.d + h * AT + half * 64;
-    uint32_t r0[32], r1[32];
-    tmem_ld32(tO + lanes, r0);
-    tmem_ld32(tO + lanes + 32, r1);
-    tmem_ld_wait_regs(r0);
-    tmem_ld_wait_regs(r1);
-    float v[64];
-#pragma unroll
-    for (int t = 0; t < 32; ++t) {
-      v[t] = __uint_as_float(r0[t]) * inv;
-      v[32 + t] = __uint_as_float(r1[t]) * inv;
-    }
-#pragma unroll
-    for (int t = 0; t < 64; t += 8) st_bf16x8(orow + t, v + t);
-    if (half == 0) a.lse[(size_t)z * a.T + qi] = mref + __log2f(ltot);
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 1) tmem_dealloc(tmem, 512);
+  if ((a.diag & 0x400) && threadIdx.x == 0) {
+    a.cta[3 * blockIdx.x] = smid();
+    a.cta[3 * blockIdx.x + 1] = cta_t0;
+    a.cta[3 * blockIdx.x + 2] = gtimer();
+  }
 }
 
 // ============================================================== backward
@@ -397,6 +472,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int nb = a.T / AT, Z = a.b * a.H;
+  const long long cta_t0 = (a.diag & 0x400) ? gtimer() : 0;
   const int kb = (int)(blockIdx.x / Z);  // heavy (early) key blocks first
   const int z = blockIdx.x % Z;
   const int s = z / a.H, h = z % a.H;
@@ -698,6 +774,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 1) tmem_dealloc(tmem, 512);
+  if ((a.diag & 0x400) && threadIdx.x == 0) {
+    a.cta[3 * blockIdx.x] = smid();
+    a.cta[3 * blockIdx.x + 1] = cta_t0;
+    a.cta[3 * blockIdx.x + 2] = gtimer();
+  }
 #undef TRACE
 }
 
@@ -776,6 +857,50 @@ static_assert(kFwdSmem <= 232448, "attn fwd shared memory");
 constexpr int kBwdSmem = 2 * TILE + (2 * NQS + 2) * QTILE + 4 * 4096 + 2 * NQS * QB * 4 + 256;
 static_assert(kBwdSmem <= 232448, "attn bwd shared memory");
 
+// diag 0x400: per-CTA occupancy summary of one launch (third call of each kernel)
+static void cta_summary(const char* name, long long* dev, int n, int blocks_of(int), cudaStream_t st) {
+  static int calls[2] = {0, 0};
+  const int k = name[5] == 'f' ? 0 : 1;
+  if (calls[k]++ != 2) return;
+  std::vector<long long> h(3 * (size_t)n);
+  cudaStreamSynchronize(st);
+  cudaMemcpy(h.data(), dev, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+  long long t0 = h[1], t1 = h[2], busy = 0;
+  for (int i = 0; i < n; ++i) {
+    t0 = std::min(t0, h[3 * i + 1]);
+    t1 = std::max(t1, h[3 * i + 2]);
+    busy += h[3 * i + 2] - h[3 * i + 1];
+  }
+  fprintf(stderr, "%s ctas %d span %.2f us  sum cta %.2f us  occupancy(148 SM) %.3f\n", name, n, (t1 - t0) / 1e3,
+          busy / 1e3, busy / (148.0 * (t1 - t0)));
+  // per work size: mean duration, mean start
+  std::vector<double> dsum(64, 0), ssum(64, 0), esum(64, 0);
+  std::vector<int> cnt(64, 0);
+  for (int i = 0; i < n; ++i) {
+    int w = blocks_of(i);
+    if (w < 0 || w >= 64) continue;
+    dsum[w] += h[3 * i + 2] - h[3 * i + 1];
+    ssum[w] += h[3 * i + 1] - t0;
+    esum[w] += h[3 * i + 2] - t0;
+    cnt[w]++;
+  }
+  for (int w = 0; w < 64; ++w)
+    if (cnt[w])
+      fprintf(stderr, "  blocks %2d: n %3d  dur %7.2f us  start %7.2f  end %7.2f\n", w, cnt[w], dsum[w] / cnt[w] / 1e3,
+              ssum[w] / cnt[w] / 1e3, esum[w] / cnt[w] / 1e3);
+}
+static int g_nqb = 16, g_Z = 16, g_G = 148;
+static int fwd_blocks(int c) {  // total key blocks of persistent CTA c (snake deal, as fwd_item)
+  int tot = 0;
+  for (int r = 0;; ++r) {
+    const int i = (r & 1) ? (r + 1) * g_G - 1 - c : r * g_G + c;
+    if (i >= g_nqb * g_Z) break;
+    tot += g_nqb - i / g_Z;
+  }
+  return tot;
+}
+static int bwd_blocks(int i) { return g_nqb - (i / g_Z); }
+
 int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d, cudaStream_t st) {
   if (d != H * AT || T % AT) return set_error(ADAPTRA_EINVAL, "attn_fwd_tc: head dim 128 and T % 128 required");
   CUtensorMap m;
@@ -794,7 +919,21 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
   a.o = o;
   a.lse = lse;
   void* pb = prof_on() ? prof_begin(st) : nullptr;
-  attn_fwd_kernel<<<b * H * (T / AT), kAttnThreads, kFwdSmem, st>>>(m, a);
+  static const int fdiag = getenv("ADAPTRA_ATTN_DIAG") ? atoi(getenv("ADAPTRA_ATTN_DIAG")) : 0;
+  a.diag = fdiag & 0x400;
+  static long long* fcta = nullptr;
+  if ((fdiag & 0x400) && !fcta) cudaMalloc(&fcta, 3 * 4096 * sizeof(long long));
+  a.cta = fcta;
+  static int n_sm[32] = {0};
+  if (!n_sm[dev & 31]) cudaDeviceGetAttribute(&n_sm[dev & 31], cudaDevAttrMultiProcessorCount, dev);
+  // ADAPTRA_ATTN_FWD_GRID=items: one CTA per item (the non-persistent launch, for comparison)
+  static const bool per_item = getenv("ADAPTRA_ATTN_FWD_GRID") && !strcmp(getenv("ADAPTRA_ATTN_FWD_GRID"), "items");
+  const int items = b * H * (T / AT), grid = per_item ? items : std::min(items, n_sm[dev & 31]);
+  attn_fwd_kernel<<<grid, kAttnThreads, kFwdSmem, st>>>(m, a);
+  if (fdiag & 0x400) {
+    g_nqb = T / AT; g_Z = b * H; g_G = grid;
+    cta_summary("attn_fwd", fcta, grid, fwd_blocks, st);
+  }
   if (pb) {
     double fl = 4.0 * (double)T * T * AT * b * H * 0.5;  // algorithmic: QK^T + PV, causal half (R28)
     prof_end(pb, st, PROF_ATTN, fl, 0);
@@ -831,7 +970,14 @@ int attn_bwd_tc(const bf16* qkv, const bf16* dO, const float* lse, const float* 
   static long long* trace = nullptr;
   if ((diag & 0x200) && !trace) cudaMalloc(&trace, 64 * 16 * sizeof(long long));
   a.trace = trace;
+  static long long* bcta = nullptr;
+  if ((diag & 0x400) && !bcta) cudaMalloc(&bcta, 3 * 4096 * sizeof(long long));
+  a.cta = bcta;
   attn_bwd_kernel<<<b * H * (T / AT), kBwdThreads, kBwdSmem, st>>>(mkv, mq, mdo, mdq, a);
+  if (diag & 0x400) {
+    g_nqb = T / AT; g_Z = b * H;
+    cta_summary("attn_bwd", bcta, b * H * (T / AT), bwd_blocks, st);
+  }
   if (diag & 0x200) {
     static int dumped = 0;
     long long h[64 * 16];

@@ -29,6 +29,9 @@ CASES = [
     ("gpt", L.F32, 1, 256, 512, 2, 2, 128, 2),
     ("gpt", L.BF16, 2, 256, 1024, 2, 1, 256, 2),
     ("gpt", L.BF16, 1, 256, 512, 2, 2, 128, 2),
+    # 3 sequences x 4 heads x 16 query blocks = 192 attention items on the
+    # persistent forward grid (148 CTAs): CTAs with one and with two items
+    ("gpt", L.BF16, 1, 512, 1024, 4, 3, 2048, 1),
 ]
 
 
