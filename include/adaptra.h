@@ -245,7 +245,9 @@ int adaptra_stage_destroy(adaptra_stage_t s);
  *  x_in   [b*T, d] dtype, must stay valid until W of this slot (mailbox slot).
  *  y_out  [b*T, d] dtype, written by the last GEMM epilogue (may be a peer
  *         mailbox mapped over NVLink); ignored on the last stage.
- *  target [b*T, d] fp32 (last stage only); loss_acc: fp32 scalar, += L_j / N. */
+ *  target [b*T, d] fp32 (last stage only); loss_acc: fp32 scalar, += L_j / N
+ *         (block partials summed in a fixed order: the loss is reproducible
+ *         bit for bit, independent of scheduling and transport). */
 int adaptra_stage_F(adaptra_stage_t s, int32_t slot, const void* x_in, void* y_out, const float* target,
                     float* loss_acc, void* stream);
 /* B: input gradient only.  dy_in [b*T,d] dtype (NULL on the last

@@ -360,7 +360,7 @@ __global__ void attn_rowdot_kernel(const T* __restrict__ dO, const T* __restrict
 // L_j = (1/(R d)) sum 1/2 (y - tgt)^2, loss_acc += L_j / N;  dy = (y - tgt)/(N R d).
 template <typename T>
 __global__ void mse_kernel(const T* __restrict__ y, const float* __restrict__ tgt, T* __restrict__ dy,
-                           float* __restrict__ loss_acc, long n, float inv_n_total, float inv_loss) {
+                           float* __restrict__ part, long n, float inv_n_total, float inv_loss) {
   __shared__ float red[32];
   float acc = 0.f;
   for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long)gridDim.x * blockDim.x) {
@@ -374,7 +374,21 @@ __global__ void mse_kernel(const T* __restrict__ y, const float* __restrict__ tg
   if (threadIdx.x < 32) {
     float v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
     v = warp_sum(v);
-    if (threadIdx.x == 0) atomicAdd(loss_acc, v * inv_loss);
+    if (threadIdx.x == 0) part[blockIdx.x] = v * inv_loss;
+  }
+}
+// fixed-order sum of the per-block partials (one block of 256 threads)
+__global__ void mse_sum_kernel(const float* __restrict__ part, int n, float* __restrict__ loss_acc) {
+  __shared__ float red[8];
+  float acc = 0.f;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += part[i];
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float v = 0.f;
+    for (int w = 0; w < (int)blockDim.x / 32; ++w) v += red[w];
+    *loss_acc += v;
   }
 }
 
@@ -456,11 +470,12 @@ int attn_rowdot(const T* dO, const T* O, float* D, int b, int H, int Tn, int dh,
   return launch_check("attn_rowdot");
 }
 template <typename T>
-int mse_loss(const T* y, const float* tgt, T* dy, float* loss_acc, long n, int n_mb, cudaStream_t st) {
+int mse_loss(const T* y, const float* tgt, T* dy, float* loss_acc, float* part, long n, int n_mb, cudaStream_t st) {
   float inv_total = 1.f / ((float)n_mb * (float)n);
   float inv_loss = 1.f / ((float)n * (float)n_mb);
-  int blocks = (int)std::min<long>(1184, (n + 255) / 256);
-  mse_kernel<T><<<blocks, 256, 0, st>>>(y, tgt, dy, loss_acc, n, inv_total, inv_loss);
+  int blocks = (int)std::min<long>(kMseMaxBlocks, (n + 255) / 256);
+  mse_kernel<T><<<blocks, 256, 0, st>>>(y, tgt, dy, part, n, inv_total, inv_loss);
+  mse_sum_kernel<<<1, 256, 0, st>>>(part, blocks, loss_acc);
   return launch_check("mse_loss");
 }
 int copy_async(void* dst, const void* src, long bytes, cudaStream_t st) {
@@ -562,7 +577,7 @@ int colsum_grouped(const ColsumJob* jobs, int n, int R, cudaStream_t st) {
   template int softmax_causal<T>(const float*, T*, int, int, cudaStream_t);                                       \
   template int attn_rowdot<T>(const T*, const T*, float*, int, int, int, int, int, cudaStream_t);                 \
   template int colsum_grouped<T>(const ColsumJob*, int, int, cudaStream_t);                                       \
-  template int mse_loss<T>(const T*, const float*, T*, float*, long, int, cudaStream_t);
+  template int mse_loss<T>(const T*, const float*, T*, float*, float*, long, int, cudaStream_t);
 INST(float)
 INST(bf16)
 

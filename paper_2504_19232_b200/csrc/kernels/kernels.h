@@ -48,8 +48,11 @@ template <typename T>
 int softmax_causal(const float* S, T* P, int Z, int Tn, cudaStream_t st);
 template <typename T>
 int attn_rowdot(const T* dO, const T* O, float* D, int b, int H, int Tn, int dh, int ld, cudaStream_t st);
+// MSE loss + dy seed; per-block partial sums go to part[kMseMaxBlocks] and a
+// one-block kernel adds them to *loss_acc in a fixed order (reproducible loss).
+constexpr int kMseMaxBlocks = 1184;
 template <typename T>
-int mse_loss(const T* y, const float* tgt, T* dy, float* loss_acc, long n, int n_mb, cudaStream_t st);
+int mse_loss(const T* y, const float* tgt, T* dy, float* loss_acc, float* part, long n, int n_mb, cudaStream_t st);
 int copy_async(void* dst, const void* src, long bytes, cudaStream_t st);
 // fused causal attention (bf16, head dim 128): attn_tc.cu
 int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d, cudaStream_t st);

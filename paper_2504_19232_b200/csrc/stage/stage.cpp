@@ -68,7 +68,7 @@ struct SlotLayout {
   // per layer (MLP): xl a g da dyl
   long xl, h1, qkv, P, o, y1, h2, a, g, dqkv, dy1, da, dyl, dh2, dh1, mean1, rstd1, mean2, rstd2;
   long layer_bytes, fb_layer_bytes, fb_slot_bytes;
-  long yL, seed;  // stage-level (after the per-layer block)
+  long yL, seed, lpart;  // stage-level (after the per-layer block); lpart: loss partials + ticket
   long slot_bytes;
   // work area
   long w_S, w_dS, w_do, w_D, w_dq, work_bytes;
@@ -162,7 +162,8 @@ static int compute_layout(const adaptra_stage_desc_t& d, SlotLayout& L) {
   long tail = L.layer_bytes * d.n_layers;
   L.yL = tail;
   L.seed = align256(L.yL + R * D * e);
-  L.slot_bytes = d.is_last ? align256(L.seed + R * D * e) : tail;
+  L.lpart = align256(L.seed + R * D * e);
+  L.slot_bytes = d.is_last ? align256(L.lpart + (kMseMaxBlocks + 1) * 4) : tail;
   L.fb_slot_bytes = L.fb_layer_bytes * d.n_layers;
   long w = 0;
   if (d.block == ADAPTRA_BLOCK_GPT) {
@@ -315,7 +316,8 @@ struct StageOps {
       if (!target || !loss_acc) return set_error(ADAPTRA_EINVAL, "stage_F: last stage needs target and loss_acc");
       const T* y = (const T*)(slot_base(slot) + s->L.yL);
       T* seed = (T*)(slot_base(slot) + s->L.seed);
-      TRY(mse_loss<T>(y, target, seed, loss_acc, s->R * D.d, D.n_microbatches, st));
+      TRY(mse_loss<T>(y, target, seed, loss_acc, (float*)(slot_base(slot) + s->L.lpart), s->R * D.d,
+                      D.n_microbatches, st));
       s->dy_in[slot] = seed;
     }
     return ADAPTRA_OK;
