@@ -193,10 +193,19 @@ def main():
     from paper_2504_19232_b200.pipeline import Arm, ModelCfg, Pipeline
     import synthetic as sy
 
+    # ADAPTRA_OVERSUBSCRIBE=1 (testing only): more ranks than GPUs, rank r on
+    # GPU r % n (e.g. the 8-rank path on a 4-GPU box); NCCL refuses two ranks
+    # on one GPU, and every collective here is on the gloo group anyway
+    oversub = os.environ.get("ADAPTRA_OVERSUBSCRIBE") == "1"
+    if oversub:
+        local_rank = local_rank % torch.cuda.device_count()
     torch.cuda.set_device(local_rank)
     group = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        if oversub:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
         group = dist.new_group(backend="gloo")
     # The metric is quoted at 8 stages (configs C2/C3, N = 32).  That fits from
     # 2 GPUs up (8 stages x 32 weight-gradient stash slots of a C1 stage is
