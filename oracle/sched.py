@@ -16,6 +16,13 @@ ZB figure, the 1F1B closed form T=(N+S-1)(tF+tB+tW) and bubble (S-1)/(N+S-1),
 the ZB closed form (S-1)tF+N(tF+tB+tW), the Lemma x_i >= x_{i+1},
 hand traces of Alg. 1/2, Eq. 1 boundaries, Theorem 1 regimes, dependency
 validity of every emitted schedule, and brute-force optimality on tiny cases.
+The checkers are pinned negatively: a mutated copy of the ideal schedule is
+flagged with each violation class (dup, missing, duration, overlap, dep of
+F / B / W, badop), and non-monotone / out-of-range plans are rejected; the
+R26 clamp and the R18 policy are pinned by hand traces; P2's interior and
+utilisation bubbles (0.0886 / 0.182) from the printed 440 ms; P11 against an
+exact branch-and-bound optimum at the paper's smallest setting (S=3, N=6),
+itself cross-checked against exhaustive search on S=2.
 """
 from __future__ import annotations
 
@@ -110,17 +117,25 @@ def slackness(x) -> list[int]:
     return [x[i] - x[i + 1] for i in range(len(x) - 1)]
 
 
-def validate_plan(N: int, x) -> list[str]:
-    """Lemma: x non-increasing; plus x_{S-1} >= 1 and x_0 <= N."""
+def plan_violations(N: int, x) -> list[tuple]:
+    """Lemma: x non-increasing; plus x_{S-1} >= 1 (Alg. 1/2 set
+    the last stage's count to 1) and x_0 <= N (R11: there
+    are only N forwards).  Returns (code, index) tuples; codes "nonmono" (at
+    link i), "x_last", "x0_gt_N"."""
     v = []
     for i in range(len(x) - 1):
         if x[i] < x[i + 1]:
-            v.append(f"non-monotone at {i}")
+            v.append(("nonmono", i))
     if x[-1] < 1:
-        v.append("x_{S-1} < 1")
+        v.append(("x_last", len(x) - 1))
     if x[0] > N:
-        v.append("x_0 > N")
+        v.append(("x0_gt_N", 0))
     return v
+
+
+def validate_plan(N: int, x) -> list[str]:
+    """plan_violations as readable strings ([] = valid plan)."""
+    return [f"{code} at {i}" for code, i in plan_violations(N, x)]
 
 
 # ---------------------------------------------------------------------------
@@ -310,9 +325,23 @@ def order_of(X):
 # Validation and metrics
 # ---------------------------------------------------------------------------
 
-def validate(S, N, tF, tB, tW, c, X, merge_w=False) -> list[str]:
-    """Check a timed schedule: completeness, no overlap, exact durations,
-    dependency rules (R1, R2, R8)."""
+def violations(S, N, tF, tB, tW, c, X, merge_w=False) -> list[tuple]:
+    """Check a timed schedule against the problem's constraints and return
+    every violation as (code, stage, kind, mb):
+
+      "badop"    kind not F/B/W, mb outside 1..N, or a W op in a merged
+                 (1F1B) schedule, which has none (R10);
+      "dup"      the op appears twice on its stage;
+      "missing"  an op of the stage's 3N (2N merged) is absent;
+      "duration" end - start != the stage's op time (B + W merged, R10);
+      "overlap"  the op starts before the previous op on its stage ended
+                 (one op at a time per stage, P:2754 busy());
+      "dep"      the op starts before a dependency's end + link latency:
+                 F after the upstream F + c (R1); B after the
+                 downstream B + c, or after its own F on the last stage
+                 (R2); W after its own B and the B that makes
+                 it available (R8).
+    A valid schedule returns []."""
     v = []
     kinds = (F, B) if merge_w else (F, B, W)
     end = {}
@@ -320,21 +349,24 @@ def validate(S, N, tF, tB, tW, c, X, merge_w=False) -> list[str]:
         seen = set()
         prev_end = None
         for op in X[i]:
+            if op.kind not in kinds or not 1 <= op.mb <= N:
+                v.append(("badop", i, op.kind, op.mb))
+                continue
             key = (op.kind, op.mb)
             if key in seen:
-                v.append(f"dup {key} on stage {i}")
+                v.append(("dup", i, op.kind, op.mb))
             seen.add(key)
             want = {F: tF[i], B: tB[i] + (tW[i] if merge_w else 0), W: tW[i]}[op.kind]
             if op.end - op.start != want:
-                v.append(f"duration {key} stage {i}")
+                v.append(("duration", i, op.kind, op.mb))
             if prev_end is not None and op.start < prev_end:
-                v.append(f"overlap at {key} stage {i}")
+                v.append(("overlap", i, op.kind, op.mb))
             prev_end = op.end
             end[(i, op.kind, op.mb)] = (op.start, op.end)
         for k in kinds:
             for j in range(1, N + 1):
                 if (k, j) not in seen:
-                    v.append(f"missing {k}{j} on stage {i}")
+                    v.append(("missing", i, k, j))
     for (i, k, j), (s, _e) in end.items():
         for (dep, link) in _deps(S, i, k, j):
             if merge_w and dep[1] == W:
@@ -343,8 +375,13 @@ def validate(S, N, tF, tB, tW, c, X, merge_w=False) -> list[str]:
                 continue
             need = end[dep][1] + (c[link] if link is not None else 0)
             if s < need:
-                v.append(f"dep violated: {k}{j}@{i} starts {s} < {need}")
+                v.append(("dep", i, k, j))
     return v
+
+
+def validate(S, N, tF, tB, tW, c, X, merge_w=False) -> list[str]:
+    """violations() as readable strings ([] = valid schedule)."""
+    return [f"{code} {k}{j} on stage {i}" for code, i, k, j in violations(S, N, tF, tB, tW, c, X, merge_w)]
 
 
 def metrics(S, X, T=None) -> dict:
@@ -491,4 +528,133 @@ def brute_force_optimum(S, N, tF, tB, tW, c):
             orders[i].pop()
 
     rec([[] for _ in range(S)], [list(o) for o in ops_all])
+    return best[0]
+
+
+def exact_optimum(S, N, tF, tB, tW, c, ub=None):
+    """Minimum makespan over ALL feasible schedules (no restriction on the
+    per-stage orders), by branch and bound over active schedules.
+
+    Each stage is a machine that runs one op at a time; an op may start once
+    every dependency of `_deps` has ended plus its link latency (P:1743-1753,
+    R1, R8).  Some optimal schedule is active (no op can start earlier without
+    delaying another), and Giffler-Thompson generation enumerates every active
+    schedule: take the schedulable op o* with the earliest possible
+    completion e*, on stage m*; branch on every schedulable op of m* that can
+    start before e*.  Pruning: a stage cannot finish before its free time
+    plus its remaining work, and (one-machine relaxation) not before the
+    earliest head of its unscheduled ops + their work + the shortest tail
+    (longest dependency chain that must follow an op).  Symmetry:
+    microbatches are identical, so among candidates of the same stage and
+    kind whose microbatches have identical histories only one is tried.
+    Tiny inputs only (S <= 4, N <= 8)."""
+    kinds = (F, B, W)
+    dur = {(i, F): tF[i] for i in range(S)}
+    dur.update({(i, B): tB[i] for i in range(S)})
+    dur.update({(i, W): tW[i] for i in range(S)})
+    # topological order of one microbatch's ops: F down the stages, B back up, W
+    topo = [(i, F) for i in range(S)] + [(i, B) for i in range(S - 1, -1, -1)] + [(i, W) for i in range(S)]
+    allops = [(i, k, j) for j in range(1, N + 1) for (i, k) in topo]
+    deps = {op: _deps(S, *op) for op in allops}
+    succ = {op: [] for op in allops}
+    for op in allops:
+        for dep, link in deps[op]:
+            succ[dep].append((op, c[link] if link is not None else 0))
+    tail = {}
+    for op in reversed(allops):
+        tail[op] = max((lag + dur[(s[0], s[1])] + tail[s] for s, lag in succ[op]), default=0)
+    end = {}
+    free = [0] * S
+    rem = [N * (tF[i] + tB[i] + tW[i]) for i in range(S)]
+    best = [INF if ub is None else ub + 1]
+
+    def history(j):
+        return tuple(end.get((i, k, j), -1) for i in range(S) for k in kinds)
+
+    def jackson(jobs):
+        """Preemptive one-machine bound: jobs (release, duration, tail); run
+        the released job with the largest tail, preempting on arrivals;
+        returns max(completion + tail) (a lower bound on that machine)."""
+        jobs = sorted(jobs)
+        t, k, lb = 0, 0, 0
+        ready = []                      # [-tail, remaining]
+        while k < len(jobs) or ready:
+            if not ready and t < jobs[k][0]:
+                t = jobs[k][0]
+            while k < len(jobs) and jobs[k][0] <= t:
+                ready.append([-jobs[k][2], jobs[k][1]])
+                k += 1
+            ready.sort()
+            nxt = jobs[k][0] if k < len(jobs) else INF
+            run = min(ready[0][1], nxt - t)
+            t += run
+            ready[0][1] -= run
+            if ready[0][1] == 0:
+                lb = max(lb, t - ready[0][0])
+                ready.pop(0)
+        return lb
+
+    def lower_bound():
+        head = {}
+        jobs = [[] for _ in range(S)]
+        for op in allops:
+            if op in end:
+                continue
+            h = free[op[0]]
+            for dep, link in deps[op]:
+                fin = end[dep] if dep in end else head[dep] + dur[(dep[0], dep[1])]
+                h = max(h, fin + (c[link] if link is not None else 0))
+            head[op] = h
+            jobs[op[0]].append((h, dur[(op[0], op[1])], tail[op]))
+        return max(max(free), max(jackson(js) for js in jobs))
+
+    seen_states = set()
+
+    def rec(n_left):
+        if n_left == 0:
+            best[0] = min(best[0], max(free))
+            return
+        if lower_bound() >= best[0]:
+            return
+        # the same partial schedule up to a relabelling of the (identical)
+        # microbatches, reached by another branch order
+        key = (tuple(free), tuple(sorted(history(j) for j in range(1, N + 1))))
+        if key in seen_states:
+            return
+        seen_states.add(key)
+        cand = []
+        for op in allops:
+            if op in end:
+                continue
+            r = 0
+            ok = True
+            for dep, link in deps[op]:
+                if dep not in end:
+                    ok = False
+                    break
+                r = max(r, end[dep] + (c[link] if link is not None else 0))
+            if ok:
+                es = max(r, free[op[0]])
+                cand.append((es + dur[(op[0], op[1])], es, op))
+        e_star, _, o_star = min(cand)
+        m = o_star[0]
+        seen = set()
+        for e, es, op in sorted(cand):
+            if op[0] != m or es >= e_star:
+                continue
+            sig = (op[1], es, history(op[2]))
+            if sig in seen:
+                continue
+            seen.add(sig)
+            i, k, _ = op
+            old = free[i]
+            end[op] = e
+            free[i] = e
+            rem[i] -= dur[(i, k)]
+            rec(n_left - 1)
+            rem[i] += dur[(i, k)]
+            free[i] = old
+            del end[op]
+
+    rec(len(allops))
     return best[0]

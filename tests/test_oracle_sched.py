@@ -52,6 +52,14 @@ def test_p2_delayed_zb(key):
     if "stage0_B1_start_ms" in g:
         b1 = [op for op in X[0] if op.kind == "B" and op.mb == 1][0]
         assert b1.start == g["stage0_B1_start_ms"]
+        # S_0 now finishes last; internal idle per stage
+        # 80/40/20/0 ms (every stage busy 36 x 10 ms over its span)
+        m = sc.metrics(4, X, T)
+        span = [ops[-1].end - ops[0].start for ops in X]
+        assert X[0][-1].end == T
+        assert [sp - b for sp, b in zip(span, m["busy"])] == g["stage_internal_idle_ms"]
+        assert abs(m["interior_bubble"] - 140 / 1580) < 1e-12 and round(m["interior_bubble"], 4) == 0.0886
+        assert abs(m["util_bubble"] - (1 - 1440 / 1760)) < 1e-12 and round(m["util_bubble"], 3) == 0.182
 
 
 def test_p6_alg1_alg2_hand_traces():
@@ -146,6 +154,156 @@ def test_p10_adaptive_reaches_lower_bound_under_trace_events():
         _, Tz = sc.replay(S, N, t, t, t, c, sc.order_of(Xz))
         _, T1 = sc.replay(S, N, t, t, t, c, sc.order_of(X1), merge_w=True)
         assert T < Tz and T < T1
+
+
+def _ideal():
+    X, T, _ = sc.schedule(4, 12, T10, T10, T10, [0, 0, 0], [7, 5, 3, 1], 1)
+    return X
+
+
+def _codes(v):
+    return {code for code, *_ in v}
+
+
+def _shift(op, d):
+    return sc.Op(op.kind, op.mb, op.start + d, op.end + d)
+
+
+@pytest.mark.parametrize("case", ["dup", "missing", "duration", "overlap", "dep_F_c", "dep_B_c",
+                                  "dep_B_last", "W_before_B", "badop", "W_in_1f1b"])
+def test_validate_flags_each_violation_class(case):
+    """Dependency validity of every emitted schedule (north_star) rests on
+    validate(): a mutated copy of the ideal ZB schedule (P1, valid) must be
+    flagged with the mutated op's violation class."""
+    X = [list(ops) for ops in _ideal()]
+    c = [0, 0, 0]
+    merge = False
+    if case == "dup":                     # F5 of stage 1 appears twice
+        op = X[1][4]
+        X[1].append(_shift(op, 1000))
+        want = ("dup", 1, "F", 5)
+    elif case == "missing":               # last W of stage 3 dropped
+        X[3].pop()
+        want = ("missing", 3, "W", 12)
+    elif case == "duration":              # the last op of stage 2 runs 1 ms long
+        X[2][-1] = sc.Op(X[2][-1].kind, X[2][-1].mb, X[2][-1].start, X[2][-1].end + 1)
+        want = ("duration", 2, X[2][-1].kind, X[2][-1].mb)
+    elif case == "overlap":               # stage 0's 2nd op starts 1 ms early
+        X[0][1] = _shift(X[0][1], -1)
+        want = ("overlap", 0, "F", 2)
+    elif case == "dep_F_c":               # same times, but link 0 now has c = 1 ms
+        c = [1, 0, 0]
+        want = ("dep", 1, "F", 1)         # F1 on stage 1 starts when F1 on stage 0 ends
+    elif case == "dep_B_c":
+        c = [0, 0, 1]
+        want = ("dep", 2, "B", 1)         # B1 on stage 2 starts when B1 on stage 3 ends
+    elif case == "dep_B_last":            # last stage: B1 moved before its own F1 ends
+        k = [q for q, op in enumerate(X[3]) if (op.kind, op.mb) == ("B", 1)][0]
+        X[3][k] = sc.Op("B", 1, X[3][0].start + 5, X[3][0].start + 15)
+        want = ("dep", 3, "B", 1)
+    elif case == "W_before_B":            # S=2, N=1: stage 1 runs W1 before its own B1
+        t = [10, 10]
+        X = [[sc.Op("F", 1, 0, 10), sc.Op("B", 1, 40, 50), sc.Op("W", 1, 50, 60)],
+             [sc.Op("F", 1, 10, 20), sc.Op("W", 1, 20, 30), sc.Op("B", 1, 30, 40)]]
+        v = sc.violations(2, 1, t, t, t, [0], X)
+        assert ("dep", 1, "W", 1) in v and _codes(v) == {"dep"}
+        assert sc.validate(2, 1, t, t, t, [0], X)
+        return
+    elif case == "badop":
+        X[1].append(sc.Op("F", 13, 2000, 2010))   # microbatch 13 of N = 12
+        want = ("badop", 1, "F", 13)
+    else:                                 # a W op inside a merged 1F1B schedule (R10)
+        t = [10] * 4
+        X1, _, _ = sc.schedule_1f1b(4, 4, t, t, t, 1)
+        assert sc.violations(4, 4, t, t, t, [0] * 3, X1, merge_w=True) == []
+        X1[2].append(sc.Op("W", 1, 10_000, 10_010))
+        v = sc.violations(4, 4, t, t, t, [0] * 3, X1, merge_w=True)
+        assert ("badop", 2, "W", 1) in v
+        return
+    v = sc.violations(4, 12, T10, T10, T10, c, X, merge_w=merge)
+    assert want in v, v
+    assert sc.validate(4, 12, T10, T10, T10, c, X, merge_w=merge)
+
+
+def test_validate_plan_flags_each_violation_class():
+    """The Lemma and the plan's bounds: x_{S-1} = 1 (Alg. 1/2)
+    and x_0 <= N (R11)."""
+    assert sc.plan_violations(12, [7, 5, 3, 1]) == []
+    assert sc.plan_violations(12, [3, 4, 1]) == [("nonmono", 0)]
+    assert sc.plan_violations(12, [5, 3, 3, 4]) == [("nonmono", 2)]
+    assert sc.plan_violations(4, [5, 3, 1]) == [("x0_gt_N", 0)]
+    assert sc.plan_violations(12, [3, 2, 0]) == [("x_last", 2)]
+    assert sc.validate_plan(4, [2, 3, 0]) and sc.validate_plan(12, [7, 5, 3, 1]) == []
+    with pytest.raises(sc.PlanError):
+        sc.schedule(3, 4, [10] * 3, [10] * 3, [10] * 3, [0, 0], [3, 4, 1], 1)
+
+
+def test_clamp_plan_hand_traces():
+    """R26 by hand: x_i <- min(x_i, cap_i), then the Lemma restored from the
+    last stage upwards, x_i <- max(x_i, x_{i+1})."""
+    assert sc.clamp_plan([9, 7, 5, 1], [20] * 4) == [9, 7, 5, 1]        # cap inactive
+    assert sc.clamp_plan([9, 7, 5, 1], [6] * 4) == [6, 6, 5, 1]         # clipped, still monotone
+    # a low cap on stage 0 below stage 1's count: the Lemma wins (x_0 = x_1)
+    assert sc.clamp_plan([8, 6, 4, 1], [3, 5, 5, 5]) == [5, 5, 4, 1]
+    assert sc.clamp_plan([12, 8, 4, 1], [10, 3, 9, 9]) == [10, 4, 4, 1]
+
+
+def test_adaptive_orders_hand_traces():
+    """R18 by hand on S=4, N=12, t=10 (x_init = [7,5,3,1] = Alg. 1 = Alg. 2 at
+    c=0): (1) Eq. 1 holds under c_0 = 10 (its boundary, P7) -> the plan is
+    kept; (2) c_0 = 20 breaks it -> Alg. 2 gives [8,5,3,1] (P6); (3) c_2 = 100
+    -> Alg. 2 clips Delta_2 at N-2S = 4 -> [9,7,5,1], and with an x_cap of 6
+    the R26 clamp gives [6,6,5,1]; (4) all links nominal again -> the init
+    plan; each iteration's order is Schedule() of that plan under that c."""
+    x0 = [7, 5, 3, 1]
+    cs_seq = [[0, 0, 0], [10, 0, 0], [20, 0, 0], [0, 0, 100], [0, 0, 0]]
+    out = sc.adaptive_orders(4, 12, T10, T10, T10, cs_seq, x0)
+    assert [x for x, _ in out] == [x0, x0, [8, 5, 3, 1], [9, 7, 5, 1], x0]
+    capped = sc.adaptive_orders(4, 12, T10, T10, T10, cs_seq, x0, x_cap=[6] * 4)
+    # the clamp applies to every Alg. 2 re-plan ([8,5,3,1] -> [6,5,3,1]), not to
+    # a plan Eq. 1 keeps or to the init plan
+    assert [x for x, _ in capped] == [x0, x0, [6, 5, 3, 1], [6, 6, 5, 1], x0]
+    for (x, order), c in zip(out, cs_seq):
+        X, _, _ = sc.schedule(4, 12, T10, T10, T10, c, x, 1)   # delta = max(1, 10 // 30) = 1
+        assert order == sc.order_of(X)
+    # (1): Eq. 1 holds at the boundary, so iteration 2 reuses iteration 1's plan
+    assert sc.eq1_holds(T10, T10, [10, 0, 0], x0) == [True] * 3
+    assert sc.eq1_holds(T10, T10, [20, 0, 0], x0) == [False, True, True]
+
+
+def test_exact_optimum_agrees_with_restricted_brute_force():
+    """Two independent exact methods on S = 2: branch and bound over active
+    schedules (no order restriction) and exhaustive per-stage orders with
+    forwards in microbatch order; both equal the (S-1)t + 3Nt bound where it
+    applies (E1)."""
+    for seed in range(8):
+        S, N = 2, 3 if seed % 2 else 2
+        tF, tB, tW, c = sy.stage_profile(seed, S, 5, 20, 15)
+        assert sc.exact_optimum(S, N, tF, tB, tW, c) == sc.brute_force_optimum(S, N, tF, tB, tW, c)
+    t = [10, 10]
+    assert sc.exact_optimum(2, 2, t, t, t, [0]) == 70
+    t = [10] * 3
+    assert sc.exact_optimum(3, 4, t, t, t, [0, 0]) == 2 * 10 + 4 * 30      # ZB closed form = LB
+
+
+def test_p11_near_optimal_paper_sizes():
+    """P11: against the optimum, Schedule() with
+    ceil(t_o/delta) = 30 is within 1 % "in all settings" (3-8 stages, 6-32
+    microbatches, random profiles).  Smallest setting, S = 3, N = 6, 24
+    random profiles (op times 5-20, c 0-15): mean gap < 1 % and >= 75 % of
+    instances within 1 %.  (A B > F priority inversion gives a 5.9 % mean,
+    W first 19 %.)"""
+    gaps = []
+    for seed in range(24):
+        tF, tB, tW, c = sy.stage_profile(1000 + seed, 3, 5, 20, 15)
+        delta = sc.default_delta(tF, tB, tW)
+        x = sc.get_adapted_warmup_fwds(3, 6, tF, tB, c)
+        _, T, _ = sc.schedule(3, 6, tF, tB, tW, c, x, delta)
+        opt = sc.exact_optimum(3, 6, tF, tB, tW, c, ub=T)
+        assert opt <= T
+        gaps.append((T - opt) / opt)
+    assert sum(gaps) / len(gaps) < 0.01
+    assert sum(g <= 0.01 for g in gaps) >= 0.75 * len(gaps)
 
 
 def test_p11_near_optimal_tiny():
