@@ -60,6 +60,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--link-mode", default="direct", choices=["direct", "p2p"])
+    ap.add_argument("--replan-log", default="", help="write the adaptive arm's per-step plans (JSONL)")
     return ap.parse_args()
 
 
@@ -228,33 +229,24 @@ def main():
         dist.all_gather_object(out, obj, group=group)
         return out
 
-    # -------- profile t^F, t^B, t^W per stage (ZB order at c = 0), quantised to 1 us
+    # -------- a1: profile t^F, t^B, t^W per stage (ZB order at c = 0): the
+    # library's profiler, median over the last iterations, quantised to 1 us
     zero = [0] * (S - 1)
     prof_arm = Arm("zb", S, N, [1000] * S, [1000] * S, [1000] * S)
-    for _ in range(2):
-        r = pipe.run(prof_arm.orders)
-    loc = {i: [st["op_ns"][k] // max(1, st["op_cnt"][k]) for k in range(3)] for i, st in r.stats.items()}
-    allp = {}
-    for d in gather(loc):
-        allp.update(d)
-    tF = [max(1, allp[i][0] // 1000) * 1000 for i in range(S)]
-    tB = [max(1, allp[i][1] // 1000) * 1000 for i in range(S)]
-    tW = [max(1, allp[i][2] // 1000) * 1000 for i in range(S)]
+    for _ in range(3):
+        pipe.run(prof_arm.orders)
+    tF, tB, tW = pipe.profile(k=2)
     t_ref = sum(tF) // S
     # delegated-path latency used for planning when a link is down: measured
     host_c = measure_host_path(pipe, torch) if rank == 0 else 0
     host_c = max(gather(host_c))
-    # Alg. 1 memory input: F->B stash capacity of stage 0 (M / M^F, R12)
+    # Alg. 1 memory input (R12): M / M^F = the F->B stash capacity of stage 0;
+    # R26 clamps every plan to each stage's capacity (both inside the C planner)
     cap_fb = {i: st.n_slots_fb for i, st in pipe.stages.items()}
     caps = {}
     for d in gather(cap_fb):
         caps.update(d)
     x_cap = [caps[i] for i in range(S)]
-    from paper_2504_19232_b200 import sched as cs
-    x_init = cs.plan_init(S, N, x_cap[0], 1)
-    x_init = [min(v, c) for v, c in zip(x_init, x_cap)]
-    for i in range(S - 2, -1, -1):
-        x_init[i] = max(x_init[i], x_init[i + 1])
 
     events = sy.PAPER_TRACE
     arms = [a for a in args.arms.split(",") if a]
@@ -262,15 +254,16 @@ def main():
     lib = L.lib()
     timer = torch.cuda.Stream(device=local_rank)
 
-    def run_arm(name, with_trace, steps, warmup, e2e=False, prof=False):
-        arm = Arm(name, S, N, tF, tB, tW, x_init=x_init if name.startswith("adaptive") else None, x_cap=x_cap)
-        host_in = None
-        if e2e and 0 in pipe.stages:
-            host_in = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in pipe.inputs]
-            for h, t in zip(host_in, pipe.inputs):
-                h.copy_(t)
+    replan_log = []
+
+    def run_arm(name, with_trace, steps, warmup, e2e=False, prof=False, log=False):
+        arm = Arm(name, S, N, tF, tB, tW, x_cap=x_cap, mem=(x_cap[0], 1))
+        io = pipe.set_host_io(e2e)
         busy_tot, span_tot, n_it, losses = 0, 0, 0, []
         dev_busy = 0
+        if log and rank == 0:
+            replan_log.append({"arm": name, "S": S, "N": N, "tF": tF, "tB": tB, "tW": tW, "x_cap": x_cap,
+                               "mem": [x_cap[0], 1], "ratio": 30, "x_init": arm.x_init})
 
         def one_step(k):
             ev = events[k % len(events)] if with_trace else None
@@ -280,11 +273,16 @@ def main():
                 if pipe.latency[l] != want:
                     pipe.set_latency(l, want)
             orders = arm.plan(c)
-            if host_in is not None:
-                for h, t in zip(host_in, pipe.inputs):
-                    t.copy_(h, non_blocking=True)
-                torch.cuda.current_stream().synchronize()
+            if log and rank == 0:
+                e = dict(arm.last)
+                e["step"] = k
+                e["orders"] = [" ".join(f"{kd}{mb}" for kd, mb in o) for o in orders]
+                replan_log.append(e)
             res = pipe.run(orders, merge_w=arm.merge_w, want_times=True, inorder=arm.inorder)
+            if arm.name == "adaptive":
+                # a1: the profiler tracks op times continuously; the planner adopts
+                # the latest medians at its next re-plan
+                arm.set_profile(*pipe.profile(k=5))
             return res
 
         for k in range(warmup):
@@ -326,7 +324,7 @@ def main():
         if prof:
             lib.adaptra_prof_enable(0)
         n_launch = lib.adaptra_launch_count() - n_launch0
-        g = gather({"ms": ms, "busy": busy_tot, "span": span_tot, "dev_busy": dev_busy, "launches": n_launch,
+        g = gather({"ms": ms, "busy": busy_tot, "span": span_tot, "dev_busy": dev_busy, "launches": n_launch, "io": io,
                     "links": {str(k): v for k, v in pipe.link_stats().items()}})
         ms_max = max(x["ms"] for x in g)
         busy = sum(x["busy"] for x in g)
@@ -345,12 +343,15 @@ def main():
                "gpu_launches": sum(x["launches"] for x in g)}
         if losses:
             out["loss_last"] = losses[-1]
+        out["h2d_bytes"], out["d2h_bytes"] = sum(x["io"][0] for x in g), sum(x["io"][1] for x in g)
+        pipe.set_host_io(False)
         return out
 
     # -------- timed arms: headline = adaptive under the trace
     gem, gem_attn, fused_attn, fused_attn_b = [], [], [], []
     for name in arms:
-        results[(name, "trace")] = run_arm(name, True, args.steps, args.warmup, prof=(name == "adaptive"))
+        results[(name, "trace")] = run_arm(name, True, args.steps, args.warmup, prof=(name == "adaptive"),
+                                           log=(name == "adaptive"))
         if name == "adaptive":
             n, ms, fl, by = (__import__("ctypes").c_int64(), __import__("ctypes").c_double(),
                              __import__("ctypes").c_double(), __import__("ctypes").c_double())
@@ -366,10 +367,19 @@ def main():
         results[(name, "nominal")] = run_arm(name, False, max(3, args.steps // 2), 1)
     e2e = None
     if not args.no_e2e and "adaptive" in arms:
-        e2e_r = run_arm("adaptive", True, max(3, args.steps // 2), 1, e2e=True)
-        bi = N * model.tokens_per_mb * model.d * 2
-        e2e = {"value": e2e_r["tokens_per_s"], "unit": "tokens/s", "h2d_bytes_per_step": bi,
-               "d2h_bytes_per_step": 4}
+        # the same arm, steps and trace events as the timed one, through the
+        # C-ABI's host I/O: inputs uploaded from pinned host memory by the
+        # executor every step, the loss copied back to the host every step
+        e2e_r = run_arm("adaptive", True, args.steps, args.warmup, e2e=True)
+        e2e = {"value": e2e_r["tokens_per_s"], "unit": "tokens/s", "h2d_bytes_per_step": e2e_r["h2d_bytes"],
+               "d2h_bytes_per_step": e2e_r["d2h_bytes"],
+               "how": "adaptra_exec_set_host_io: per step, H2D of all N inputs from pinned host buffers "
+                      "(side stream, F(mb) waits for its copy) and D2H of the loss; same arm/steps/events "
+                      "as the device-timed value"}
+    if args.replan_log and rank == 0:
+        with open(args.replan_log, "w") as f:
+            for e in replan_log:
+                f.write(json.dumps(e) + "\n")
 
     with Clocks(local_rank) as clk:
         clocked = run_arm("adaptive", True, max(3, args.steps // 2), 1)
@@ -445,22 +455,24 @@ def main():
                        "t_ref_us": t_ref / 1e3, "host_path_c_us": host_c / 1e3},
             "arms": {f"{a}/{w}": {k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()}
                      for (a, w), r in results.items()},
-            "roofline": {"bound": "tensor", "achieved": round(achieved, 1) if achieved else None,
+            "roofline": {"bound": "tensor",
+                         "achieved": round(union_tf / world, 1) if union_tf else None,
                          "peak": peak, "unit": "TFLOP/s",
-                         "frac": round(achieved / peak, 4) if achieved else None, "traffic": traffic,
-                         "traffic_source": traffic_src,
-                         "kernel": "gemm_tc_kernel (tcgen05), stage linear layers (Z=1)", "launches": n_l,
-                         "avg_launch_us": round(avg_ms * 1e3, 2),
-                         "note": "per-launch CUDA-event durations on the launching stream during the timed "
-                                 "steps; stages co-located on one GPU run concurrently, which stretches each "
-                                 "launch (see profiles/ for serialised ncu shares)",
+                         "frac": round(union_tf / (world * peak), 4) if union_tf else None,
+                         "traffic": traffic, "traffic_source": traffic_src,
+                         "kernel": "gemm_tc_kernel / gemm_tc_grouped_kernel (tcgen05), stage linear layers",
+                         "how": "algorithmic GEMM FLOPs of the timed steps / the union of the GEMM launch "
+                                "intervals on a GPU (the time any GEMM ran, CUDA events on the launching "
+                                "streams), per GPU; peak = MEASURED_PEAKS bf16 sustained (kernels inside a "
+                                "long step)",
+                         "per_launch": {"achieved": round(achieved, 1) if achieved else None,
+                                        "frac": round(achieved / peak, 4) if achieved else None,
+                                        "launches": n_l, "avg_launch_us": round(avg_ms * 1e3, 2),
+                                        "note": "flops per launch / mean launch duration; with several "
+                                                "stages on one GPU launches overlap, which stretches each "
+                                                "one, so this is not a kernel efficiency there"},
                          "attention_gemm": attn_line,
                          "attention_fused": fused_line,
-                         "class_union": {"achieved": round(union_tf, 1) if union_tf else None,
-                                         "frac": round(union_tf / (world * peak), 4) if union_tf else None,
-                                         "how": "algorithmic GEMM FLOPs of the timed steps / union of the GEMM "
-                                                "launch intervals across a GPU's stage streams (time any GEMM ran), "
-                                                "summed over GPUs; peak x n_gpus"},
                          "isolated": isolated,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"},
             "clocks": clocks,

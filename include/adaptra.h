@@ -103,10 +103,91 @@ int adaptra_replay(int32_t S, int32_t N, const int64_t* tF, const int64_t* tB, c
                    const int64_t* c, const adaptra_op_t* order, const int32_t* n_ops, uint32_t flags,
                    adaptra_op_t* timed_out, int64_t* makespan_out);
 
-/* Number of dependency/completeness violations of a timed schedule (0 = valid). */
+/* One violation found by adaptra_validate / adaptra_validate_plan. */
+typedef struct adaptra_violation {
+  int32_t code;  /* ADAPTRA_V_*                                                  */
+  int32_t stage; /* stage of the offending op (plan codes: the index i of x_i)   */
+  int32_t kind;  /* ADAPTRA_OP_* of the offending op (-1 for plan codes)        */
+  int32_t mb;    /* its microbatch, 1..N (0 for plan codes)                      */
+} adaptra_violation_t;
+
+#define ADAPTRA_V_BADOP 1    /* kind not F/B/W, mb outside 1..N, or a W op in a MERGE_W schedule (R10) */
+#define ADAPTRA_V_DUP 2      /* the op appears twice on its stage                                      */
+#define ADAPTRA_V_MISSING 3  /* one of the stage's 3N (2N with MERGE_W) ops is absent                  */
+#define ADAPTRA_V_DURATION 4 /* end - start != the stage's op time (B + W with MERGE_W)                 */
+#define ADAPTRA_V_OVERLAP 5  /* starts before the previous op of its stage ended (P:2754 busy())        */
+#define ADAPTRA_V_DEP 6      /* starts before a dependency's end + link latency (R1, R2,
+                                R8); one entry per violated dependency                                 */
+#define ADAPTRA_V_NONMONO 7  /* plan: x_i < x_{i+1} (the Lemma); stage = i                 */
+#define ADAPTRA_V_X_LAST 8   /* plan: x_{S-1} < 1 (Alg. 1/2 end at 1)                  */
+#define ADAPTRA_V_X0_GT_N 9  /* plan: x_0 > N (R11)                                                     */
+
+/* Check a timed schedule (layout of adaptra_schedule's ops_out) against the
+ * problem's constraints (violations are values, not errors).
+ * Writes the first min(cap, total) violations to violations_out (caller-owned,
+ * may be NULL when cap == 0) in stage order and sets *n_violations_out to the
+ * total (0 = valid).  EINVAL on bad pointers or n_ops outside 0..3N. */
 int adaptra_validate(int32_t S, int32_t N, const int64_t* tF, const int64_t* tB, const int64_t* tW,
                      const int64_t* c, const adaptra_op_t* ops, const int32_t* n_ops, uint32_t flags,
-                     int32_t* n_violations_out);
+                     adaptra_violation_t* violations_out, int32_t cap, int32_t* n_violations_out);
+/* Check a warm-up plan x[S] (codes ADAPTRA_V_NONMONO / X_LAST / X0_GT_N), same
+ * output convention. */
+int adaptra_validate_plan(int32_t S, int32_t N, const int32_t* x, adaptra_violation_t* violations_out, int32_t cap,
+                          int32_t* n_violations_out);
+
+/* 1F1B warm-up counts x_i = min(S - i, N) (R21 baseline).  x_out[S]. */
+int adaptra_plan_1f1b(int32_t S, int32_t N, int32_t* x_out);
+/* R26 (no host offload of the F->B stash): x_i <- min(x_i, cap_i), then the
+ * Lemma restored from the last stage up, x_i <- max(x_i, x_{i+1}).  In place. */
+int adaptra_clamp_plan(int32_t S, const int32_t* cap, int32_t* x_inout);
+/* R10: delta = max(1, floor(t_o / ratio)), t_o = the largest op time (ratio 30).
+ * Returns delta (1 on bad arguments). */
+int64_t adaptra_default_delta(int32_t S, const int64_t* tF, const int64_t* tB, const int64_t* tW, int32_t ratio);
+
+/* ---------------------------------------------------------------- planner
+ * One schedule arm per object, so that the per-iteration planning decision of
+ * the bench / training loop is one C call (DESIGN.md §3 R18, R21, R26):
+ *  ADAPTRA_ARM_1F1B      x_i = min(S-i, N), Schedule(SEL_CAP | MERGE_W) at c = 0, frozen;
+ *  ADAPTRA_ARM_ZB        x = Alg. 2 at c = 0, Schedule(SEL_PAPER) at c = 0, frozen (R21);
+ *  ADAPTRA_ARM_ADAPTIVE  x_init = desc.x_init if given, else Alg. 1 (mem_capacity /
+ *                        mem_per_act, R12) clamped to x_cap (R26) if mem_per_act > 0,
+ *                        else Alg. 2 at c = 0.  At each step whose c differs from the
+ *                        previous step's (R18): every link nominal (c = 0) -> x_init;
+ *                        else if Eq. 1 fails on some link under the current x -> Alg. 2
+ *                        with c, clamped to x_cap (R26); else x is kept.  The orders are
+ *                        Schedule(SEL_PAPER, c, x, delta).  A profile passed with
+ *                        adaptra_planner_set_profile is adopted at the next such re-plan.
+ * delta = adaptra_default_delta(profile, ratio).  Everything is integer and
+ * bit-exact with the oracle (oracle.sched.adaptive_orders). */
+#define ADAPTRA_ARM_1F1B 0
+#define ADAPTRA_ARM_ZB 1
+#define ADAPTRA_ARM_ADAPTIVE 2
+#define ADAPTRA_MAX_STAGES 64
+
+typedef struct adaptra_planner_desc {
+  int32_t S, N, arm, ratio;          /* ratio: ceil(t_o/delta) target, 0 = 30   */
+  const int64_t *tF, *tB, *tW;       /* [S] op times in ticks (ns), each >= 1            */
+  const int32_t* x_init;             /* [S] or NULL                                      */
+  const int32_t* x_cap;              /* [S] device stash capacity per stage, or NULL      */
+  int64_t mem_capacity, mem_per_act; /* Alg. 1 inputs M, M^F (used if mem_per_act > 0)   */
+} adaptra_planner_desc_t;
+
+typedef struct adaptra_plan_info {
+  int64_t makespan, delta, replans;  /* the simulated T, the step, re-plans so far       */
+  int64_t tF[ADAPTRA_MAX_STAGES], tB[ADAPTRA_MAX_STAGES], tW[ADAPTRA_MAX_STAGES]; /* profile used */
+} adaptra_plan_info_t;
+
+typedef struct adaptra_planner* adaptra_planner_t;
+int adaptra_planner_create(const adaptra_planner_desc_t* d, adaptra_planner_t* out);
+int adaptra_planner_destroy(adaptra_planner_t p);
+/* Queue a new profile (e.g. adaptra_exec_profile's medians); ticks >= 1. */
+int adaptra_planner_set_profile(adaptra_planner_t p, const int64_t* tF, const int64_t* tB, const int64_t* tW);
+/* Plan the next iteration under link latencies c[S-1] (finite, >= 0; a failed
+ * link is planned at its delegated-path cost, R33).  Outputs (each optional):
+ * ops_out[S*3N] / n_ops_out[S] as adaptra_schedule, x_out[S], *replanned_out = 1
+ * when x changed, info. */
+int adaptra_planner_step(adaptra_planner_t p, const int64_t* c, adaptra_op_t* ops_out, int32_t* n_ops_out,
+                         int32_t* x_out, int32_t* replanned_out, adaptra_plan_info_t* info);
 
 /* ================================================================ GEMM
  * One dense contraction C[m,n] = sum_k A(m,k) B(n,k) over Z batches, with a
@@ -266,8 +347,10 @@ int adaptra_stage_zero_grads(adaptra_stage_t s, void* stream);
  *
  * Inbox (library-allocated so it can be exported over CUDA IPC):
  *   mailbox  [n_mb * bytes] device memory of the receiver, one slot per mb;
- *   flags    uint32[n_mb] device memory; message (mb) of iteration `epoch` is
- *            ready when flags[mb] >= epoch (epochs start at 1, increase);
+ *   flags    uint32[n_mb] in pinned, device-mapped HOST memory (a POSIX shm
+ *            segment, so the sender's process can map it); message (mb) of
+ *            iteration `epoch` is ready when flags[mb] >= epoch (epochs start
+ *            at 1, increase; wrap-around compare);
  *   host ring (optional, POSIX shm `host_name`, pinned with cudaHostRegister):
  *            [n_mb * bytes] data + uint32[n_mb] host flags: the delegated path
  *            (P:2270-2350).  A process-wide delegate thread copies arrived host
@@ -309,11 +392,17 @@ int adaptra_inbox_destroy(adaptra_inbox_t ib);
 /* 128 bytes: CUDA IPC handle of the mailbox (64) + name of the flag segment (64). */
 int adaptra_inbox_export(adaptra_inbox_t ib, uint8_t* handle_out);
 void* adaptra_inbox_slot(adaptra_inbox_t ib, int32_t mb);
-/* Enqueue on `consumer` a GPU-side wait (stream memory op, no host blocking,
- * no SM) until message mb of iteration epoch is in the mailbox; the slot
- * address is returned in slot_out. */
+/* Wait on the CALLING HOST THREAD until message mb of iteration epoch is in
+ * the mailbox (its flag, in pinned host memory, reaches epoch; spin, then
+ * yield, then 2 us sleeps; ELINK after $ADAPTRA_TIMEOUT_MS, default 120 s),
+ * then return the slot address in slot_out.  `consumer` is unused: the caller
+ * launches the consuming op on its stream after this returns, so stream order
+ * puts the op after the data.  Only the stage thread that consumes the message
+ * blocks (every stage has its own thread), so a late message delays only the
+ * ops that follow it in that stage's order -- no cross-stage head-of-line
+ * blocking; the paper's busy wait. */
 int adaptra_recv(adaptra_inbox_t ib, int32_t mb, uint32_t epoch, void* consumer, void** slot_out);
-/* Abort path: set every flag to 0x3F3F3F3F (>= any epoch) so that all waiters proceed
+/* Abort path: set every flag to 0x3F3F3F3F (>= any epoch) so that all host waiters proceed
  * (after a failed or timed-out iteration); adaptra_inbox_reset clears flags
  * (and host flags) back to 0 before epochs restart at 1. */
 int adaptra_inbox_poison(adaptra_inbox_t ib);
@@ -345,16 +434,23 @@ int adaptra_send(adaptra_outbox_t ob, int32_t mb, void* producer, uint32_t epoch
  * the compute sequence would). */
 int adaptra_recv_blocking(adaptra_inbox_t ib, int32_t mb, uint32_t epoch, void** slot_out);
 int adaptra_send_wait(adaptra_outbox_t ob, int32_t mb, uint32_t epoch);
-/* Gate statistics since open: messages, sum/max of (flag post - data ready) in ns. */
+/* Gate statistics since open: messages, sum/max of (flag post - data ready) in ns
+ * (all cumulative since the outbox was opened). */
 int adaptra_link_stats(adaptra_outbox_t ob, int64_t* n_msgs, int64_t* sum_delay_ns, int64_t* max_delay_ns);
+/* Same, but the max covers only the messages since the previous _take (it is
+ * reset to 0 by this call); n_msgs and sum_delay_ns stay cumulative. */
+int adaptra_link_stats_take(adaptra_outbox_t ob, int64_t* n_msgs, int64_t* sum_delay_ns, int64_t* max_delay_ns);
 
 /* ================================================================ executor
  * Interprets one iteration of a stage's op order (from adaptra_schedule) on
- * the stage's compute stream from a dedicated host thread: per op, a GPU-side
- * wait for its input message (so a late message never blocks the host from
- * launching later work: no HOL stall), the F/B/W kernels, CUDA
- * events around the op, and the send of its output.  Stash slots are taken
- * at F and released at W (in op order, on the one compute stream).
+ * the stage's compute stream from a dedicated host thread: per op, a host
+ * wait for its input message's flag (adaptra_recv; only this stage's thread
+ * waits, so a late message never stalls another stage's launches: no HOL
+ * stall), the F/B/W kernels, CUDA events around the op, and the
+ * send of its output (adaptra_send: never blocks).  At most
+ * $ADAPTRA_LOOKAHEAD (default 3) ops are queued ahead on the stream.  Stash
+ * slots are taken at F and released at W (in op order, on the one compute
+ * stream).
  */
 typedef struct adaptra_exec_desc {
   adaptra_stage_t stage;
@@ -389,6 +485,13 @@ int adaptra_exec_destroy(adaptra_exec_t e);
  * head-of-line blocking).  Non-blocking (the stage thread enqueues). */
 #define ADAPTRA_EXEC_INORDER 16u
 int adaptra_run_iteration(adaptra_exec_t e, const adaptra_op_t* ops, int32_t n, uint32_t epoch, uint32_t flags);
+/* End-to-end host I/O (NULL disables): on stage 0, host_inputs[n_mb] are pinned
+ * host buffers of `bytes` each; every iteration copies them into the device
+ * inputs of the exec desc (H2D on a side stream, issued in the order stage 0
+ * runs its F ops; F(mb) waits for its own copy), so the input upload overlaps
+ * the pipeline.  On the last stage, host_loss receives the iteration's loss
+ * (D2H behind the last op).  Caller-owned; must outlive the iterations. */
+int adaptra_exec_set_host_io(adaptra_exec_t e, const void* const* host_inputs, int64_t bytes, float* host_loss);
 /* Report op times relative to `event` (a cudaEvent_t recorded by the caller on
  * the stage's device before the iteration; NULL = the stage's own start
  * event), so that stages sharing a device share one time base. */
@@ -401,6 +504,18 @@ int adaptra_exec_join(adaptra_exec_t e);
  * $ADAPTRA_TIMEOUT_MS, default 120000: ELINK on timeout); fill stats.
  * op_times_out (optional, n x 2 int64: start, end ns) gets per-op times. */
 int adaptra_exec_wait(adaptra_exec_t e, adaptra_iter_stats_t* stats_out, int64_t* op_times_out);
+
+/* Profiler ("the profiler continuously tracks ...", P:2436-2437
+ * "leverages CUDA Events"): every adaptra_exec_wait appends the iteration's
+ * mean op time per kind (F, B, W; CUDA events on the compute stream) to the
+ * stage's history (last 256 iterations).  t_out[3] = for each kind the lower
+ * median over the last k iterations that ran that kind, floored to `quantum`
+ * ns and at least one quantum (0 if none ran), i.e. the t^F_i, t^B_i, t^W_i
+ * ticks the planner takes.  EINVAL if k < 1 or quantum < 1. */
+int adaptra_exec_profile(adaptra_exec_t e, int32_t k, int64_t quantum, int64_t* t_out);
+/* The reduction it applies: lower median of v[n], floored to quantum, >= quantum
+ * (-1 on bad arguments).  Pure host function. */
+int64_t adaptra_median_ticks(const int64_t* v, int32_t n, int64_t quantum);
 
 #ifdef __cplusplus
 }

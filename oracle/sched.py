@@ -474,20 +474,31 @@ def clamp_plan(x, cap):
     return out
 
 
+def adaptive_step(S, N, tF, tB, tW, c, x_prev, x_init, x_cap=None, ratio=30):
+    """One iteration boundary of the adaptive arm (R18): every link nominal ->
+    the init plan; Eq. 1 violated on some link under the
+    current plan -> Alg. 2 with the current c (P:2108-2127), clamped by R26;
+    otherwise the current plan is kept.  Returns (x, per-stage (kind, mb)
+    order of Schedule() under c with delta = t_o / ratio, R10)."""
+    if all(v == 0 for v in c):
+        x = list(x_init)
+    elif not all(eq1_holds(tF, tB, c, x_prev)):
+        xa = get_adapted_warmup_fwds(S, N, tF, tB, c)
+        x = clamp_plan(xa, x_cap) if x_cap else xa
+    else:
+        x = list(x_prev)
+    X, _, _ = schedule(S, N, tF, tB, tW, c, x, default_delta(tF, tB, tW, ratio))
+    return x, order_of(X)
+
+
 def adaptive_orders(S, N, tF, tB, tW, cs_seq, x_init, x_cap=None, ratio=30):
     """The adaptive arm over a sequence of per-iteration latency vectors
     (R18): returns [(x, per-stage (kind, mb) order)] for every iteration."""
-    delta = default_delta(tF, tB, tW, ratio)
     x = list(x_init)
     out = []
     for c in cs_seq:
-        if all(v == 0 for v in c):
-            x = list(x_init)
-        elif not all(eq1_holds(tF, tB, c, x)):
-            xa = get_adapted_warmup_fwds(S, N, tF, tB, c)
-            x = clamp_plan(xa, x_cap) if x_cap else xa
-        X, _, _ = schedule(S, N, tF, tB, tW, c, x, delta)
-        out.append((list(x), order_of(X)))
+        x, order = adaptive_step(S, N, tF, tB, tW, c, x, x_init, x_cap, ratio)
+        out.append((list(x), order))
     return out
 
 

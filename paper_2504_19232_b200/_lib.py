@@ -41,6 +41,28 @@ class Op(C.Structure):
     _fields_ = [("kind", _i32), ("mb", _i32), ("start", _i64), ("end", _i64)]
 
 
+class Violation(C.Structure):
+    _fields_ = [("code", _i32), ("stage", _i32), ("kind", _i32), ("mb", _i32)]
+
+
+V_CODES = {1: "badop", 2: "dup", 3: "missing", 4: "duration", 5: "overlap", 6: "dep",
+           7: "nonmono", 8: "x_last", 9: "x0_gt_N"}
+ARM_1F1B, ARM_ZB, ARM_ADAPTIVE = 0, 1, 2
+MAX_STAGES = 64
+
+
+class PlannerDesc(C.Structure):
+    _fields_ = [("S", _i32), ("N", _i32), ("arm", _i32), ("ratio", _i32),
+                ("tF", C.POINTER(_i64)), ("tB", C.POINTER(_i64)), ("tW", C.POINTER(_i64)),
+                ("x_init", C.POINTER(_i32)), ("x_cap", C.POINTER(_i32)),
+                ("mem_capacity", _i64), ("mem_per_act", _i64)]
+
+
+class PlanInfo(C.Structure):
+    _fields_ = [("makespan", _i64), ("delta", _i64), ("replans", _i64),
+                ("tF", _i64 * MAX_STAGES), ("tB", _i64 * MAX_STAGES), ("tW", _i64 * MAX_STAGES)]
+
+
 class GemmDesc(C.Structure):
     _fields_ = [
         ("dtype", _i32), ("M", _i32), ("N", _i32), ("K", _i32), ("Z", _i32), ("zdiv", _i32),
@@ -90,7 +112,15 @@ _SIGS = {
     "adaptra_replay": (_i32, [_i32, _i32, _P(_i64), _P(_i64), _P(_i64), _P(_i64), _P(Op), _P(_i32), _u32,
                               _P(Op), _P(_i64)]),
     "adaptra_validate": (_i32, [_i32, _i32, _P(_i64), _P(_i64), _P(_i64), _P(_i64), _P(Op), _P(_i32), _u32,
-                                _P(_i32)]),
+                                _P(Violation), _i32, _P(_i32)]),
+    "adaptra_validate_plan": (_i32, [_i32, _i32, _P(_i32), _P(Violation), _i32, _P(_i32)]),
+    "adaptra_plan_1f1b": (_i32, [_i32, _i32, _P(_i32)]),
+    "adaptra_clamp_plan": (_i32, [_i32, _P(_i32), _P(_i32)]),
+    "adaptra_default_delta": (_i64, [_i32, _P(_i64), _P(_i64), _P(_i64), _i32]),
+    "adaptra_planner_create": (_i32, [_P(PlannerDesc), _P(_vp)]),
+    "adaptra_planner_destroy": (_i32, [_vp]),
+    "adaptra_planner_set_profile": (_i32, [_vp, _P(_i64), _P(_i64), _P(_i64)]),
+    "adaptra_planner_step": (_i32, [_vp, _P(_i64), _P(Op), _P(_i32), _P(_i32), _P(_i32), _P(PlanInfo)]),
     "adaptra_gemm": (_i32, [_P(GemmDesc), _vp]),
     "adaptra_prof_enable": (_i32, [_i32]),
     "adaptra_launch_count": (_i64, []),
@@ -126,12 +156,16 @@ _SIGS = {
     "adaptra_recv_blocking": (_i32, [_vp, _i32, _u32, _P(_vp)]),
     "adaptra_send_wait": (_i32, [_vp, _i32, _u32]),
     "adaptra_link_stats": (_i32, [_vp, _P(_i64), _P(_i64), _P(_i64)]),
+    "adaptra_link_stats_take": (_i32, [_vp, _P(_i64), _P(_i64), _P(_i64)]),
     "adaptra_exec_create": (_i32, [_P(ExecDesc), _P(_vp)]),
     "adaptra_exec_destroy": (_i32, [_vp]),
     "adaptra_run_iteration": (_i32, [_vp, _P(Op), _i32, _u32, _u32]),
     "adaptra_exec_set_time_base": (_i32, [_vp, _vp]),
+    "adaptra_exec_set_host_io": (_i32, [_vp, _P(_vp), _i64, _vp]),
     "adaptra_exec_join": (_i32, [_vp]),
     "adaptra_exec_wait": (_i32, [_vp, _P(IterStats), _P(_i64)]),
+    "adaptra_exec_profile": (_i32, [_vp, _i32, _i64, _P(_i64)]),
+    "adaptra_median_ticks": (_i64, [_P(_i64), _i32, _i64]),
 }
 
 _lib = None

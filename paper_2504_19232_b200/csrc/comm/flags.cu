@@ -69,24 +69,6 @@ int host_wait_hmem(const volatile uint32_t* p, uint32_t v) {
   return ADAPTRA_OK;
 }
 
-// Host-side wait on a flag in device memory (copies it back); diagnostics only.
-int host_wait(const uint32_t* addr, uint32_t v) {
-  thread_local uint32_t* h = nullptr;
-  thread_local cudaStream_t s = nullptr;
-  if (!h) {
-    cudaHostAlloc((void**)&h, 64, cudaHostAllocDefault);
-    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
-  }
-  const uint64_t t0 = (uint64_t)now_ns();
-  for (;;) {
-    cudaMemcpyAsync(h, addr, 4, cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    if ((int32_t)(*h - v) >= 0) return ADAPTRA_OK;
-    if ((uint64_t)now_ns() - t0 > wait_timeout_ns()) return set_error(ADAPTRA_ELINK, "host wait timed out");
-    std::this_thread::sleep_for(std::chrono::microseconds(20));
-  }
-}
-
 int stream_write(cudaStream_t st, uint32_t* addr, uint32_t v) {
   signal_flag_kernel<<<1, 1, 0, st>>>(addr, v);
   count_launch();

@@ -679,3 +679,12 @@ extern "C" int adaptra_link_stats(adaptra_outbox_t ob, int64_t* n, int64_t* sum,
   if (mx) *mx = ob->max_delay.load();
   return ADAPTRA_OK;
 }
+
+extern "C" int adaptra_link_stats_take(adaptra_outbox_t ob, int64_t* n, int64_t* sum, int64_t* mx) {
+  if (!ob) return set_error(ADAPTRA_EINVAL, "link_stats_take: null");
+  if (n) *n = ob->n_msgs.load();
+  if (sum) *sum = ob->sum_delay.load();
+  const int64_t m = ob->max_delay.exchange(0);
+  if (mx) *mx = m;
+  return ADAPTRA_OK;
+}

@@ -1,14 +1,19 @@
 // Per-stage schedule executor: one host thread per stage interprets the
-// stage's op order for one iteration.  Inputs are awaited on the GPU
-// (adaptra_recv enqueues a stream memory wait), so the thread enqueues the
-// whole iteration without ever blocking on communication: a late message
-// delays only the ops that depend on it, never the launch of later kernels
-// (no head-of-line blocking).  Outputs are handed to the outbox
-// right after the producing op (adaptra_send, own stream).
+// stage's op order for one iteration.  Before an op that consumes a message
+// the stage's thread waits on the message's flag in pinned host memory
+// (adaptra_recv); every stage has its own thread, so a late message delays
+// only the ops after it in that stage's order and never another stage's
+// launches (no cross-stage head-of-line blocking).  Outputs are
+// handed to the outbox right after the producing op (adaptra_send, never
+// blocks).  ADAPTRA_EXEC_INORDER is the blocking baseline (N1).  Per-kind op
+// times feed the profiler (adaptra_exec_profile, a1).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <condition_variable>
+#include <array>
+#include <deque>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -54,6 +59,16 @@ struct adaptra_exec {
   cudaEvent_t ev_base = nullptr;  // optional common time base (same device), set by the caller
   std::vector<cudaEvent_t> ev_s, ev_e;
   std::vector<int> slot_of_mb;
+  // a1 profiler: per completed iteration, the mean op time per kind (ns; -1 = none)
+  std::deque<std::array<int64_t, 3>> hist;
+  // host I/O (end-to-end runs): stage 0 copies each microbatch's input from
+  // pinned host memory (H2D on its own stream, overlapped with compute; F(mb)
+  // waits for its copy); the last stage copies the loss back at the end
+  const void* const* host_inputs = nullptr;
+  int64_t host_in_bytes = 0;
+  float* host_loss = nullptr;
+  cudaStream_t h2d = nullptr;
+  std::vector<cudaEvent_t> ev_in;
 
   int run_one() {
     cudaSetDevice(dev);
@@ -66,6 +81,16 @@ struct adaptra_exec {
     slot_of_mb.assign(N + 1, -1);
     ADAPTRA_CUDA_TRY(cudaEventRecord(ev_t0, cs));
     if (i == S - 1 && d.loss_acc) ADAPTRA_CUDA_TRY(cudaMemsetAsync(d.loss_acc, 0, sizeof(float), cs));
+    if (i == 0 && host_inputs) {
+      // the iteration's inputs, in the order stage 0 consumes them
+      ADAPTRA_CUDA_TRY(cudaStreamWaitEvent(h2d, ev_t0, 0));
+      for (const adaptra_op_t& o : ops) {
+        if (o.kind != ADAPTRA_OP_F || o.mb < 1 || o.mb > N) continue;
+        ADAPTRA_CUDA_TRY(cudaMemcpyAsync((void*)d.inputs[o.mb - 1], host_inputs[o.mb - 1], host_in_bytes,
+                                         cudaMemcpyHostToDevice, h2d));
+        ADAPTRA_CUDA_TRY(cudaEventRecord(ev_in[o.mb - 1], h2d));
+      }
+    }
     int rc;
     DBG("start epoch %u n_ops %zu", epoch, ops.size());
     if ((rc = adaptra_stage_zero_grads(d.stage, cs))) return rc;  // gradients of this iteration only
@@ -94,6 +119,7 @@ struct adaptra_exec {
         const void* x = nullptr;
         if (i == 0) {
           x = d.inputs[mb - 1];
+          if (host_inputs) ADAPTRA_CUDA_TRY(cudaStreamWaitEvent(cs, ev_in[mb - 1], 0));
         } else {
           void* p = nullptr;
           if ((rc = inorder ? adaptra_recv_blocking(d.in_fwd, mb - 1, epoch, &p)
@@ -143,6 +169,8 @@ struct adaptra_exec {
         return set_error(ADAPTRA_EINVAL, "exec: bad op kind");
       }
     }
+    if (i == S - 1 && host_loss && d.loss_acc)
+      ADAPTRA_CUDA_TRY(cudaMemcpyAsync(host_loss, d.loss_acc, sizeof(float), cudaMemcpyDeviceToHost, cs));
     host_ns = now_ns() - t_start;
     DBG("enqueued all");
     return ADAPTRA_OK;
@@ -202,6 +230,8 @@ extern "C" int adaptra_exec_destroy(adaptra_exec_t e) {
   e->cv.notify_all();
   e->th.join();
   cudaSetDevice(e->dev);
+  if (e->h2d) cudaStreamDestroy(e->h2d);
+  for (auto ev : e->ev_in) cudaEventDestroy(ev);
   cudaEventDestroy(e->ev_t0);
   for (auto ev : e->ev_s) cudaEventDestroy(ev);
   for (auto ev : e->ev_e) cudaEventDestroy(ev);
@@ -221,6 +251,26 @@ extern "C" int adaptra_run_iteration(adaptra_exec_t e, const adaptra_op_t* ops, 
   e->busy = true;
   e->rc = ADAPTRA_OK;
   e->cv.notify_all();
+  return ADAPTRA_OK;
+}
+
+extern "C" int adaptra_exec_set_host_io(adaptra_exec_t e, const void* const* host_inputs, int64_t bytes,
+                                        float* host_loss) {
+  if (!e) return set_error(ADAPTRA_EINVAL, "exec_set_host_io: null");
+  std::unique_lock<std::mutex> lk(e->mu);
+  if (e->busy) return set_error(ADAPTRA_EINVAL, "exec_set_host_io: iteration running");
+  const int i = e->d.stage_index, S = e->d.n_stages, N = e->d.n_microbatches;
+  if (host_inputs && (i != 0 || bytes <= 0)) return set_error(ADAPTRA_EINVAL, "exec_set_host_io: inputs on stage 0 only");
+  if (host_loss && i != S - 1) return set_error(ADAPTRA_EINVAL, "exec_set_host_io: loss on the last stage only");
+  cudaSetDevice(e->dev);
+  if (host_inputs && !e->h2d) {
+    ADAPTRA_CUDA_TRY(cudaStreamCreateWithFlags(&e->h2d, cudaStreamNonBlocking));
+    e->ev_in.resize(N);
+    for (auto& ev : e->ev_in) ADAPTRA_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  }
+  e->host_inputs = host_inputs;
+  e->host_in_bytes = bytes;
+  e->host_loss = host_loss;
   return ADAPTRA_OK;
 }
 
@@ -285,5 +335,29 @@ extern "C" int adaptra_exec_wait(adaptra_exec_t e, adaptra_iter_stats_t* st, int
   if (s.n_ops == 0) s.first_start_ns = 0;
   s.host_enqueue_ns = e->host_ns;
   if (st) *st = s;
+  std::array<int64_t, 3> m{-1, -1, -1};
+  for (int k = 0; k < 3; ++k)
+    if (s.op_cnt[k] > 0) m[k] = s.op_ns[k] / s.op_cnt[k];
+  e->hist.push_back(m);
+  while (e->hist.size() > 256) e->hist.pop_front();
+  return ADAPTRA_OK;
+}
+
+extern "C" int64_t adaptra_median_ticks(const int64_t* v, int32_t n, int64_t quantum) {
+  if (!v || n < 1 || quantum < 1) return -1;
+  std::vector<int64_t> a(v, v + n);
+  std::sort(a.begin(), a.end());
+  const int64_t med = a[(n - 1) / 2];                  // lower median
+  return std::max<int64_t>(quantum, med / quantum * quantum);  // floor to the quantum, >= 1 quantum
+}
+
+extern "C" int adaptra_exec_profile(adaptra_exec_t e, int32_t k, int64_t quantum, int64_t* t_out) {
+  if (!e || k < 1 || quantum < 1 || !t_out) return set_error(ADAPTRA_EINVAL, "exec_profile: bad args");
+  for (int kind = 0; kind < 3; ++kind) {
+    std::vector<int64_t> v;
+    for (auto it = e->hist.rbegin(); it != e->hist.rend() && (int)v.size() < k; ++it)
+      if ((*it)[kind] >= 0) v.push_back((*it)[kind]);
+    t_out[kind] = v.empty() ? 0 : adaptra_median_ticks(v.data(), (int32_t)v.size(), quantum);
+  }
   return ADAPTRA_OK;
 }

@@ -20,6 +20,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -906,12 +907,12 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
   CUtensorMap m;
   int rc = map2d(&m, qkv, (int64_t)b * T, 3LL * d, 3LL * d, 2, 64, AT, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
-  static unsigned attr = 0;
+  static std::atomic<unsigned> attr{0};  // per device; stage threads may race here
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!(attr & (1u << dev))) {
+  if (!(attr.load(std::memory_order_acquire) & (1u << dev))) {
     cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem);
-    attr |= 1u << dev;
+    attr.fetch_or(1u << dev, std::memory_order_release);
   }
   AttnArgs a{};
   a.b = b; a.H = H; a.T = T; a.d = d;
@@ -950,12 +951,12 @@ int attn_bwd_tc(const bf16* qkv, const bf16* dO, const float* lse, const float* 
   if (!rc) rc = map2d(&mdo, dO, (int64_t)b * T, d, d, 2, 64, QB, CU_TENSOR_MAP_SWIZZLE_128B);
   if (!rc) rc = map2d(&mdq, dq_acc, (int64_t)b * H * AT, T, T, 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
-  static unsigned attr = 0;
+  static std::atomic<unsigned> attr{0};  // per device; stage threads may race here
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!(attr & (1u << dev))) {
+  if (!(attr.load(std::memory_order_acquire) & (1u << dev))) {
     cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem);
-    attr |= 1u << dev;
+    attr.fetch_or(1u << dev, std::memory_order_release);
   }
   AttnArgs a{};
   a.b = b; a.H = H; a.T = T; a.d = d;

@@ -20,6 +20,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -566,12 +567,12 @@ static int launch_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
   ti.k_blocks = (g.K + BK - 1) / BK;
   const int n_tiles = ti.m_blocks * ti.n_blocks * ti.Z;
   auto kern = gemm_tc_kernel<CG, BN, AMN, BMN>;
-  static unsigned attr_mask = 0;  // per device
+  static std::atomic<unsigned> attr_mask{0};  // per device; stage threads may race here
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!(attr_mask & (1u << dev))) {
+  if (!(attr_mask.load(std::memory_order_acquire) & (1u << dev))) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
-    attr_mask |= 1u << dev;
+    attr_mask.fetch_or(1u << dev, std::memory_order_release);
   }
   bool f32out = (g.epi == ADAPTRA_EPI_ACC_F32 || g.epi == ADAPTRA_EPI_STORE_F32);
   int vec_ok = (g.ldc % (f32out ? 4 : 8) == 0) && ((uintptr_t)g.C % 16 == 0) &&
@@ -915,12 +916,12 @@ int gemm_tc_grouped(const adaptra_gemm_desc_t* gs, int n, cudaStream_t st) {
   ga.tile_start[n] = tiles;
   ga.total_tiles = tiles;
   auto kern = gemm_tc_grouped_kernel<BN>;
-  static unsigned attr_mask = 0;
+  static std::atomic<unsigned> attr_mask{0};  // per device; stage threads may race here
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!(attr_mask & (1u << dev))) {
+  if (!(attr_mask.load(std::memory_order_acquire) & (1u << dev))) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
-    attr_mask |= 1u << dev;
+    attr_mask.fetch_or(1u << dev, std::memory_order_release);
   }
   const int slots = num_sms() / 2;
   const int grid = (tiles < slots ? tiles : slots) * 2;

@@ -270,10 +270,18 @@ extern "C" int adaptra_replay(int32_t S, int32_t N, const int64_t* tF, const int
   return ADAPTRA_OK;
 }
 
+namespace {
+void push_v(adaptra_violation_t* out, int32_t cap, int32_t& n, int32_t code, int32_t stage, int32_t kind, int32_t mb) {
+  if (out && n < cap) out[n] = adaptra_violation_t{code, stage, kind, mb};
+  n++;
+}
+}  // namespace
+
 extern "C" int adaptra_validate(int32_t S, int32_t N, const int64_t* tF, const int64_t* tB, const int64_t* tW,
                                 const int64_t* c, const adaptra_op_t* ops, const int32_t* n_ops, uint32_t flags,
-                                int32_t* n_viol) {
-  if (S < 1 || N < 1 || !tF || !tB || !tW || (S > 1 && !c) || !ops || !n_ops || !n_viol)
+                                adaptra_violation_t* out, int32_t cap, int32_t* n_viol) {
+  if (S < 1 || N < 1 || !tF || !tB || !tW || (S > 1 && !c) || !ops || !n_ops || !n_viol || cap < 0 ||
+      (cap > 0 && !out))
     return set_error(ADAPTRA_EINVAL, "validate: bad arguments");
   const bool merge = flags & ADAPTRA_MERGE_W;
   Dur du(S, tF, tB, tW, merge);
@@ -281,25 +289,26 @@ extern "C" int adaptra_validate(int32_t S, int32_t N, const int64_t* tF, const i
   std::vector<int64_t> st((size_t)S * 3 * N, -1), en((size_t)S * 3 * N, -1);
   int32_t v = 0;
   for (int i = 0; i < S; ++i) {
+    if (n_ops[i] < 0 || n_ops[i] > per) return set_error(ADAPTRA_EINVAL, "validate: bad n_ops");
     int64_t prev_end = INT64_MIN;
     for (int q = 0; q < n_ops[i]; ++q) {
       const adaptra_op_t& o = ops[(int64_t)i * per + q];
       if (o.kind < 0 || o.kind > 2 || o.mb < 1 || o.mb > N || (merge && o.kind == ADAPTRA_OP_W)) {
-        v++;
+        push_v(out, cap, v, ADAPTRA_V_BADOP, i, o.kind, o.mb);
         continue;
       }
       size_t key = ((size_t)i * 3 + o.kind) * N + (o.mb - 1);
-      if (st[key] >= 0) v++;  // duplicate
+      if (st[key] >= 0) push_v(out, cap, v, ADAPTRA_V_DUP, i, o.kind, o.mb);
       st[key] = o.start;
       en[key] = o.end;
-      if (o.end - o.start != du.d[o.kind][i]) v++;
-      if (o.start < prev_end) v++;
+      if (o.end - o.start != du.d[o.kind][i]) push_v(out, cap, v, ADAPTRA_V_DURATION, i, o.kind, o.mb);
+      if (o.start < prev_end) push_v(out, cap, v, ADAPTRA_V_OVERLAP, i, o.kind, o.mb);
       prev_end = o.end;
     }
     for (int k = 0; k < 3; ++k) {
       if (merge && k == ADAPTRA_OP_W) continue;
       for (int j = 0; j < N; ++j)
-        if (st[((size_t)i * 3 + k) * N + j] < 0) v++;  // missing
+        if (st[((size_t)i * 3 + k) * N + j] < 0) push_v(out, cap, v, ADAPTRA_V_MISSING, i, k, j + 1);
     }
   }
   for (int i = 0; i < S; ++i)
@@ -313,9 +322,181 @@ extern "C" int adaptra_validate(int32_t S, int32_t N, const int64_t* tF, const i
           if (merge && dk[q] == ADAPTRA_OP_W) continue;
           int64_t e = en[((size_t)ds[q] * 3 + dk[q]) * N + j];
           if (e < 0) continue;
-          if (s0 < e + (dl[q] >= 0 ? c[dl[q]] : 0)) v++;
+          if (s0 < e + (dl[q] >= 0 ? c[dl[q]] : 0)) push_v(out, cap, v, ADAPTRA_V_DEP, i, k, j + 1);
         }
       }
   *n_viol = v;
+  return ADAPTRA_OK;
+}
+
+extern "C" int adaptra_validate_plan(int32_t S, int32_t N, const int32_t* x, adaptra_violation_t* out, int32_t cap,
+                                     int32_t* n_viol) {
+  if (S < 1 || !x || !n_viol || cap < 0 || (cap > 0 && !out)) return set_error(ADAPTRA_EINVAL, "validate_plan: bad arguments");
+  int32_t v = 0;
+  for (int i = 0; i + 1 < S; ++i)
+    if (x[i] < x[i + 1]) push_v(out, cap, v, ADAPTRA_V_NONMONO, i, -1, 0);
+  if (x[S - 1] < 1) push_v(out, cap, v, ADAPTRA_V_X_LAST, S - 1, -1, 0);
+  if (x[0] > N) push_v(out, cap, v, ADAPTRA_V_X0_GT_N, 0, -1, 0);
+  *n_viol = v;
+  return ADAPTRA_OK;
+}
+
+extern "C" int adaptra_plan_1f1b(int32_t S, int32_t N, int32_t* x) {
+  if (S < 1 || N < 1 || !x) return set_error(ADAPTRA_EINVAL, "plan_1f1b: bad arguments");
+  for (int i = 0; i < S; ++i) x[i] = std::min<int32_t>(S - i, N);  // canonical 1F1B warm-ups
+  return ADAPTRA_OK;
+}
+
+extern "C" int adaptra_clamp_plan(int32_t S, const int32_t* cap, int32_t* x) {
+  if (S < 1 || !cap || !x) return set_error(ADAPTRA_EINVAL, "clamp_plan: bad arguments");
+  for (int i = 0; i < S; ++i) x[i] = std::min(x[i], cap[i]);       // R26
+  for (int i = S - 2; i >= 0; --i) x[i] = std::max(x[i], x[i + 1]);  // Lemma
+  return ADAPTRA_OK;
+}
+
+extern "C" int64_t adaptra_default_delta(int32_t S, const int64_t* tF, const int64_t* tB, const int64_t* tW,
+                                         int32_t ratio) {
+  if (S < 1 || !tF || !tB || !tW || ratio < 1) return 1;
+  int64_t t_o = 0;
+  for (int i = 0; i < S; ++i) t_o = std::max({t_o, tF[i], tB[i], tW[i]});
+  return std::max<int64_t>(1, t_o / ratio);  // R10: delta = max(1, floor(t_o / 30))
+}
+
+// ---------------------------------------------------------------- planner
+// The arm policies (R18, R21, R26) on top of the planning calls above.
+struct adaptra_planner {
+  int32_t S = 0, N = 0, arm = 0, ratio = 30;
+  std::vector<int64_t> tF, tB, tW;           // profile in use
+  std::vector<int64_t> ptF, ptB, ptW;        // pending profile (applied at the next re-plan)
+  bool pending = false;
+  std::vector<int32_t> x, x_init, x_cap;
+  std::vector<int64_t> c;                    // latencies the current orders were planned for
+  std::vector<adaptra_op_t> ops;             // S * 3N
+  std::vector<int32_t> n_ops;
+  int64_t makespan = 0, delta = 1, replans = 0;
+  bool have = false;
+
+  int plan_for(const int64_t* cv) {
+    const uint32_t fl = arm == ADAPTRA_ARM_1F1B ? (ADAPTRA_SEL_CAP | ADAPTRA_MERGE_W) : ADAPTRA_SEL_PAPER;
+    int64_t steps = 0;
+    return adaptra_schedule(S, N, tF.data(), tB.data(), tW.data(), cv, x.data(), delta, fl, ops.data(), n_ops.data(),
+                            &makespan, &steps);
+  }
+};
+
+extern "C" int adaptra_planner_create(const adaptra_planner_desc_t* d, adaptra_planner_t* out) {
+  if (!d || !out || d->S < 2 || d->N < 1 || !d->tF || !d->tB || !d->tW || d->arm < 0 || d->arm > 2)
+    return set_error(ADAPTRA_EINVAL, "planner_create: bad arguments");
+  auto* p = new adaptra_planner();
+  const int S = d->S, N = d->N;
+  p->S = S;
+  p->N = N;
+  p->arm = d->arm;
+  p->ratio = d->ratio > 0 ? d->ratio : 30;
+  p->tF.assign(d->tF, d->tF + S);
+  p->tB.assign(d->tB, d->tB + S);
+  p->tW.assign(d->tW, d->tW + S);
+  p->x.assign(S, 0);
+  p->c.assign(S - 1, 0);
+  p->ops.resize((size_t)S * 3 * N);
+  p->n_ops.assign(S, 0);
+  if (d->x_cap) p->x_cap.assign(d->x_cap, d->x_cap + S);
+  p->delta = adaptra_default_delta(S, p->tF.data(), p->tB.data(), p->tW.data(), p->ratio);
+  int rc = ADAPTRA_OK;
+  if (d->arm == ADAPTRA_ARM_1F1B) {
+    rc = adaptra_plan_1f1b(S, N, p->x.data());                              // R21 baseline
+  } else if (d->arm == ADAPTRA_ARM_ZB) {
+    rc = adaptra_plan_adapt(S, N, p->tF.data(), p->tB.data(), p->c.data(), p->x.data());  // R21: Alg. 2 at c = 0
+  } else if (d->x_init) {
+    p->x.assign(d->x_init, d->x_init + S);
+  } else if (d->mem_per_act > 0) {
+    rc = adaptra_plan_init(S, N, d->mem_capacity, d->mem_per_act, p->x.data());  // Alg. 1 (R12)
+    if (!rc && !p->x_cap.empty()) rc = adaptra_clamp_plan(S, p->x_cap.data(), p->x.data());
+  } else {
+    rc = adaptra_plan_adapt(S, N, p->tF.data(), p->tB.data(), p->c.data(), p->x.data());
+  }
+  if (!rc) rc = p->plan_for(p->c.data());
+  if (rc) {
+    delete p;
+    return rc;
+  }
+  p->x_init = p->x;
+  p->have = true;
+  *out = p;
+  return ADAPTRA_OK;
+}
+
+extern "C" int adaptra_planner_destroy(adaptra_planner_t p) {
+  delete p;
+  return ADAPTRA_OK;
+}
+
+extern "C" int adaptra_planner_set_profile(adaptra_planner_t p, const int64_t* tF, const int64_t* tB,
+                                           const int64_t* tW) {
+  if (!p || !tF || !tB || !tW) return set_error(ADAPTRA_EINVAL, "planner_set_profile: bad arguments");
+  for (int i = 0; i < p->S; ++i)
+    if (tF[i] < 1 || tB[i] < 1 || tW[i] < 1) return set_error(ADAPTRA_EINVAL, "planner_set_profile: times >= 1");
+  p->ptF.assign(tF, tF + p->S);
+  p->ptB.assign(tB, tB + p->S);
+  p->ptW.assign(tW, tW + p->S);
+  p->pending = true;
+  return ADAPTRA_OK;
+}
+
+extern "C" int adaptra_planner_step(adaptra_planner_t p, const int64_t* c, adaptra_op_t* ops_out, int32_t* n_ops_out,
+                                    int32_t* x_out, int32_t* replanned_out, adaptra_plan_info_t* info) {
+  if (!p || !c) return set_error(ADAPTRA_EINVAL, "planner_step: bad arguments");
+  const int S = p->S, N = p->N;
+  for (int i = 0; i + 1 < S; ++i)
+    if (c[i] < 0 || c[i] == ADAPTRA_LINK_DOWN) return set_error(ADAPTRA_EINVAL, "planner_step: c must be finite >= 0");
+  int32_t replanned = 0;
+  const bool same_c = std::equal(p->c.begin(), p->c.end(), c);
+  if (p->arm == ADAPTRA_ARM_ADAPTIVE && !same_c) {
+    // R18 at an iteration boundary, with the latest profile (a1)
+    if (p->pending) {
+      p->tF = p->ptF;
+      p->tB = p->ptB;
+      p->tW = p->ptW;
+      p->pending = false;
+      p->delta = adaptra_default_delta(S, p->tF.data(), p->tB.data(), p->tW.data(), p->ratio);
+    }
+    std::vector<int32_t> xn = p->x;
+    bool nominal = true;
+    for (int i = 0; i + 1 < S; ++i) nominal = nominal && c[i] == 0;
+    if (nominal) {
+      xn = p->x_init;                                   // every link nominal: the init plan
+    } else {
+      std::vector<uint8_t> ok(S - 1);
+      int rc = adaptra_eq1_holds(S, p->tF.data(), p->tB.data(), c, p->x.data(), ok.data());
+      if (rc) return rc;
+      bool all = true;
+      for (auto v : ok) all = all && v;
+      if (!all) {                                        // Eq. 1 violated: Alg. 2 with the current c
+        rc = adaptra_plan_adapt(S, N, p->tF.data(), p->tB.data(), c, xn.data());
+        if (!rc && !p->x_cap.empty()) rc = adaptra_clamp_plan(S, p->x_cap.data(), xn.data());  // R26
+        if (rc) return rc;
+      }
+    }
+    replanned = xn != p->x;
+    p->replans += replanned;
+    p->x = xn;
+    p->c.assign(c, c + S - 1);
+    int rc = p->plan_for(p->c.data());
+    if (rc) return rc;
+  }
+  if (ops_out) std::copy(p->ops.begin(), p->ops.end(), ops_out);
+  if (n_ops_out) std::copy(p->n_ops.begin(), p->n_ops.end(), n_ops_out);
+  if (x_out) std::copy(p->x.begin(), p->x.end(), x_out);
+  if (replanned_out) *replanned_out = replanned;
+  if (info) {
+    info->makespan = p->makespan;
+    info->delta = p->delta;
+    info->replans = p->replans;
+    for (int i = 0; i < S && i < ADAPTRA_MAX_STAGES; ++i) {
+      info->tF[i] = p->tF[i];
+      info->tB[i] = p->tB[i];
+      info->tW[i] = p->tW[i];
+    }
+  }
   return ADAPTRA_OK;
 }

@@ -59,7 +59,8 @@ class LinkMonitor:
         for name, boxes in (("fwd", self.pipe.out_fwd), ("bwd", self.pipe.out_bwd)):
             for i, h in boxes.items():
                 n, s, m = C.c_int64(), C.c_int64(), C.c_int64()
-                L.check(lib.adaptra_link_stats(h, C.byref(n), C.byref(s), C.byref(m)))
+                # max since the previous sample (reset on read); counts cumulative
+                L.check(lib.adaptra_link_stats_take(h, C.byref(n), C.byref(s), C.byref(m)))
                 # link index: fwd outbox of stage i feeds link i, bwd outbox of stage i feeds link i-1
                 link = i if name == "fwd" else i - 1
                 out[(name, link)] = (n.value, s.value, m.value)

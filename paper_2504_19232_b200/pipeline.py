@@ -248,6 +248,12 @@ class Pipeline:
         """One iteration.  orders[i] = [(kind, mb), ...] for every stage i (only
         local stages are executed here).  Returns IterResult with local stats."""
         lib = L.lib()
+        # Iteration boundary across ranks (the optimizer-step boundary of real
+        # training): the receiver's W of the previous iteration still reads
+        # its inbox slots (x_in / dy_in alias the mailboxes until W), so no
+        # sender may start writing them for the next iteration before every
+        # rank has finished the previous one (write-after-read across ranks).
+        self._barrier()
         self.epoch += 1
         flags = (L.MERGE_W if merge_w else 0) | (L.EXEC_INORDER if inorder else 0)
         self._base_event.record(self._base_stream)
@@ -279,8 +285,56 @@ class Pipeline:
             if want_times:
                 st["op_times"] = [(times[2 * q], times[2 * q + 1]) for q in range(n)]
             stats[i] = st
-        loss = float(self.loss.item()) if self.S - 1 in self.stages else None
+        if self.S - 1 not in self.stages:
+            loss = None
+        elif getattr(self, "_host_loss", None) is not None:
+            loss = float(self._host_loss[0])          # already copied back by the executor
+        else:
+            loss = float(self.loss.item())
         return IterResult(self.epoch, stats, loss)
+
+    def set_host_io(self, on=True):
+        """End-to-end mode (adaptra_exec_set_host_io): the inputs come from
+        pinned host memory every iteration (H2D inside the executor, overlapped
+        with the pipeline) and the loss goes back to pinned host memory.
+        Returns (h2d_bytes, d2h_bytes) per iteration on this rank."""
+        lib = L.lib()
+        self._host_in, self._host_loss = None, None
+        h2d = d2h = 0
+        if 0 in self.stages:
+            if on:
+                self._host_in = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in self.inputs]
+                for h, t in zip(self._host_in, self.inputs):
+                    h.copy_(t)
+                arr = (C.c_void_p * self.N)(*[h.data_ptr() for h in self._host_in])
+                self._keep.append(arr)
+                nbytes = self.inputs[0].numel() * self.inputs[0].element_size()
+                h2d = nbytes * self.N
+                L.check(lib.adaptra_exec_set_host_io(self.execs[0], arr, nbytes, None))
+            else:
+                L.check(lib.adaptra_exec_set_host_io(self.execs[0], None, 0, None))
+        if self.S - 1 in self.stages:
+            if on:
+                self._host_loss = torch.zeros(1, dtype=torch.float32, pin_memory=True)
+                d2h = 4
+            L.check(lib.adaptra_exec_set_host_io(self.execs[self.S - 1], None, 0,
+                                                 C.c_void_p(self._host_loss.data_ptr()) if on else None))
+        return h2d, d2h
+
+    def profile(self, k=5, quantum=1000):
+        """a1: per-stage (t^F, t^B, t^W) in ns = lower median over the last k
+        iterations of each stage's mean op time (adaptra_exec_profile, CUDA
+        events), floored to `quantum` ns; gathered over ranks.  Kinds that did
+        not run (W under 1F1B) report 0."""
+        lib = L.lib()
+        loc = {}
+        for i in self.local:
+            t = (C.c_int64 * 3)()
+            L.check(lib.adaptra_exec_profile(self.execs[i], k, quantum, t))
+            loc[i] = list(t)
+        allp = self._allgather(loc)
+        return ([allp[i][0] for i in range(self.S)], [allp[i][1] for i in range(self.S)],
+                [allp[i][2] for i in range(self.S)])
 
     def abort(self):
         """Release every GPU-side wait of this rank (after a failure)."""
@@ -330,58 +384,46 @@ def orders_from(X):
 
 
 class Arm:
-    """Schedule policy for one arm (R18 / R21)."""
+    """One schedule arm: marshalling around the C planner (adaptra_planner_*,
+    R18 / R21 / R26 in csrc/sched/sched.cpp).
 
-    def __init__(self, name, S, N, tF, tB, tW, *, x_init=None, ratio=30, x_cap=None):
-        # "<arm>-inorder": same order, executed with blocking sends/receives in
-        # the compute sequence (SURVEY N1: the HOL-blocking baseline)
+    name: "1f1b" | "zb" | "adaptive", optionally suffixed "-inorder" (the same
+    orders executed with blocking sends/receives in the compute sequence,
+    SURVEY N1: the HOL-blocking baseline).  mem = (M, M^F) selects Alg. 1 for
+    the adaptive arm's initial plan (R12), clamped to x_cap (R26)."""
+
+    def __init__(self, name, S, N, tF, tB, tW, *, x_init=None, ratio=30, x_cap=None, mem=None):
         self.inorder = name.endswith("-inorder")
         name = name[:-len("-inorder")] if self.inorder else name
         self.name, self.S, self.N = name, S, N
-        self.tF, self.tB, self.tW = list(tF), list(tB), list(tW)
-        self.delta = max(1, max(max(tF), max(tB), max(tW)) // ratio)
         self.merge_w = name == "1f1b"
-        self.x_cap = x_cap
-        zero = [0] * (S - 1)
-        if name == "1f1b":
-            x = [min(S - i, N) for i in range(S)]
-            X, _, _ = cs.schedule(S, N, tF, tB, tW, zero, x, self.delta, mode="cap", merge_w=True)
-        elif name == "zb":
-            x = cs.plan_adapt(S, N, tF, tB, zero)
-            X, _, _ = cs.schedule(S, N, tF, tB, tW, zero, x, self.delta)
-        elif name == "adaptive":
-            x = list(x_init) if x_init else cs.plan_adapt(S, N, tF, tB, zero)
-            self.x_init = list(x)
-            X, _, _ = cs.schedule(S, N, tF, tB, tW, zero, x, self.delta)
-        else:
-            raise ValueError(name)
-        self.x = x
-        self.orders = orders_from(X)
-        self.c = zero
-        self.replans = 0
+        self.planner = cs.Planner(name, S, N, tF, tB, tW, x_init=x_init if name == "adaptive" else None,
+                                  x_cap=x_cap if name == "adaptive" else None,
+                                  mem=mem if name == "adaptive" else None, ratio=ratio)
+        self.orders, self.x, _ = self.planner.step([0] * (S - 1))
+        self.x_init = list(self.x)
+        self.c = [0] * (S - 1)
+        self.last = {"c": list(self.c), "x": list(self.x), "replanned": False}
 
-    def _clamp(self, x):
-        if not self.x_cap:
-            return x
-        out = [min(v, cap) for v, cap in zip(x, self.x_cap)]
-        for i in range(len(out) - 2, -1, -1):          # keep the Lemma after clamping
-            out[i] = max(out[i], out[i + 1])
-        return out
+    @property
+    def replans(self):
+        return self.planner.info.replans
+
+    @property
+    def delta(self):
+        return self.planner.info.delta
+
+    def set_profile(self, tF, tB, tW):
+        """Adopted at the next re-plan (adaptra_planner_set_profile)."""
+        self.planner.set_profile(tF, tB, tW)
 
     def plan(self, c):
         """Orders for the next iteration given the link latencies c (ns, finite)."""
-        if self.name != "adaptive" or list(c) == list(self.c):
-            return self.orders
-        S, N = self.S, self.N
-        if all(v == 0 for v in c):
-            x = list(self.x_init)
-        elif not all(cs.eq1_holds(self.tF, self.tB, c, self.x)):
-            x = self._clamp(cs.plan_adapt(S, N, self.tF, self.tB, c))
-        else:
-            x = list(self.x)
-        X, _, _ = cs.schedule(S, N, self.tF, self.tB, self.tW, c, x, self.delta)
-        if x != self.x:
-            self.replans += 1
-        self.x, self.c = x, list(c)
-        self.orders = orders_from(X)
+        x_prev = list(self.x)
+        self.orders, self.x, replanned = self.planner.step(c)
+        self.c = list(c)
+        tF, tB, tW = self.planner.profile
+        self.last = {"c": list(c), "x_prev": x_prev, "x": list(self.x), "replanned": replanned,
+                     "tF": tF, "tB": tB, "tW": tW, "delta": self.planner.info.delta,
+                     "makespan": self.planner.info.makespan}
         return self.orders

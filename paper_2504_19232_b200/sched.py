@@ -86,13 +86,96 @@ def replay(S, N, tF, tB, tW, c, order, merge_w=False):
     return X, T.value
 
 
-def validate(S, N, tF, tB, tW, c, X, merge_w=False):
+def validate(S, N, tF, tB, tW, c, X, merge_w=False, cap=4096):
+    """adaptra_validate: [(code, stage, kind, mb)] with the codes of
+    L.V_CODES ("dep", "overlap", ...) and kinds "F"/"B"/"W"; [] = valid."""
     arr, n = _pack(S, N, X)
+    out = (L.Violation * cap)()
     v = C.c_int32()
     L.check(L.lib().adaptra_validate(S, N, _arr(C.c_int64, tF), _arr(C.c_int64, tB), _arr(C.c_int64, tW),
-                                     _arr(C.c_int64, list(c) or [0]), arr, n, _flags("paper", merge_w),
+                                     _arr(C.c_int64, list(c) or [0]), arr, n, _flags("paper", merge_w), out, cap,
                                      C.byref(v)))
-    return v.value
+    return [(L.V_CODES[o.code], o.stage, KIND.get(o.kind, o.kind), o.mb) for o in out[:min(cap, v.value)]]
+
+
+def validate_plan(S, N, x, cap=256):
+    out = (L.Violation * cap)()
+    v = C.c_int32()
+    L.check(L.lib().adaptra_validate_plan(S, N, _arr(C.c_int32, x), out, cap, C.byref(v)))
+    return [(L.V_CODES[o.code], o.stage) for o in out[:min(cap, v.value)]]
+
+
+def plan_1f1b(S, N):
+    x = (C.c_int32 * S)()
+    L.check(L.lib().adaptra_plan_1f1b(S, N, x))
+    return list(x)
+
+
+def clamp_plan(x, cap):
+    xs = _arr(C.c_int32, x)
+    L.check(L.lib().adaptra_clamp_plan(len(x), _arr(C.c_int32, cap), xs))
+    return list(xs)
+
+
+def default_delta(tF, tB, tW, ratio=30):
+    return L.lib().adaptra_default_delta(len(tF), _arr(C.c_int64, tF), _arr(C.c_int64, tB), _arr(C.c_int64, tW),
+                                         ratio)
+
+
+class Planner:
+    """adaptra_planner_*: one schedule arm (1F1B / ZB / adaptive, R18/R21/R26)."""
+
+    ARMS = {"1f1b": L.ARM_1F1B, "zb": L.ARM_ZB, "adaptive": L.ARM_ADAPTIVE}
+
+    def __init__(self, arm, S, N, tF, tB, tW, *, x_init=None, x_cap=None, mem=None, ratio=30):
+        d = L.PlannerDesc()
+        d.S, d.N, d.arm, d.ratio = S, N, self.ARMS[arm], ratio
+        self._keep = [_arr(C.c_int64, tF), _arr(C.c_int64, tB), _arr(C.c_int64, tW)]
+        d.tF, d.tB, d.tW = self._keep
+        if x_init is not None:
+            self._keep.append(_arr(C.c_int32, x_init))
+            d.x_init = self._keep[-1]
+        if x_cap is not None:
+            self._keep.append(_arr(C.c_int32, x_cap))
+            d.x_cap = self._keep[-1]
+        if mem is not None:
+            d.mem_capacity, d.mem_per_act = mem
+        self.S, self.N, self.arm = S, N, arm
+        self.h = C.c_void_p()
+        L.check(L.lib().adaptra_planner_create(C.byref(d), C.byref(self.h)))
+        self.info = L.PlanInfo()
+
+    def set_profile(self, tF, tB, tW):
+        L.check(L.lib().adaptra_planner_set_profile(self.h, _arr(C.c_int64, tF), _arr(C.c_int64, tB),
+                                                    _arr(C.c_int64, tW)))
+
+    def step(self, c):
+        """Returns (orders, x, replanned): orders[i] = [(kind, mb), ...]."""
+        S, per = self.S, 3 * self.N
+        ops = (L.Op * (S * per))()
+        n = (C.c_int32 * S)()
+        x = (C.c_int32 * S)()
+        r = C.c_int32()
+        L.check(L.lib().adaptra_planner_step(self.h, _arr(C.c_int64, list(c) or [0]), ops, n, x, C.byref(r),
+                                             C.byref(self.info)))
+        orders = [[(KIND[ops[i * per + q].kind], ops[i * per + q].mb) for q in range(n[i])] for i in range(S)]
+        return orders, list(x), bool(r.value)
+
+    @property
+    def profile(self):
+        S = self.S
+        return list(self.info.tF[:S]), list(self.info.tB[:S]), list(self.info.tW[:S])
+
+    def close(self):
+        if self.h:
+            L.lib().adaptra_planner_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def order_of(X):

@@ -121,3 +121,32 @@ def test_pipeline_full_size_c1_layers():
     finally:
         pipe.set_latency(0, 0)
         pipe.close()
+
+
+def test_host_io_end_to_end_matches_device_path():
+    """adaptra_exec_set_host_io: inputs uploaded from pinned host buffers by the
+    executor every iteration and the loss copied back to the host give the
+    same loss (bit for bit: fixed-order reduction) and gradients as the
+    device-resident run, and the profiler (adaptra_exec_profile, a1) reports
+    every kind's median op time."""
+    S, N = 2, 4
+    pipe, Lref, gref = _setup("gpt", L.BF16, S, N, 4, 256, 1024, 2, 1, 128)
+    try:
+        t = [1000] * S
+        a = Arm("zb", S, N, t, t, t)
+        orders = a.plan([0])
+        dev = pipe.run(orders).loss
+        h2d, d2h = pipe.set_host_io(True)   # pinned host copies of the inputs
+        for t_ in pipe.inputs:              # the device copies are rewritten by the uploads
+            t_.zero_()
+        torch.cuda.synchronize()
+        assert h2d == N * 128 * 256 * 2 and d2h == 4
+        for _ in range(3):
+            res = pipe.run(orders)
+        assert res.loss == dev
+        _check(pipe, res, Lref, gref, 2e-2)
+        tF, tB, tW = pipe.profile(k=3)
+        assert all(v >= 1000 and v % 1000 == 0 for v in tF + tB + tW)
+        pipe.set_host_io(False)
+    finally:
+        pipe.close()

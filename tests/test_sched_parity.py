@@ -70,7 +70,11 @@ def test_random_parity(spec):
         Xc, Tc, s_c = cs.schedule(S, N, tF, tB, tW, c, x, delta, mode=mode, merge_w=merge)
         assert (To, so) == (Tc, s_c)
         assert _ox(Xo) == Xc
-        assert cs.validate(S, N, tF, tB, tW, c, Xc, merge) == 0
+        assert cs.validate(S, N, tF, tB, tW, c, Xc, merge) == []
+        # under other latencies the same timing is invalid in the same places on both sides
+        c3 = [v + 3 for v in c]
+        assert sorted(cs.validate(S, N, tF, tB, tW, c3, Xc, merge)) == sorted(
+            sc.violations(S, N, tF, tB, tW, c3, Xo, merge))
         # replay under other latencies
         c2 = [v * 3 + 5 for v in c]
         Ro, RTo = sc.replay(S, N, tF, tB, tW, c2, sc.order_of(Xo), merge_w=merge)
@@ -94,7 +98,81 @@ def test_errors():
     bad = [list(s) for s in X]
     k, m, s0, e0 = bad[1][0]
     bad[1][0] = (k, m, s0 - 5, e0 - 5)
-    assert cs.validate(4, 12, t, t, t, [0, 0, 0], bad) > 0
+    assert ("dep", 1, "F", 1) in cs.validate(4, 12, t, t, t, [0, 0, 0], bad)
+
+
+def _mutants():
+    t = [10] * 4
+    X, _, _ = sc.schedule(4, 12, t, t, t, [0, 0, 0], [7, 5, 3, 1], 1)
+    base = [[(o.kind, o.mb, o.start, o.end) for o in ops] for ops in X]
+    out = []
+    m = [list(s) for s in base]; m[1][-1] = m[1][4][:2] + (m[1][-1][2], m[1][-1][3]); out.append(m)  # dup + missing
+    m = [list(s) for s in base]; m[3].pop(); out.append(m)
+    m = [list(s) for s in base]; k, j, a, b = m[2][-1]; m[2][-1] = (k, j, a, b + 1); out.append(m)
+    m = [list(s) for s in base]; k, j, a, b = m[0][1]; m[0][1] = (k, j, a - 1, b - 1); out.append(m)
+    m = [list(s) for s in base]; m[1][-1] = ("F", 13) + m[1][-1][2:]; out.append(m)
+    m = [list(s) for s in base]; m[2] = m[2][::-1]; out.append(m)
+    return out
+
+
+@pytest.mark.parametrize("k", range(6))
+def test_validate_violation_lists_match_oracle(k):
+    """adaptra_validate returns the same violation list (as a multiset) as
+    oracle.sched.violations on mutated copies of the ideal ZB schedule."""
+    t = [10] * 4
+    m = _mutants()[k]
+    for c in ([0, 0, 0], [1, 0, 2]):
+        got = cs.validate(4, 12, t, t, t, c, m)
+        ref = sc.violations(4, 12, t, t, t, c, [[sc.Op(*o) for o in ops] for ops in m])
+        assert got and sorted(got) == sorted(ref)
+    # capacity: the total is reported even when the list is cut
+    assert len(cs.validate(4, 12, t, t, t, [0, 0, 0], m, cap=1)) == 1
+
+
+def test_validate_plan_matches_oracle():
+    for N, x in ((12, [7, 5, 3, 1]), (12, [3, 4, 1]), (12, [5, 3, 3, 4]), (4, [5, 3, 1]), (12, [3, 2, 0]),
+                 (2, [1, 3, 0])):
+        assert sorted(cs.validate_plan(len(x), N, x)) == sorted(sc.plan_violations(N, x))
+
+
+@st.composite
+def arm_specs(draw):
+    S = draw(st.integers(2, 8))
+    N = draw(st.integers(1, 40))
+    seed = draw(st.integers(0, 10 ** 9))
+    tF, tB, tW, _ = sy.stage_profile(seed, S, 1, 60)
+    cs_seq = []
+    for k in range(draw(st.integers(1, 8))):
+        c_hi = draw(st.sampled_from([0, 0, 10, 60, 300]))
+        cs_seq.append(sy.stage_profile(seed + k + 1, S, 1, 2, c_hi)[3])
+    cap = draw(st.sampled_from([None, 3, 8]))
+    x_cap = None if cap is None else [max(1, cap - i // 2) for i in range(S)]
+    return S, N, tF, tB, tW, cs_seq, x_cap, draw(st.sampled_from([10, 30]))
+
+
+@settings(max_examples=150, deadline=None)
+@given(arm_specs())
+def test_planner_arms_match_oracle(spec):
+    """adaptra_planner (R18 / R21 / R26 in C) == the oracle's baselines and
+    adaptive_orders, iteration by iteration: plan and per-stage order."""
+    S, N, tF, tB, tW, cs_seq, x_cap, ratio = spec
+    zero = [0] * (S - 1)
+    d = sc.default_delta(tF, tB, tW, ratio)
+    assert cs.default_delta(tF, tB, tW, ratio) == d
+    X1, _, _ = sc.schedule_1f1b(S, N, tF, tB, tW, d)
+    Xz, _, _ = sc.schedule(S, N, tF, tB, tW, zero, sc.get_adapted_warmup_fwds(S, N, tF, tB, zero), d)
+    for name, ref in (("1f1b", sc.order_of(X1)), ("zb", sc.order_of(Xz))):
+        p = cs.Planner(name, S, N, tF, tB, tW, ratio=ratio)
+        for c in cs_seq:                      # frozen: the latencies change nothing
+            assert p.step(c)[0] == ref
+    x_init = sc.get_init_warmup_fwds(S, 40, 1, N)
+    if x_cap:
+        x_init = sc.clamp_plan(x_init, x_cap)
+    ref = sc.adaptive_orders(S, N, tF, tB, tW, cs_seq, x_init, x_cap, ratio)
+    p = cs.Planner("adaptive", S, N, tF, tB, tW, x_cap=x_cap, mem=(40, 1), ratio=ratio)
+    for (x_ref, order_ref), c in zip(ref, cs_seq):
+        orders, x, _ = p.step(c)
+        assert (x, orders) == (x_ref, order_ref)
 
 
 def test_generation_latency_under_100ms():
