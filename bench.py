@@ -250,6 +250,10 @@ def main():
 
     events = sy.PAPER_TRACE
     arms = [a for a in args.arms.split(",") if a]
+    if S == world and world > 1 and not any(a.endswith("-nccl") for a in arms):
+        arms.append("zb-nccl")     # N1: the NCCL baseline needs one stage per GPU
+    if any(a.endswith("-nccl") for a in arms):
+        pipe.enable_nccl(host_c)
     results = {}
     lib = L.lib()
     timer = torch.cuda.Stream(device=local_rank)
@@ -278,7 +282,7 @@ def main():
                 e["step"] = k
                 e["orders"] = [" ".join(f"{kd}{mb}" for kd, mb in o) for o in orders]
                 replan_log.append(e)
-            res = pipe.run(orders, merge_w=arm.merge_w, want_times=True, inorder=arm.inorder)
+            res = pipe.run(orders, merge_w=arm.merge_w, want_times=True, inorder=arm.inorder, nccl=arm.nccl)
             if arm.name == "adaptive":
                 # a1: the profiler tracks op times continuously; the planner adopts
                 # the latest medians at its next re-plan

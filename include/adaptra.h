@@ -480,11 +480,38 @@ typedef struct adaptra_iter_stats {
 int adaptra_exec_create(const adaptra_exec_desc_t* d, adaptra_exec_t* out);
 int adaptra_exec_destroy(adaptra_exec_t e);
 /* Post one iteration: ops[n] (kind, mb) in order; flags: ADAPTRA_MERGE_W runs W
- * right after each B (1F1B); ADAPTRA_EXEC_INORDER makes every receive and every
- * send block the stage thread (the sequential-launch baseline that exhibits
- * head-of-line blocking).  Non-blocking (the stage thread enqueues). */
+ * right after each B (1F1B); ADAPTRA_EXEC_INORDER is the sequential-launch
+ * baseline that exhibits head-of-line blocking: every receive
+ * blocks the stage thread until its message is there, and a send blocks it
+ * while more than Q of the outbox's messages are undelivered (the
+ * transmission queue is full; Q = $ADAPTRA_INORDER_QUEUE,
+ * default 2; 0 = rendezvous, every send waits for its delivery + c).
+ * Non-blocking (the stage thread enqueues). */
 #define ADAPTRA_EXEC_INORDER 16u
 int adaptra_run_iteration(adaptra_exec_t e, const adaptra_op_t* ops, int32_t n, uint32_t epoch, uint32_t flags);
+/* ---------------------------------------------------------------- NCCL baseline (N1)
+ * north_star: "NCCL send/recv is used only as the baseline".  With
+ * ADAPTRA_EXEC_NCCL the executor runs the fixed execution plan of
+ * Megatron-style runtimes: per op, in order on the compute
+ * stream, the previous op's send grouped with this op's receive
+ * (ncclSend/ncclRecv inside ncclGroupStart/End), then the op's kernels; an
+ * injected latency c (adaptra_set_link_latency on the outbox) holds the compute
+ * stream for c before the send -- a slow transfer blocks everything queued
+ * behind it (head-of-line blocking).  A failed link costs
+ * `down_ns` (the measured delegated-path time) instead.  Outputs go to the
+ * sender's staging slots, inputs land in the receiver's mailbox slots; the
+ * epoch flags are not used.  One communicator over all ranks (one stage per
+ * GPU: NCCL refuses two ranks on one device). */
+#define ADAPTRA_NCCL_ID_BYTES 128
+#define ADAPTRA_EXEC_NCCL 32u
+/* ncclGetUniqueId into id_out[128] (rank 0; broadcast it to the others). */
+int adaptra_nccl_unique_id(uint8_t* id_out);
+/* ncclCommInitRank on device dev; *comm_out is an ncclComm_t. */
+int adaptra_nccl_comm_init(const uint8_t* id, int32_t nranks, int32_t rank, int32_t dev, void** comm_out);
+int adaptra_nccl_comm_destroy(void* comm);
+/* Communicator and the NCCL ranks of stages i-1 / i+1 (-1 if none). */
+int adaptra_exec_set_nccl(adaptra_exec_t e, void* comm, int32_t rank_prev, int32_t rank_next, int64_t down_ns);
+
 /* End-to-end host I/O (NULL disables): on stage 0, host_inputs[n_mb] are pinned
  * host buffers of `bytes` each; every iteration copies them into the device
  * inputs of the exec desc (H2D on a side stream, issued in the order stage 0

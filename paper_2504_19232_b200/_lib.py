@@ -18,6 +18,8 @@ EINVAL, EPLAN, EDEADLOCK, ECUDA, ENOMEM, ELINK, ETOOBIG = -1, -2, -3, -4, -5, -6
 OP_F, OP_B, OP_W = 0, 1, 2
 SEL_PAPER, SEL_CAP, MERGE_W = 0, 1, 2
 EXEC_INORDER = 16
+EXEC_NCCL = 32
+NCCL_ID_BYTES = 128
 F32, BF16 = 0, 1
 BLOCK_MLP, BLOCK_GPT = 0, 1
 
@@ -162,6 +164,10 @@ _SIGS = {
     "adaptra_run_iteration": (_i32, [_vp, _P(Op), _i32, _u32, _u32]),
     "adaptra_exec_set_time_base": (_i32, [_vp, _vp]),
     "adaptra_exec_set_host_io": (_i32, [_vp, _P(_vp), _i64, _vp]),
+    "adaptra_exec_set_nccl": (_i32, [_vp, _vp, _i32, _i32, _i64]),
+    "adaptra_nccl_unique_id": (_i32, [_P(C.c_uint8)]),
+    "adaptra_nccl_comm_init": (_i32, [_P(C.c_uint8), _i32, _i32, _i32, _P(_vp)]),
+    "adaptra_nccl_comm_destroy": (_i32, [_vp]),
     "adaptra_exec_join": (_i32, [_vp]),
     "adaptra_exec_wait": (_i32, [_vp, _P(IterStats), _P(_i64)]),
     "adaptra_exec_profile": (_i32, [_vp, _i32, _i64, _P(_i64)]),

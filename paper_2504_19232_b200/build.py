@@ -73,7 +73,7 @@ def build(force=False, verbose=False, jobs=None):
     objs = [_obj(s) for s in srcs]
     if todo or not os.path.exists(LIB):
         cmd = [NVCC] + ARCH + ["-shared", "-cudart", "shared", "-o", LIB] + objs + [
-            "-Xlinker", "-rpath=/usr/local/cuda/lib64", "-lpthread"]
+            "-Xlinker", "-rpath=/usr/local/cuda/lib64", "-lpthread", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

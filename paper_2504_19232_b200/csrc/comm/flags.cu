@@ -69,6 +69,23 @@ int host_wait_hmem(const volatile uint32_t* p, uint32_t v) {
   return ADAPTRA_OK;
 }
 
+// Holds a stream for `ns` nanoseconds of GPU time (one thread): the injected
+// link latency of the NCCL baseline arm, where the transfer occupies the
+// compute stream in op order.
+__global__ void spin_ns_kernel(int64_t ns) {
+  const uint64_t t0 = globaltimer();
+  while ((int64_t)(globaltimer() - t0) < ns) __nanosleep(1000);
+}
+
+int stream_spin(cudaStream_t st, int64_t ns) {
+  if (ns <= 0) return ADAPTRA_OK;
+  spin_ns_kernel<<<1, 1, 0, st>>>(ns);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(ADAPTRA_ECUDA, std::string("spin launch: ") + cudaGetErrorString(e));
+  return ADAPTRA_OK;
+}
+
 int stream_write(cudaStream_t st, uint32_t* addr, uint32_t v) {
   signal_flag_kernel<<<1, 1, 0, st>>>(addr, v);
   count_launch();

@@ -464,10 +464,28 @@ extern "C" int adaptra_inbox_set_host(adaptra_inbox_t ib, int32_t on) {
 }
 
 // ================================================================ outbox
+// Sender-side staging slots: the producing op writes here when the data does
+// not go straight into the peer mailbox (P2P copy kernel, HOST path).  DIRECT
+// outboxes only need them once the link fails over to the host path, so they
+// are allocated then (adaptra_set_link_latency(LINK_DOWN)), not up front.
+static int ensure_staging(adaptra_outbox* ob) {
+  if (ob->staging) return ADAPTRA_OK;
+  cudaSetDevice(ob->dev);
+  if (cudaMalloc(&ob->staging, (size_t)ob->n_mb * ob->bytes) != cudaSuccess) {
+    cudaGetLastError();
+    ob->staging = nullptr;
+    return set_error(ADAPTRA_ENOMEM, "outbox: staging cudaMalloc failed");
+  }
+  return ADAPTRA_OK;
+}
+
 static int outbox_common(adaptra_outbox* ob) {
   cudaSetDevice(ob->dev);
   ADAPTRA_CUDA_TRY(cudaStreamCreateWithFlags(&ob->lstream, cudaStreamNonBlocking));
-  ADAPTRA_CUDA_TRY(cudaMalloc(&ob->staging, (size_t)ob->n_mb * ob->bytes));
+  if (ob->mode != ADAPTRA_LINK_DIRECT) {
+    int rc = ensure_staging(ob);
+    if (rc) return rc;
+  }
   ob->ev_prod.resize(ob->n_mb);
   ob->ev_moved.resize(ob->n_mb);
   for (int k = 0; k < ob->n_mb; ++k) {
@@ -565,7 +583,7 @@ extern "C" int adaptra_outbox_close(adaptra_outbox_t ob) {
   for (auto e : ob->ev_prod) cudaEventDestroy(e);
   for (auto e : ob->ev_moved) cudaEventDestroy(e);
   cudaStreamDestroy(ob->lstream);
-  cudaFree(ob->staging);
+  if (ob->staging) cudaFree(ob->staging);
   if (ob->ipc) {
     cudaIpcCloseMemHandle(ob->peer_mbox);
     flags_close(ob->fl_map);
@@ -586,6 +604,10 @@ extern "C" void* adaptra_outbox_dst(adaptra_outbox_t ob, int32_t mb) {
 extern "C" int adaptra_set_link_latency(adaptra_outbox_t ob, int64_t ns) {
   if (!ob || ns < 0) return set_error(ADAPTRA_EINVAL, "set_link_latency: bad args");
   if (ns == ADAPTRA_LINK_DOWN && !ob->has_ring) return set_error(ADAPTRA_ELINK, "link down but no host ring");
+  if (ns == ADAPTRA_LINK_DOWN) {
+    int rc = ensure_staging(ob);
+    if (rc) return rc;
+  }
   ob->latency.store(ns);
   return ADAPTRA_OK;
 }
@@ -688,3 +710,12 @@ extern "C" int adaptra_link_stats_take(adaptra_outbox_t ob, int64_t* n, int64_t*
   if (mx) *mx = m;
   return ADAPTRA_OK;
 }
+
+namespace adaptra {
+int64_t outbox_latency(adaptra_outbox_t ob) { return ob ? ob->latency.load() : 0; }
+int64_t outbox_bytes(adaptra_outbox_t ob) { return ob ? ob->bytes : 0; }
+void* outbox_local_slot(adaptra_outbox_t ob, int mb) {
+  if (!ob || mb < 0 || mb >= ob->n_mb || ensure_staging(ob)) return nullptr;
+  return (char*)ob->staging + (size_t)mb * ob->bytes;
+}
+}  // namespace adaptra

@@ -69,12 +69,137 @@ struct adaptra_exec {
   float* host_loss = nullptr;
   cudaStream_t h2d = nullptr;
   std::vector<cudaEvent_t> ev_in;
+  // NCCL baseline arm (N1): communicator and the peers' ranks
+  void* nccl = nullptr;
+  int nccl_prev = -1, nccl_next = -1;
+  int64_t nccl_down_ns = 0;
+
+  // ADAPTRA_EXEC_NCCL: the fixed execution plan of Megatron-style runtimes
+  // (P:1801-1813).  Per op, in order on the compute stream: the send of the
+  // previous op's output grouped with the receive of this op's input
+  // (ncclGroupStart/End, as send_forward_recv_backward pairs them), then the
+  // op's kernels.  An injected latency c holds the stream for c before the
+  // send (the transfer occupies the in-order stream); a failed
+  // link costs its measured delegated-path time instead (baselines have no
+  // delegation, so this is generous to them).
+  int run_nccl(std::vector<int>& free_slots) {
+    const int S = d.n_stages, i = d.stage_index, N = d.n_microbatches;
+    const bool merge = flags & ADAPTRA_MERGE_W;
+    int rc;
+    const void* p_buf = nullptr;
+    int64_t p_bytes = 0, p_lat = 0;
+    int p_peer = -1;
+    auto flush = [&](void* r_buf, int64_t r_bytes, int r_peer) -> int {
+      if (!p_buf && !r_buf) return ADAPTRA_OK;
+      if (p_buf && p_lat > 0) {
+        int r = stream_spin(cs, p_lat);
+        if (r) return r;
+      }
+      int r = nccl_p2p(nccl, p_buf, p_bytes, p_peer, r_buf, r_bytes, r_peer, cs);
+      p_buf = nullptr;
+      return r;
+    };
+    auto lat_of = [&](adaptra_outbox_t ob) {
+      int64_t l = outbox_latency(ob);
+      return l == ADAPTRA_LINK_DOWN ? nccl_down_ns : l;
+    };
+    for (size_t q = 0; q < ops.size(); ++q) {
+      const adaptra_op_t& o = ops[q];
+      const int mb = o.mb;
+      if (mb < 1 || mb > N) return set_error(ADAPTRA_EINVAL, "exec: bad microbatch");
+      if (o.kind == ADAPTRA_OP_F) {
+        if (free_slots.empty()) return set_error(ADAPTRA_ENOMEM, "exec: stash slots exhausted (plan needs more)");
+        int slot = free_slots.back();
+        free_slots.pop_back();
+        slot_of_mb[mb] = slot;
+        const void* x = nullptr;
+        if (i == 0) {
+          x = d.inputs[mb - 1];
+          if (host_inputs) ADAPTRA_CUDA_TRY(cudaStreamWaitEvent(cs, ev_in[mb - 1], 0));
+          if ((rc = flush(nullptr, 0, -1))) return rc;
+        } else {
+          void* p = adaptra_inbox_slot(d.in_fwd, mb - 1);
+          if ((rc = flush(p, outbox_bytes(d.out_bwd), nccl_prev))) return rc;
+          x = p;
+        }
+        void* y = (i < S - 1) ? outbox_local_slot(d.out_fwd, mb - 1) : nullptr;
+        if (i < S - 1 && !y) return set_error(ADAPTRA_ENOMEM, "exec: no send buffer");
+        ADAPTRA_CUDA_TRY(cudaEventRecord(ev_s[q], cs));
+        if ((rc = adaptra_stage_F(d.stage, slot, x, y, i == S - 1 ? d.targets[mb - 1] : nullptr,
+                                  i == S - 1 ? d.loss_acc : nullptr, cs)))
+          return rc;
+        ADAPTRA_CUDA_TRY(cudaEventRecord(ev_e[q], cs));
+        if (i < S - 1) {
+          p_buf = y;
+          p_bytes = outbox_bytes(d.out_fwd);
+          p_peer = nccl_next;
+          p_lat = lat_of(d.out_fwd);
+        }
+      } else if (o.kind == ADAPTRA_OP_B) {
+        int slot = slot_of_mb[mb];
+        if (slot < 0) return set_error(ADAPTRA_EINVAL, "exec: B before F");
+        void* dy = nullptr;
+        if (i < S - 1) {
+          dy = adaptra_inbox_slot(d.in_bwd, mb - 1);
+          if ((rc = flush(dy, outbox_bytes(d.out_fwd), nccl_next))) return rc;
+        } else if ((rc = flush(nullptr, 0, -1))) {
+          return rc;
+        }
+        void* dx = (i > 0) ? outbox_local_slot(d.out_bwd, mb - 1) : nullptr;
+        if (i > 0 && !dx) return set_error(ADAPTRA_ENOMEM, "exec: no send buffer");
+        ADAPTRA_CUDA_TRY(cudaEventRecord(ev_s[q], cs));
+        if ((rc = adaptra_stage_B(d.stage, slot, dy, dx, cs))) return rc;
+        if (merge) {
+          if ((rc = adaptra_stage_W(d.stage, slot, cs))) return rc;
+          free_slots.push_back(slot);
+          slot_of_mb[mb] = -1;
+        }
+        ADAPTRA_CUDA_TRY(cudaEventRecord(ev_e[q], cs));
+        if (i > 0) {
+          p_buf = dx;
+          p_bytes = outbox_bytes(d.out_bwd);
+          p_peer = nccl_prev;
+          p_lat = lat_of(d.out_bwd);
+        }
+      } else if (o.kind == ADAPTRA_OP_W) {
+        int slot = slot_of_mb[mb];
+        if (slot < 0) return set_error(ADAPTRA_EINVAL, "exec: W before F");
+        if ((rc = flush(nullptr, 0, -1))) return rc;
+        ADAPTRA_CUDA_TRY(cudaEventRecord(ev_s[q], cs));
+        if ((rc = adaptra_stage_W(d.stage, slot, cs))) return rc;
+        ADAPTRA_CUDA_TRY(cudaEventRecord(ev_e[q], cs));
+        free_slots.push_back(slot);
+        slot_of_mb[mb] = -1;
+      } else {
+        return set_error(ADAPTRA_EINVAL, "exec: bad op kind");
+      }
+    }
+    return flush(nullptr, 0, -1);
+  }
 
   int run_one() {
     cudaSetDevice(dev);
     const int S = d.n_stages, i = d.stage_index, N = d.n_microbatches;
     const bool merge = flags & ADAPTRA_MERGE_W;
     const bool inorder = flags & ADAPTRA_EXEC_INORDER;
+    // In-order baseline (N1): a send blocks the stage thread only
+    // while more than Q of this outbox's messages are still undelivered (the
+    // transmission queue is full); Q = $ADAPTRA_INORDER_QUEUE (default 2;
+    // 0 = synchronous rendezvous, every send waits for its delivery)
+    static const int qdepth = [] {
+      const char* v = getenv("ADAPTRA_INORDER_QUEUE");
+      return v ? std::max(0, atoi(v)) : 2;
+    }();
+    std::deque<std::pair<int, uint32_t>> q_fwd, q_bwd;
+    auto send_q = [&](adaptra_outbox_t ob, std::deque<std::pair<int, uint32_t>>& qu, int m) -> int {
+      qu.emplace_back(m, epoch);
+      while ((int)qu.size() > qdepth) {
+        int r = adaptra_send_wait(ob, qu.front().first, qu.front().second);
+        if (r) return r;
+        qu.pop_front();
+      }
+      return ADAPTRA_OK;
+    };
     const int64_t t_start = now_ns();
     std::vector<int> free_slots;
     for (int k = stage_n_slots(d.stage) - 1; k >= 0; --k) free_slots.push_back(k);
@@ -95,6 +220,14 @@ struct adaptra_exec {
     DBG("start epoch %u n_ops %zu", epoch, ops.size());
     if ((rc = adaptra_stage_zero_grads(d.stage, cs))) return rc;  // gradients of this iteration only
     DBG("zeroed");
+    if (flags & ADAPTRA_EXEC_NCCL) {
+      if (!nccl) return set_error(ADAPTRA_EINVAL, "exec: NCCL arm without a communicator (adaptra_exec_set_nccl)");
+      if ((rc = run_nccl(free_slots))) return rc;
+      if (i == S - 1 && host_loss && d.loss_acc)
+        ADAPTRA_CUDA_TRY(cudaMemcpyAsync(host_loss, d.loss_acc, sizeof(float), cudaMemcpyDeviceToHost, cs));
+      host_ns = now_ns() - t_start;
+      return ADAPTRA_OK;
+    }
     static const int lookahead = [] {
       const char* v = getenv("ADAPTRA_LOOKAHEAD");
       return v ? atoi(v) : 3;
@@ -136,7 +269,7 @@ struct adaptra_exec {
         DBG("  F launched");
         ADAPTRA_CUDA_TRY(cudaEventRecord(ev_e[q], cs));
         if (i < S - 1 && (rc = adaptra_send(d.out_fwd, mb - 1, cs, epoch))) return rc;
-        if (inorder && i < S - 1 && (rc = adaptra_send_wait(d.out_fwd, mb - 1, epoch))) return rc;
+        if (inorder && i < S - 1 && (rc = send_q(d.out_fwd, q_fwd, mb - 1))) return rc;
       } else if (o.kind == ADAPTRA_OP_B) {
         int slot = slot_of_mb[mb];
         if (slot < 0) return set_error(ADAPTRA_EINVAL, "exec: B before F");
@@ -156,7 +289,7 @@ struct adaptra_exec {
         }
         ADAPTRA_CUDA_TRY(cudaEventRecord(ev_e[q], cs));
         if (i > 0 && (rc = adaptra_send(d.out_bwd, mb - 1, cs, epoch))) return rc;
-        if (inorder && i > 0 && (rc = adaptra_send_wait(d.out_bwd, mb - 1, epoch))) return rc;
+        if (inorder && i > 0 && (rc = send_q(d.out_bwd, q_bwd, mb - 1))) return rc;
       } else if (o.kind == ADAPTRA_OP_W) {
         int slot = slot_of_mb[mb];
         if (slot < 0) return set_error(ADAPTRA_EINVAL, "exec: W before F");
@@ -271,6 +404,18 @@ extern "C" int adaptra_exec_set_host_io(adaptra_exec_t e, const void* const* hos
   e->host_inputs = host_inputs;
   e->host_in_bytes = bytes;
   e->host_loss = host_loss;
+  return ADAPTRA_OK;
+}
+
+extern "C" int adaptra_exec_set_nccl(adaptra_exec_t e, void* comm, int32_t rank_prev, int32_t rank_next,
+                                     int64_t down_ns) {
+  if (!e) return set_error(ADAPTRA_EINVAL, "exec_set_nccl: null");
+  std::unique_lock<std::mutex> lk(e->mu);
+  if (e->busy) return set_error(ADAPTRA_EINVAL, "exec_set_nccl: iteration running");
+  e->nccl = comm;
+  e->nccl_prev = rank_prev;
+  e->nccl_next = rank_next;
+  e->nccl_down_ns = down_ns;
   return ADAPTRA_OK;
 }
 

@@ -244,7 +244,29 @@ class Pipeline:
         if link in self.in_bwd:
             L.check(lib.adaptra_inbox_set_host(self.in_bwd[link], down))
 
-    def run(self, orders, merge_w=False, want_times=False, inorder=False):
+    def enable_nccl(self, down_ns=0):
+        """N1 baseline: one NCCL communicator over all ranks for the
+        ADAPTRA_EXEC_NCCL arms (one stage per rank: NCCL refuses two ranks on a
+        device, and one communicator must not be driven by two stage threads)."""
+        if getattr(self, "_nccl", None):
+            return
+        if len(self.local) != 1 or self.S != self.world:
+            raise ValueError("the NCCL baseline needs exactly one stage per rank (S == world)")
+        lib = L.lib()
+        uid = (C.c_uint8 * L.NCCL_ID_BYTES)()
+        if self.rank == 0:
+            L.check(lib.adaptra_nccl_unique_id(uid))
+        raw = self._bcast(bytes(uid))
+        uid = (C.c_uint8 * L.NCCL_ID_BYTES)(*raw)
+        comm = C.c_void_p()
+        L.check(lib.adaptra_nccl_comm_init(uid, self.world, self.rank, self.dev, C.byref(comm)))
+        self._nccl = comm
+        i = self.local[0]
+        prev = self.stage_rank[i - 1] if i > 0 else -1
+        nxt = self.stage_rank[i + 1] if i < self.S - 1 else -1
+        L.check(lib.adaptra_exec_set_nccl(self.execs[i], comm, prev, nxt, int(down_ns)))
+
+    def run(self, orders, merge_w=False, want_times=False, inorder=False, nccl=False):
         """One iteration.  orders[i] = [(kind, mb), ...] for every stage i (only
         local stages are executed here).  Returns IterResult with local stats."""
         lib = L.lib()
@@ -255,7 +277,7 @@ class Pipeline:
         # rank has finished the previous one (write-after-read across ranks).
         self._barrier()
         self.epoch += 1
-        flags = (L.MERGE_W if merge_w else 0) | (L.EXEC_INORDER if inorder else 0)
+        flags = (L.MERGE_W if merge_w else 0) | (L.EXEC_INORDER if inorder else 0) | (L.EXEC_NCCL if nccl else 0)
         self._base_event.record(self._base_stream)
         keep = []
         for i in self.local:
@@ -366,6 +388,9 @@ class Pipeline:
         for h in self.execs.values():
             lib.adaptra_exec_destroy(h)
         self.execs = {}
+        if getattr(self, "_nccl", None):
+            lib.adaptra_nccl_comm_destroy(self._nccl)
+            self._nccl = None
         torch.cuda.synchronize(self.dev)
         for h in list(self.out_fwd.values()) + list(self.out_bwd.values()):
             lib.adaptra_outbox_close(h)
@@ -394,7 +419,9 @@ class Arm:
 
     def __init__(self, name, S, N, tF, tB, tW, *, x_init=None, ratio=30, x_cap=None, mem=None):
         self.inorder = name.endswith("-inorder")
+        self.nccl = name.endswith("-nccl")       # N1: NCCL send/recv in the compute sequence
         name = name[:-len("-inorder")] if self.inorder else name
+        name = name[:-len("-nccl")] if self.nccl else name
         self.name, self.S, self.N = name, S, N
         self.merge_w = name == "1f1b"
         self.planner = cs.Planner(name, S, N, tF, tB, tW, x_init=x_init if name == "adaptive" else None,

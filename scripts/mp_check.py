@@ -21,7 +21,10 @@ from paper_2504_19232_b200.pipeline import Arm, ModelCfg, Pipeline  # noqa: E402
 def main():
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    # with fewer GPUs than ranks, ranks share devices (rank r on GPU r % n):
+    # two processes on one GPU still exercise CUDA-IPC mailboxes, the shm
+    # flags and the cross-process host ring (the 1-GPU driver box runs this)
+    local = int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
     grp = dist.new_group(backend="gloo")
@@ -62,6 +65,44 @@ def main():
         print(f"rank {rank} arm {arm_name} lat {lat}: worst grad err {worst:.2e} loss err {lerr:.2e} "
               f"{'OK' if good else 'FAIL'}", flush=True)
     pipe.close()
+    # N1 baseline: NCCL send/recv in the compute sequence, one stage per rank
+    # (needs distinct GPUs: NCCL refuses two ranks on one device)
+    if torch.cuda.device_count() >= world and os.environ.get("NCCL_ARMS", "1") == "1":
+        S2 = world
+        params = sy.gpt_params(0, S2, 1, d, dff, perturb=True, bf16=True)
+        pipe = Pipeline(m.__class__(block="gpt", n_layers=S2, d=d, d_ff=dff, n_heads=H, b=1, T=T, dtype=L.BF16),
+                        S2, N, params=params, inputs=xs, targets=tg, rank=rank, world=world, device=local,
+                        group=grp, link_mode=mode)
+        pipe.enable_nccl(500_000)
+        Lref, gref, _ = nu.full_batch("gpt", params, xs, tg, H)
+        t = [1000] * S2
+        for arm_name, lat in (("zb-nccl", None), ("1f1b-nccl", None), ("zb-nccl", (0, 2_000_000)),
+                              ("adaptive-nccl", (0, L.LINK_DOWN))):
+            a = Arm(arm_name, S2, N, t, t, t)
+            for l in range(S2 - 1):
+                pipe.set_latency(l, 0)
+            c = [0] * (S2 - 1)
+            if lat:
+                pipe.set_latency(lat[0], lat[1])
+                c[lat[0]] = lat[1] if lat[1] != L.LINK_DOWN else 500_000
+            t0 = __import__("time").perf_counter()
+            res = pipe.run(a.plan(c), merge_w=a.merge_w, nccl=a.nccl)
+            wall = __import__("time").perf_counter() - t0
+            worst = 0.0
+            for i, st in pipe.stages.items():
+                got = st.grads()
+                for l in range(len(got)):
+                    for k, ref in gref[i][l].items():
+                        e = float(np.abs(got[l][k] - ref).max() / max(np.abs(ref).max(), 1e-30))
+                        worst = max(worst, e)
+            lerr = abs(res.loss - Lref) / abs(Lref) if res.loss is not None else 0.0
+            # an injected 2 ms per message holds the in-order stream: N messages each way
+            slow_ok = lat is None or lat[1] == L.LINK_DOWN or wall >= N * 2e-3
+            good = worst < 2e-2 and lerr < 2e-2 and slow_ok
+            ok &= good
+            print(f"rank {rank} arm {arm_name} lat {lat}: worst grad err {worst:.2e} loss err {lerr:.2e} "
+                  f"wall {wall * 1e3:.1f} ms {'OK' if good else 'FAIL'}", flush=True)
+        pipe.close()
     dist.destroy_process_group()
     sys.exit(0 if ok else 1)
 
