@@ -276,6 +276,8 @@ def main():
                 want = L.LINK_DOWN if l in down else c[l]
                 if pipe.latency[l] != want:
                     pipe.set_latency(l, want)
+                # delegation policy arm: straggling links move to the host path
+                pipe.set_path(l, arm.deleg and c[l] > 0 and l not in down)
             orders = arm.plan(c)
             if log and rank == 0:
                 e = dict(arm.last)

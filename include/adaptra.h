@@ -419,6 +419,15 @@ int adaptra_outbox_close(adaptra_outbox_t ob);
 void* adaptra_outbox_dst(adaptra_outbox_t ob, int32_t mb);
 /* Injected latency in ns (>= 0), or ADAPTRA_LINK_DOWN (delegated host path). */
 int adaptra_set_link_latency(adaptra_outbox_t ob, int64_t latency_ns);
+/* Delegation policy ("the delegated communication path is
+ * activated only upon the detection of communication delays"): PATH_HOST sends
+ * this outbox's messages over the delegated host path while the link is up
+ * (its injected latency still applies: the slow network is on both paths);
+ * PATH_GPU (default) uses the link's mode.  The receiving inbox must be told
+ * with adaptra_inbox_set_host.  Set between iterations. */
+#define ADAPTRA_PATH_GPU 0
+#define ADAPTRA_PATH_HOST 1
+int adaptra_link_set_path(adaptra_outbox_t ob, int32_t path);
 /* The P2P link mode's transfer kernel (P:1575-1577 inter-stage activations /
  * gradients): copies `bytes` from `src` to `dst` (device pointers, either may
  * be a peer GPU's memory; peer access is enabled on first use) on `stream` with 16-byte

@@ -27,6 +27,7 @@ EPI_STORE, EPI_GELU, EPI_RESID, EPI_DGELU, EPI_ACC_F32, EPI_STORE_F32, EPI_DSOFT
 CAUSAL_NONE, CAUSAL_TILE, CAUSAL_KEND, CAUSAL_KSTART = range(4)
 
 LINK_DIRECT, LINK_P2P, LINK_HOST = 0, 1, 2
+PATH_GPU, PATH_HOST = 0, 1
 IPC_BYTES = 128
 LINK_DOWN = (1 << 63) - 1
 
@@ -154,6 +155,7 @@ _SIGS = {
     "adaptra_outbox_close": (_i32, [_vp]),
     "adaptra_outbox_dst": (_vp, [_vp, _i32]),
     "adaptra_set_link_latency": (_i32, [_vp, _i64]),
+    "adaptra_link_set_path": (_i32, [_vp, _i32]),
     "adaptra_send": (_i32, [_vp, _i32, _vp, _u32]),
     "adaptra_recv_blocking": (_i32, [_vp, _i32, _u32, _P(_vp)]),
     "adaptra_send_wait": (_i32, [_vp, _i32, _u32]),

@@ -274,6 +274,7 @@ struct adaptra_outbox {
   std::atomic<int64_t> latency{0};
   std::atomic<int64_t> n_msgs{0}, sum_delay{0}, max_delay{0};
   std::atomic<int64_t> inflight{0};  // gate items not yet released
+  std::atomic<int> force_host{0};    // delegated path by policy (straggler), link still up
 };
 
 // ------------------------------------------------------------ delegate thread
@@ -593,7 +594,11 @@ extern "C" int adaptra_outbox_close(adaptra_outbox_t ob) {
   return ADAPTRA_OK;
 }
 
-static bool ob_down(adaptra_outbox_t ob) { return ob->latency.load() == ADAPTRA_LINK_DOWN; }
+// true when messages take the delegated host path: the link failed, or the
+// policy moved a straggling link there (adaptra_link_set_path)
+static bool ob_down(adaptra_outbox_t ob) {
+  return ob->latency.load() == ADAPTRA_LINK_DOWN || ob->force_host.load();
+}
 
 extern "C" void* adaptra_outbox_dst(adaptra_outbox_t ob, int32_t mb) {
   if (!ob || mb < 0 || mb >= ob->n_mb) return nullptr;
@@ -626,7 +631,7 @@ extern "C" int adaptra_send(adaptra_outbox_t ob, int32_t mb, void* producer, uin
   cudaSetDevice(ob->dev);
   const int64_t lat = ob->latency.load();
   const bool down = lat == ADAPTRA_LINK_DOWN;
-  const int mode = down ? ADAPTRA_LINK_HOST : ob->mode;
+  const int mode = (down || ob->force_host.load()) ? ADAPTRA_LINK_HOST : ob->mode;
   ADAPTRA_CUDA_TRY(cudaEventRecord(ob->ev_prod[mb], (cudaStream_t)producer));
   uint32_t* flag = ob->peer_dflags + mb;
   volatile uint32_t* hflag_peer = ob->peer_hflags + mb;
@@ -686,7 +691,7 @@ extern "C" int adaptra_recv_blocking(adaptra_inbox_t ib, int32_t mb, uint32_t ep
 extern "C" int adaptra_send_wait(adaptra_outbox_t ob, int32_t mb, uint32_t epoch) {
   if (!ob || mb < 0 || mb >= ob->n_mb) return set_error(ADAPTRA_EINVAL, "send_wait: bad mb");
   cudaSetDevice(ob->dev);
-  if (ob->latency.load() == ADAPTRA_LINK_DOWN) {  // delegated path: wait for the host flag
+  if (ob_down(ob)) {  // delegated path: wait for the host flag
     volatile uint32_t* hf = ob->ring.flags(ob->bytes, ob->n_mb) + mb;
     while ((int32_t)(*hf - epoch) < 0) std::this_thread::sleep_for(std::chrono::microseconds(5));
     return ADAPTRA_OK;
@@ -719,3 +724,14 @@ void* outbox_local_slot(adaptra_outbox_t ob, int mb) {
   return (char*)ob->staging + (size_t)mb * ob->bytes;
 }
 }  // namespace adaptra
+
+extern "C" int adaptra_link_set_path(adaptra_outbox_t ob, int32_t path) {
+  if (!ob || (path != ADAPTRA_PATH_GPU && path != ADAPTRA_PATH_HOST)) return set_error(ADAPTRA_EINVAL, "link_set_path: bad args");
+  if (path == ADAPTRA_PATH_HOST) {
+    if (!ob->has_ring) return set_error(ADAPTRA_ELINK, "link_set_path: no host ring");
+    int rc = ensure_staging(ob);
+    if (rc) return rc;
+  }
+  ob->force_host.store(path == ADAPTRA_PATH_HOST ? 1 : 0);
+  return ADAPTRA_OK;
+}

@@ -238,7 +238,7 @@ class Pipeline:
             L.check(lib.adaptra_set_link_latency(self.out_fwd[link], ns))
         if link + 1 in self.out_bwd:
             L.check(lib.adaptra_set_link_latency(self.out_bwd[link + 1], ns))
-        down = 1 if ns == L.LINK_DOWN else 0
+        down = 1 if (ns == L.LINK_DOWN or link in getattr(self, "on_host", set())) else 0
         if link + 1 in self.in_fwd:
             L.check(lib.adaptra_inbox_set_host(self.in_fwd[link + 1], down))
         if link in self.in_bwd:
@@ -265,6 +265,25 @@ class Pipeline:
         prev = self.stage_rank[i - 1] if i > 0 else -1
         nxt = self.stage_rank[i + 1] if i < self.S - 1 else -1
         L.check(lib.adaptra_exec_set_nccl(self.execs[i], comm, prev, nxt, int(down_ns)))
+
+    def set_path(self, link: int, host: bool):
+        """Delegation policy: move both directions of `link` to
+        the delegated host path while it is up (host=True) or back (False)."""
+        lib = L.lib()
+        self.on_host = getattr(self, "on_host", set())
+        if (link in self.on_host) == bool(host):
+            return
+        p = L.PATH_HOST if host else L.PATH_GPU
+        if link in self.out_fwd:
+            L.check(lib.adaptra_link_set_path(self.out_fwd[link], p))
+        if link + 1 in self.out_bwd:
+            L.check(lib.adaptra_link_set_path(self.out_bwd[link + 1], p))
+        on = 1 if (host or self.latency[link] == L.LINK_DOWN) else 0
+        if link + 1 in self.in_fwd:
+            L.check(lib.adaptra_inbox_set_host(self.in_fwd[link + 1], on))
+        if link in self.in_bwd:
+            L.check(lib.adaptra_inbox_set_host(self.in_bwd[link], on))
+        (self.on_host.add if host else self.on_host.discard)(link)
 
     def run(self, orders, merge_w=False, want_times=False, inorder=False, nccl=False):
         """One iteration.  orders[i] = [(kind, mb), ...] for every stage i (only
@@ -420,6 +439,8 @@ class Arm:
     def __init__(self, name, S, N, tF, tB, tW, *, x_init=None, ratio=30, x_cap=None, mem=None):
         self.inorder = name.endswith("-inorder")
         self.nccl = name.endswith("-nccl")       # N1: NCCL send/recv in the compute sequence
+        self.deleg = name.endswith("-deleg")     # straggling links on the delegated host path
+        name = name[:-len("-deleg")] if self.deleg else name
         name = name[:-len("-inorder")] if self.inorder else name
         name = name[:-len("-nccl")] if self.nccl else name
         self.name, self.S, self.N = name, S, N

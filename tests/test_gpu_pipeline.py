@@ -99,6 +99,17 @@ def test_latency_injection_and_link_down(mode):
         pipe.set_latency(1, 0)
         res = pipe.run(orders)
         _check(pipe, res, Lref, gref, 1e-4)
+        # delegation policy: a straggling (up) link moved to the host path keeps
+        # its latency and the results
+        pipe.set_latency(1, 3_000_000)
+        pipe.set_path(1, True)
+        res = pipe.run(orders, want_times=True)
+        _check(pipe, res, Lref, gref, 1e-4)
+        assert res.stats[2]["op_times"][0][0] - res.stats[1]["op_times"][0][1] >= 2_900_000
+        pipe.set_path(1, False)
+        pipe.set_latency(1, 0)
+        res = pipe.run(orders)
+        _check(pipe, res, Lref, gref, 1e-4)
     finally:
         pipe.close()
 
