@@ -498,6 +498,24 @@ int adaptra_exec_destroy(adaptra_exec_t e);
  * Non-blocking (the stage thread enqueues). */
 #define ADAPTRA_EXEC_INORDER 16u
 int adaptra_run_iteration(adaptra_exec_t e, const adaptra_op_t* ops, int32_t n, uint32_t epoch, uint32_t flags);
+/* N4 host activation offload ("offloading activation and
+ * gradients to the host lifts the GPU memory pressure").  The
+ * stage's n_slots device F->W stash slots may be fewer than the microbatches
+ * in flight: host_pool (caller-owned pinned memory, n_host_slots x
+ * adaptra_stage_slot_bytes) takes the overflow.  Per iteration the executor
+ * plans from the known op order (Belady): when an F finds no free device
+ * slot, the complete slot (its B done) whose W is furthest away is spilled --
+ * the D2H is issued on an offload stream right after that slot's B, and the F
+ * waits only for that copy -- and a spilled slot is prefetched (H2D) when a
+ * device slot is free and its W is within `window` ops (default 4), or at the
+ * latest right before its W, which waits for it.  Results are bit-identical
+ * to the all-device run.  ENOMEM from adaptra_run_iteration's stage thread
+ * when even the host pool cannot hold the order's demand.  n_host_slots = 0
+ * disables. */
+int adaptra_exec_set_offload(adaptra_exec_t e, void* host_pool, int32_t n_host_slots, int32_t window);
+/* Spills and prefetches planned for the last iteration; bytes moved since creation. */
+int adaptra_exec_offload_stats(adaptra_exec_t e, int32_t* n_spill, int32_t* n_prefetch, int64_t* bytes);
+
 /* ---------------------------------------------------------------- NCCL baseline (N1)
  * north_star: "NCCL send/recv is used only as the baseline".  With
  * ADAPTRA_EXEC_NCCL the executor runs the fixed execution plan of

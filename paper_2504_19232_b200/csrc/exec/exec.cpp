@@ -28,6 +28,10 @@
 namespace adaptra {
 int stage_n_slots(adaptra_stage_t s);
 int stage_device(adaptra_stage_t s);
+void* stage_slot_base(adaptra_stage_t s, int slot);
+int64_t stage_slot_nbytes(adaptra_stage_t s);
+void stage_get_meta(adaptra_stage_t s, int slot, const void** x_in, const void** dy_in);
+void stage_set_meta(adaptra_stage_t s, int to, int from, const void* x_in, const void* dy_in);
 }  // namespace adaptra
 
 using namespace adaptra;
@@ -58,7 +62,6 @@ struct adaptra_exec {
   cudaEvent_t ev_t0 = nullptr;
   cudaEvent_t ev_base = nullptr;  // optional common time base (same device), set by the caller
   std::vector<cudaEvent_t> ev_s, ev_e;
-  std::vector<int> slot_of_mb;
   // a1 profiler: per completed iteration, the mean op time per kind (ns; -1 = none)
   std::deque<std::array<int64_t, 3>> hist;
   // host I/O (end-to-end runs): stage 0 copies each microbatch's input from
@@ -69,6 +72,161 @@ struct adaptra_exec {
   float* host_loss = nullptr;
   cudaStream_t h2d = nullptr;
   std::vector<cudaEvent_t> ev_in;
+  // N4 stash offload: the F->W stash slots of the
+  // stage live in `n_slots` device slots; with a pinned host pool, slots whose
+  // W is far in the op order are spilled there after their B and prefetched
+  // back before their W, so the stage can hold more in-flight microbatches
+  // than fit in HBM.  The plan is static per iteration (the op order is known
+  // in advance): Belady eviction (the complete slot whose W is furthest away)
+  // when an F needs a slot, spill D2H issued right after the victim's B,
+  // prefetch H2D up to `pf_window` ops ahead of its W when a slot is free.
+  struct OffAct {
+    int spill;  // 1 = D2H spill, 0 = H2D prefetch
+    int mb, dslot, hslot, from_slot, id;
+  };
+  struct SlotPlan {
+    std::vector<int> slot;                      // device slot of op q
+    std::vector<std::vector<OffAct>> after;     // offload actions issued after op q
+    std::vector<std::vector<int>> wait;         // action ids op q waits for
+    int n_spill = 0, n_prefetch = 0;
+  } P;
+  char* host_pool = nullptr;
+  int n_host = 0, pf_window = 4;
+  cudaStream_t off = nullptr;
+  std::vector<cudaEvent_t> ev_act;
+  std::vector<std::pair<const void*, const void*>> saved_meta;  // per mb (x_in, dy_in) while spilled
+  int64_t spilled_bytes = 0;
+
+  int plan_slots() {
+    const int N = d.n_microbatches, D = stage_n_slots(d.stage), n = (int)ops.size();
+    const bool merge = flags & ADAPTRA_MERGE_W;
+    P.slot.assign(n, -1);
+    P.after.assign(n, {});
+    P.wait.assign(n, {});
+    P.n_spill = P.n_prefetch = 0;
+    std::vector<int> bpos(N + 1, INT32_MAX), wpos(N + 1, INT32_MAX), state(N + 1, 0), dsl(N + 1, -1),
+        hsl(N + 1, -1);
+    for (int q = n - 1; q >= 0; --q) {
+      const int mb = ops[q].mb;
+      if (mb < 1 || mb > N) return set_error(ADAPTRA_EINVAL, "exec: bad microbatch");
+      if (ops[q].kind == ADAPTRA_OP_B) bpos[mb] = q;
+      if (ops[q].kind == ADAPTRA_OP_W || (merge && ops[q].kind == ADAPTRA_OP_B)) wpos[mb] = q;
+    }
+    std::vector<int> free_dev, free_host;
+    for (int k = D - 1; k >= 0; --k) free_dev.push_back(k);
+    for (int k = n_host - 1; k >= 0; --k) free_host.push_back(k);
+    int next_id = 0;
+    auto evict = [&](int q, int keep) -> int {
+      int best = -1;
+      for (int mb = 1; mb <= N; ++mb)
+        if (state[mb] == 1 && mb != keep && bpos[mb] < q && wpos[mb] > q && (best < 0 || wpos[mb] > wpos[best]))
+          best = mb;
+      if (best < 0) return set_error(ADAPTRA_ENOMEM, "exec: stash slots exhausted (no complete slot to offload)");
+      if (free_host.empty()) return set_error(ADAPTRA_ENOMEM, "exec: stash slots exhausted (host offload pool full)");
+      const int h = free_host.back();
+      free_host.pop_back();
+      OffAct a{1, best, dsl[best], h, dsl[best], next_id++};
+      P.after[bpos[best]].push_back(a);
+      P.wait[q].push_back(a.id);
+      P.n_spill++;
+      state[best] = 2;
+      hsl[best] = h;
+      free_dev.push_back(dsl[best]);
+      return ADAPTRA_OK;
+    };
+    auto prefetch = [&](int mb, int after_q, int w_q) {
+      const int s = free_dev.back();
+      free_dev.pop_back();
+      OffAct a{0, mb, s, hsl[mb], -1, next_id++};
+      P.after[after_q].push_back(a);
+      P.wait[w_q].push_back(a.id);
+      P.n_prefetch++;
+      free_host.push_back(hsl[mb]);
+      state[mb] = 1;
+      dsl[mb] = s;
+    };
+    for (int q = 0; q < n; ++q) {
+      const adaptra_op_t& o = ops[q];
+      const int mb = o.mb;
+      if (o.kind == ADAPTRA_OP_F) {
+        if (state[mb] != 0) return set_error(ADAPTRA_EINVAL, "exec: F twice");
+        int rc;
+        if (free_dev.empty() && (rc = evict(q, -1))) return rc;
+        dsl[mb] = free_dev.back();
+        free_dev.pop_back();
+        state[mb] = 1;
+        P.slot[q] = dsl[mb];
+      } else {
+        if (state[mb] == 0) return set_error(ADAPTRA_EINVAL, o.kind == ADAPTRA_OP_B ? "exec: B before F" : "exec: W before F");
+        if (state[mb] == 2) {                 // W of a spilled slot not prefetched yet: fetch now
+          int rc;
+          if (free_dev.empty() && (rc = evict(q, mb))) return rc;
+          if (q == 0) return set_error(ADAPTRA_EINVAL, "exec: W first");
+          prefetch(mb, q - 1, q);
+        }
+        P.slot[q] = dsl[mb];
+        if (o.kind == ADAPTRA_OP_W || merge) {
+          free_dev.push_back(dsl[mb]);
+          state[mb] = 0;
+        }
+      }
+      // early prefetch: the spilled slot with the nearest W, if it is within
+      // pf_window ops and the F ops before it leave a device slot free
+      while (n_host > 0 && !free_dev.empty()) {
+        int nb = -1;
+        for (int m = 1; m <= N; ++m)
+          if (state[m] == 2 && (nb < 0 || wpos[m] < wpos[nb])) nb = m;
+        if (nb < 0 || wpos[nb] > q + pf_window) break;
+        int nf = 0;
+        for (int r = q + 1; r < wpos[nb]; ++r) nf += ops[r].kind == ADAPTRA_OP_F;
+        if ((int)free_dev.size() <= nf) break;
+        prefetch(nb, q, wpos[nb]);
+      }
+    }
+    if (next_id > (int)ev_act.size()) {
+      cudaSetDevice(dev);
+      const size_t old = ev_act.size();
+      ev_act.resize(next_id);
+      for (size_t k = old; k < ev_act.size(); ++k)
+        ADAPTRA_CUDA_TRY(cudaEventCreateWithFlags(&ev_act[k], cudaEventDisableTiming));
+    }
+    if (next_id > 0 && !off) return set_error(ADAPTRA_EINVAL, "exec: offload planned without a host pool");
+    saved_meta.assign(N + 1, {nullptr, nullptr});
+    from_slot_of.assign(N + 1, -1);
+    return ADAPTRA_OK;
+  }
+
+  // before op q's kernels: wait for the spills / prefetches it depends on
+  int pre_op(size_t q) {
+    for (int id : P.wait[q]) ADAPTRA_CUDA_TRY(cudaStreamWaitEvent(cs, ev_act[id], 0));
+    return ADAPTRA_OK;
+  }
+
+  // after op q has been enqueued: issue the offload copies planned there
+  int post_op(size_t q) {
+    if (P.after[q].empty()) return ADAPTRA_OK;
+    const int64_t sb = stage_slot_nbytes(d.stage);
+    ADAPTRA_CUDA_TRY(cudaStreamWaitEvent(off, ev_e[q], 0));
+    for (const OffAct& a : P.after[q]) {
+      char* hp = host_pool + (size_t)a.hslot * sb;
+      char* dp = (char*)stage_slot_base(d.stage, a.dslot);
+      if (a.spill) {
+        const void *x = nullptr, *y = nullptr;
+        stage_get_meta(d.stage, a.dslot, &x, &y);
+        saved_meta[a.mb] = {x, y};
+        from_slot_of[a.mb] = a.dslot;
+        ADAPTRA_CUDA_TRY(cudaMemcpyAsync(hp, dp, sb, cudaMemcpyDeviceToHost, off));
+      } else {
+        stage_set_meta(d.stage, a.dslot, from_slot_of[a.mb], saved_meta[a.mb].first, saved_meta[a.mb].second);
+        ADAPTRA_CUDA_TRY(cudaMemcpyAsync(dp, hp, sb, cudaMemcpyHostToDevice, off));
+      }
+      spilled_bytes += sb;
+      ADAPTRA_CUDA_TRY(cudaEventRecord(ev_act[a.id], off));
+    }
+    return ADAPTRA_OK;
+  }
+  std::vector<int> from_slot_of;
+
   // NCCL baseline arm (N1): communicator and the peers' ranks
   void* nccl = nullptr;
   int nccl_prev = -1, nccl_next = -1;
@@ -82,7 +240,7 @@ struct adaptra_exec {
   // send (the transfer occupies the in-order stream); a failed
   // link costs its measured delegated-path time instead (baselines have no
   // delegation, so this is generous to them).
-  int run_nccl(std::vector<int>& free_slots) {
+  int run_nccl() {
     const int S = d.n_stages, i = d.stage_index, N = d.n_microbatches;
     const bool merge = flags & ADAPTRA_MERGE_W;
     int rc;
@@ -104,14 +262,13 @@ struct adaptra_exec {
       return l == ADAPTRA_LINK_DOWN ? nccl_down_ns : l;
     };
     for (size_t q = 0; q < ops.size(); ++q) {
+      if (q > 0 && (rc = post_op(q - 1))) return rc;
       const adaptra_op_t& o = ops[q];
       const int mb = o.mb;
       if (mb < 1 || mb > N) return set_error(ADAPTRA_EINVAL, "exec: bad microbatch");
       if (o.kind == ADAPTRA_OP_F) {
-        if (free_slots.empty()) return set_error(ADAPTRA_ENOMEM, "exec: stash slots exhausted (plan needs more)");
-        int slot = free_slots.back();
-        free_slots.pop_back();
-        slot_of_mb[mb] = slot;
+        const int slot = P.slot[q];
+        if ((rc = pre_op(q))) return rc;
         const void* x = nullptr;
         if (i == 0) {
           x = d.inputs[mb - 1];
@@ -136,8 +293,9 @@ struct adaptra_exec {
           p_lat = lat_of(d.out_fwd);
         }
       } else if (o.kind == ADAPTRA_OP_B) {
-        int slot = slot_of_mb[mb];
+        const int slot = P.slot[q];
         if (slot < 0) return set_error(ADAPTRA_EINVAL, "exec: B before F");
+        if ((rc = pre_op(q))) return rc;
         void* dy = nullptr;
         if (i < S - 1) {
           dy = adaptra_inbox_slot(d.in_bwd, mb - 1);
@@ -151,8 +309,6 @@ struct adaptra_exec {
         if ((rc = adaptra_stage_B(d.stage, slot, dy, dx, cs))) return rc;
         if (merge) {
           if ((rc = adaptra_stage_W(d.stage, slot, cs))) return rc;
-          free_slots.push_back(slot);
-          slot_of_mb[mb] = -1;
         }
         ADAPTRA_CUDA_TRY(cudaEventRecord(ev_e[q], cs));
         if (i > 0) {
@@ -162,18 +318,18 @@ struct adaptra_exec {
           p_lat = lat_of(d.out_bwd);
         }
       } else if (o.kind == ADAPTRA_OP_W) {
-        int slot = slot_of_mb[mb];
+        const int slot = P.slot[q];
         if (slot < 0) return set_error(ADAPTRA_EINVAL, "exec: W before F");
+        if ((rc = pre_op(q))) return rc;
         if ((rc = flush(nullptr, 0, -1))) return rc;
         ADAPTRA_CUDA_TRY(cudaEventRecord(ev_s[q], cs));
         if ((rc = adaptra_stage_W(d.stage, slot, cs))) return rc;
         ADAPTRA_CUDA_TRY(cudaEventRecord(ev_e[q], cs));
-        free_slots.push_back(slot);
-        slot_of_mb[mb] = -1;
       } else {
         return set_error(ADAPTRA_EINVAL, "exec: bad op kind");
       }
     }
+    if (!ops.empty() && (rc = post_op(ops.size() - 1))) return rc;
     return flush(nullptr, 0, -1);
   }
 
@@ -201,9 +357,8 @@ struct adaptra_exec {
       return ADAPTRA_OK;
     };
     const int64_t t_start = now_ns();
-    std::vector<int> free_slots;
-    for (int k = stage_n_slots(d.stage) - 1; k >= 0; --k) free_slots.push_back(k);
-    slot_of_mb.assign(N + 1, -1);
+    int rc;
+    if ((rc = plan_slots())) return rc;
     ADAPTRA_CUDA_TRY(cudaEventRecord(ev_t0, cs));
     if (i == S - 1 && d.loss_acc) ADAPTRA_CUDA_TRY(cudaMemsetAsync(d.loss_acc, 0, sizeof(float), cs));
     if (i == 0 && host_inputs) {
@@ -216,13 +371,12 @@ struct adaptra_exec {
         ADAPTRA_CUDA_TRY(cudaEventRecord(ev_in[o.mb - 1], h2d));
       }
     }
-    int rc;
     DBG("start epoch %u n_ops %zu", epoch, ops.size());
     if ((rc = adaptra_stage_zero_grads(d.stage, cs))) return rc;  // gradients of this iteration only
     DBG("zeroed");
     if (flags & ADAPTRA_EXEC_NCCL) {
       if (!nccl) return set_error(ADAPTRA_EINVAL, "exec: NCCL arm without a communicator (adaptra_exec_set_nccl)");
-      if ((rc = run_nccl(free_slots))) return rc;
+      if ((rc = run_nccl())) return rc;
       if (i == S - 1 && host_loss && d.loss_acc)
         ADAPTRA_CUDA_TRY(cudaMemcpyAsync(host_loss, d.loss_acc, sizeof(float), cudaMemcpyDeviceToHost, cs));
       host_ns = now_ns() - t_start;
@@ -233,6 +387,7 @@ struct adaptra_exec {
       return v ? atoi(v) : 3;
     }();
     for (size_t q = 0; q < ops.size(); ++q) {
+      if (q > 0 && (rc = post_op(q - 1))) return rc;
       const adaptra_op_t& o = ops[q];
       const int mb = o.mb;
       DBG("op %zu kind %d mb %d", q, o.kind, o.mb);
@@ -245,10 +400,8 @@ struct adaptra_exec {
       }
       if (mb < 1 || mb > N) return set_error(ADAPTRA_EINVAL, "exec: bad microbatch");
       if (o.kind == ADAPTRA_OP_F) {
-        if (free_slots.empty()) return set_error(ADAPTRA_ENOMEM, "exec: stash slots exhausted (plan needs more)");
-        int slot = free_slots.back();
-        free_slots.pop_back();
-        slot_of_mb[mb] = slot;
+        const int slot = P.slot[q];
+        if ((rc = pre_op(q))) return rc;
         const void* x = nullptr;
         if (i == 0) {
           x = d.inputs[mb - 1];
@@ -271,8 +424,9 @@ struct adaptra_exec {
         if (i < S - 1 && (rc = adaptra_send(d.out_fwd, mb - 1, cs, epoch))) return rc;
         if (inorder && i < S - 1 && (rc = send_q(d.out_fwd, q_fwd, mb - 1))) return rc;
       } else if (o.kind == ADAPTRA_OP_B) {
-        int slot = slot_of_mb[mb];
+        const int slot = P.slot[q];
         if (slot < 0) return set_error(ADAPTRA_EINVAL, "exec: B before F");
+        if ((rc = pre_op(q))) return rc;
         void* dy = nullptr;
         if (i < S - 1 && (rc = inorder ? adaptra_recv_blocking(d.in_bwd, mb - 1, epoch, &dy)
                                        : adaptra_recv(d.in_bwd, mb - 1, epoch, cs, &dy)))
@@ -284,24 +438,22 @@ struct adaptra_exec {
         DBG("  B launched");
         if (merge) {
           if ((rc = adaptra_stage_W(d.stage, slot, cs))) return rc;
-          free_slots.push_back(slot);
-          slot_of_mb[mb] = -1;
         }
         ADAPTRA_CUDA_TRY(cudaEventRecord(ev_e[q], cs));
         if (i > 0 && (rc = adaptra_send(d.out_bwd, mb - 1, cs, epoch))) return rc;
         if (inorder && i > 0 && (rc = send_q(d.out_bwd, q_bwd, mb - 1))) return rc;
       } else if (o.kind == ADAPTRA_OP_W) {
-        int slot = slot_of_mb[mb];
+        const int slot = P.slot[q];
         if (slot < 0) return set_error(ADAPTRA_EINVAL, "exec: W before F");
+        if ((rc = pre_op(q))) return rc;
         ADAPTRA_CUDA_TRY(cudaEventRecord(ev_s[q], cs));
         if ((rc = adaptra_stage_W(d.stage, slot, cs))) return rc;
         ADAPTRA_CUDA_TRY(cudaEventRecord(ev_e[q], cs));
-        free_slots.push_back(slot);
-        slot_of_mb[mb] = -1;
       } else {
         return set_error(ADAPTRA_EINVAL, "exec: bad op kind");
       }
     }
+    if (!ops.empty() && (rc = post_op(ops.size() - 1))) return rc;
     if (i == S - 1 && host_loss && d.loss_acc)
       ADAPTRA_CUDA_TRY(cudaMemcpyAsync(host_loss, d.loss_acc, sizeof(float), cudaMemcpyDeviceToHost, cs));
     host_ns = now_ns() - t_start;
@@ -364,6 +516,8 @@ extern "C" int adaptra_exec_destroy(adaptra_exec_t e) {
   e->th.join();
   cudaSetDevice(e->dev);
   if (e->h2d) cudaStreamDestroy(e->h2d);
+  if (e->off) cudaStreamDestroy(e->off);
+  for (auto ev : e->ev_act) cudaEventDestroy(ev);
   for (auto ev : e->ev_in) cudaEventDestroy(ev);
   cudaEventDestroy(e->ev_t0);
   for (auto ev : e->ev_s) cudaEventDestroy(ev);
@@ -404,6 +558,27 @@ extern "C" int adaptra_exec_set_host_io(adaptra_exec_t e, const void* const* hos
   e->host_inputs = host_inputs;
   e->host_in_bytes = bytes;
   e->host_loss = host_loss;
+  return ADAPTRA_OK;
+}
+
+extern "C" int adaptra_exec_set_offload(adaptra_exec_t e, void* host_pool, int32_t n_host_slots, int32_t window) {
+  if (!e || n_host_slots < 0 || (n_host_slots > 0 && !host_pool)) return set_error(ADAPTRA_EINVAL, "exec_set_offload: bad args");
+  std::unique_lock<std::mutex> lk(e->mu);
+  if (e->busy) return set_error(ADAPTRA_EINVAL, "exec_set_offload: iteration running");
+  cudaSetDevice(e->dev);
+  if (n_host_slots > 0 && !e->off) ADAPTRA_CUDA_TRY(cudaStreamCreateWithFlags(&e->off, cudaStreamNonBlocking));
+  e->host_pool = (char*)host_pool;
+  e->n_host = n_host_slots;
+  e->pf_window = window > 0 ? window : 4;
+  return ADAPTRA_OK;
+}
+
+extern "C" int adaptra_exec_offload_stats(adaptra_exec_t e, int32_t* n_spill, int32_t* n_prefetch, int64_t* bytes) {
+  if (!e) return set_error(ADAPTRA_EINVAL, "exec_offload_stats: null");
+  std::unique_lock<std::mutex> lk(e->mu);
+  if (n_spill) *n_spill = e->P.n_spill;
+  if (n_prefetch) *n_prefetch = e->P.n_prefetch;
+  if (bytes) *bytes = e->spilled_bytes;
   return ADAPTRA_OK;
 }
 

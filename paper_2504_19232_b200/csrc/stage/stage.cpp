@@ -483,6 +483,26 @@ using namespace adaptra;
 namespace adaptra {
 int stage_n_slots(adaptra_stage_t s) { return s->d.n_slots; }
 int stage_device(adaptra_stage_t s) { return s->dev; }
+// N4 stash offload (exec.cpp): a slot's bytes and its host-side metadata
+// (the layer-0 input and top-layer gradient pointers W reads) move together.
+void* stage_slot_base(adaptra_stage_t s, int slot) { return (char*)s->d.stash + (long)slot * s->L.slot_bytes; }
+int64_t stage_slot_nbytes(adaptra_stage_t s) { return s->L.slot_bytes; }
+void stage_get_meta(adaptra_stage_t s, int slot, const void** x_in, const void** dy_in) {
+  *x_in = s->x_in[slot];
+  *dy_in = s->dy_in[slot];
+}
+// Restore metadata saved from slot `from` into slot `to`: pointers that
+// pointed inside slot `from` (the last stage's MSE seed) are rebased.
+void stage_set_meta(adaptra_stage_t s, int to, int from, const void* x_in, const void* dy_in) {
+  const char* b0 = (const char*)stage_slot_base(s, from);
+  const char* b1 = (const char*)stage_slot_base(s, to);
+  auto rebase = [&](const void* p) -> const void* {
+    const char* c = (const char*)p;
+    return (c >= b0 && c < b0 + s->L.slot_bytes) ? b1 + (c - b0) : p;
+  };
+  s->x_in[to] = rebase(x_in);
+  s->dy_in[to] = rebase(dy_in);
+}
 }  // namespace adaptra
 
 extern "C" int64_t adaptra_stage_slot_bytes(const adaptra_stage_desc_t* d) {

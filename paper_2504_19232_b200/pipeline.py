@@ -362,6 +362,30 @@ class Pipeline:
                                                  C.c_void_p(self._host_loss.data_ptr()) if on else None))
         return h2d, d2h
 
+    def enable_offload(self, host_slots, window=4):
+        """N4: give every local stage a pinned host pool of `host_slots` F->W
+        stash slots (adaptra_exec_set_offload); the device keeps n_slots."""
+        lib = L.lib()
+        self._host_pools = getattr(self, "_host_pools", {})
+        for i in self.local:
+            hs = host_slots[i] if isinstance(host_slots, (list, tuple)) else host_slots
+            if hs > 0:
+                pool = torch.empty(hs * self.stages[i].slot_bytes, dtype=torch.uint8, pin_memory=True)
+                self._host_pools[i] = pool
+                L.check(lib.adaptra_exec_set_offload(self.execs[i], C.c_void_p(pool.data_ptr()), hs, window))
+            else:
+                self._host_pools.pop(i, None)
+                L.check(lib.adaptra_exec_set_offload(self.execs[i], None, 0, window))
+
+    def offload_stats(self):
+        lib = L.lib()
+        out = {}
+        for i in self.local:
+            a, b, c = C.c_int32(), C.c_int32(), C.c_int64()
+            L.check(lib.adaptra_exec_offload_stats(self.execs[i], C.byref(a), C.byref(b), C.byref(c)))
+            out[i] = (a.value, b.value, c.value)
+        return out
+
     def profile(self, k=5, quantum=1000):
         """a1: per-stage (t^F, t^B, t^W) in ns = lower median over the last k
         iterations of each stage's mean op time (adaptra_exec_profile, CUDA

@@ -161,3 +161,43 @@ def test_host_io_end_to_end_matches_device_path():
         pipe.set_host_io(False)
     finally:
         pipe.close()
+
+
+@pytest.mark.parametrize("arm", ["zb", "adaptive"])
+@pytest.mark.parametrize("kind,dtype,S,N,Lt,d,dff,H,b,T,tol", CFGS)
+def test_stash_offload_matches_device_run(kind, dtype, S, N, Lt, d, dff, H, b, T, tol, arm):
+    """N4: with 3 device F->W slots per stage and the rest in a
+    pinned host pool (Belady spills after B, prefetch before W), the iteration
+    gives the same loss and gradients as with every slot on the device (bit
+    for bit) and as the oracle's full batch; the plan really spilled."""
+    ref_pipe, Lref, gref = _setup(kind, dtype, S, N, Lt, d, dff, H, b, T)
+    t = [1000] * S
+    try:
+        a = Arm(arm, S, N, t, t, t)
+        c = [0] * (S - 1)
+        if arm == "adaptive":
+            c[0] = 3_000_000
+            ref_pipe.set_latency(0, c[0])
+        orders = a.plan(c)
+        ref = ref_pipe.run(orders)
+        ref_grads = {i: st.grads() for i, st in ref_pipe.stages.items()}
+    finally:
+        ref_pipe.close()
+    pipe, _, _ = _setup(kind, dtype, S, N, Lt, d, dff, H, b, T, n_slots=3)
+    try:
+        pipe.enable_offload(N, window=2)
+        if arm == "adaptive":
+            pipe.set_latency(0, c[0])
+        for _ in range(2):
+            res = pipe.run(orders)
+        assert res.loss == ref.loss
+        for i, st in pipe.stages.items():
+            got = st.grads()
+            for l in range(len(got)):
+                for k in got[l]:
+                    assert np.array_equal(got[l][k], ref_grads[i][l][k]), (i, l, k)
+        _check(pipe, res, Lref, gref, tol)
+        st = pipe.offload_stats()
+        assert sum(v[0] for v in st.values()) > 0 and all(v[0] == v[1] for v in st.values())
+    finally:
+        pipe.close()
