@@ -116,8 +116,11 @@ static int compute_layout(const adaptra_stage_desc_t& d, SlotLayout& L) {
     if (d.n_heads < 1 || D % d.n_heads) return set_error(ADAPTRA_EINVAL, "stage: d % n_heads != 0");
     long dh = D / d.n_heads;
     if (dh % 8) return set_error(ADAPTRA_EINVAL, "stage: head dim must be a multiple of 8");
-    if (d.dtype == ADAPTRA_BF16 && (d.T % 128 || (dh != 64 && dh != 128)))
-      return set_error(ADAPTRA_EINVAL, "stage bf16: T % 128 == 0 and head dim 64 or 128 required");
+    // bf16 runs the tcgen05 path: the fused attention is built for head dim
+    // 128 (GPT-2 shapes); other head dims are rejected rather than
+    // routed to an untested path (fp32 parity mode takes any multiple of 8)
+    if (d.dtype == ADAPTRA_BF16 && (d.T % 128 || dh != 128))
+      return set_error(ADAPTRA_EINVAL, "stage bf16: T % 128 == 0 and head dim 128 required");
     long PT = (long)d.b * d.n_heads * d.T * d.T;
     L.xl = put(R * D * e);
     L.h1 = put(R * D * e);

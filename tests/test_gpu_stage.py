@@ -32,10 +32,6 @@ CASES = [
     # 3 sequences x 4 heads x 16 query blocks = 192 attention items on the
     # persistent forward grid (148 CTAs): CTAs with one and with two items
     ("gpt", L.BF16, 1, 512, 1024, 4, 3, 2048, 1),
-    # bf16 with head dim 64 (d=256, 4 heads): the fused attention needs 128,
-    # so this takes the materialised tcgen05 path (batched score GEMMs)
-    ("gpt", L.BF16, 2, 256, 1024, 4, 1, 256, 2),
-    ("gpt", L.BF16, 1, 256, 512, 4, 2, 128, 2),
 ]
 
 
