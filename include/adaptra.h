@@ -338,6 +338,11 @@ int adaptra_stage_B(adaptra_stage_t s, int32_t slot, const void* dy_in, void* dx
 /* W: weight gradients of the slot, accumulated
  * into gwts/gvecs (dW += dY^T X in fp32, db += sum dY, LN dgamma/dbeta). */
 int adaptra_stage_W(adaptra_stage_t s, int32_t slot, void* stream);
+/* W of two slots as one launch: every dW += X^T dY product runs over both
+ * microbatches' rows (K = 2 b T, slot_a's rows first) and is reduce-added into
+ * the fp32 gradient once (the executor uses it for two consecutive W ops of
+ * a stage's order, $ADAPTRA_W_PAIRS=0 disables); bias / LN sums per slot. */
+int adaptra_stage_W2(adaptra_stage_t s, int32_t slot_a, int32_t slot_b, void* stream);
 int adaptra_stage_zero_grads(adaptra_stage_t s, void* stream);
 
 /* ================================================================ transport

@@ -382,6 +382,10 @@ struct adaptra_exec {
       host_ns = now_ns() - t_start;
       return ADAPTRA_OK;
     }
+    static const bool w_pairs = [] {
+      const char* v = getenv("ADAPTRA_W_PAIRS");
+      return v ? atoi(v) != 0 : true;
+    }();
     static const int lookahead = [] {
       const char* v = getenv("ADAPTRA_LOOKAHEAD");
       return v ? atoi(v) : 3;
@@ -446,6 +450,20 @@ struct adaptra_exec {
         const int slot = P.slot[q];
         if (slot < 0) return set_error(ADAPTRA_EINVAL, "exec: W before F");
         if ((rc = pre_op(q))) return rc;
+        // two consecutive W ops of the order run as one launch over K = 2bT
+        // (adaptra_stage_W2): same work, half the fp32 gradient traffic; the
+        // pair's time is booked on the first op (the second gets zero length)
+        if (w_pairs && !merge && q + 1 < ops.size() && ops[q + 1].kind == ADAPTRA_OP_W && P.slot[q + 1] >= 0) {
+          if ((rc = pre_op(q + 1))) return rc;
+          ADAPTRA_CUDA_TRY(cudaEventRecord(ev_s[q], cs));
+          if ((rc = adaptra_stage_W2(d.stage, slot, P.slot[q + 1], cs))) return rc;
+          ADAPTRA_CUDA_TRY(cudaEventRecord(ev_e[q], cs));
+          ADAPTRA_CUDA_TRY(cudaEventRecord(ev_s[q + 1], cs));
+          ADAPTRA_CUDA_TRY(cudaEventRecord(ev_e[q + 1], cs));
+          if ((rc = post_op(q))) return rc;
+          ++q;
+          continue;
+        }
         ADAPTRA_CUDA_TRY(cudaEventRecord(ev_s[q], cs));
         if ((rc = adaptra_stage_W(d.stage, slot, cs))) return rc;
         ADAPTRA_CUDA_TRY(cudaEventRecord(ev_e[q], cs));

@@ -685,9 +685,10 @@ static int launch_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
 constexpr int kMaxGroup = 24;
 struct GroupArgs {
   CUtensorMap tmA[kMaxGroup], tmB[kMaxGroup], tmC[kMaxGroup];
+  CUtensorMap tmA2[kMaxGroup], tmB2[kMaxGroup];  // second K half (two-slot W), if k_split < k_blocks
   int n, total_tiles;
   int tile_start[kMaxGroup + 1];
-  int m_blocks[kMaxGroup], k_blocks[kMaxGroup], N[kMaxGroup];
+  int m_blocks[kMaxGroup], k_blocks[kMaxGroup], k_split[kMaxGroup], N[kMaxGroup];
   float alpha[kMaxGroup];
 };
 
@@ -753,13 +754,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_grouped_kernel(const __gr
           if (rank == 0) mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes * CG);
           uint8_t* a_dst = sA + stage * Cfg::kABytes;
           uint8_t* b_dst = sB + stage * Cfg::kBBytes;
-          const int k0 = kb * BK;
+          const bool second = kb >= ga.k_split[q];
+          const int k0 = (second ? kb - ga.k_split[q] : kb) * BK;
+          const CUtensorMap* mA = second ? &ga.tmA2[q] : &ga.tmA[q];
+          const CUtensorMap* mB = second ? &ga.tmB2[q] : &ga.tmB[q];
 #pragma unroll
           for (int j = 0; j < BM / 64; ++j)
-            tma_load_2d_2sm(a_dst + j * (BK * 128), &ga.tmA[q], &full[stage], m0 + 64 * j, k0);
+            tma_load_2d_2sm(a_dst + j * (BK * 128), mA, &full[stage], m0 + 64 * j, k0);
 #pragma unroll
           for (int j = 0; j < Cfg::kBRows / 64; ++j)
-            tma_load_2d_2sm(b_dst + j * (BK * 128), &ga.tmB[q], &full[stage], n0 + 64 * j, k0);
+            tma_load_2d_2sm(b_dst + j * (BK * 128), mB, &full[stage], n0 + 64 * j, k0);
           if (++stage == Cfg::kStages) {
             stage = 0;
             phase ^= 1;
@@ -874,25 +878,31 @@ int gemm_tc(const adaptra_gemm_desc_t& g, cudaStream_t st);
 
 // Grouped dW products (see above).  Falls back to one gemm_tc launch per
 // product when a product does not fit the specialisation.
-int gemm_tc_grouped(const adaptra_gemm_desc_t* gs, int n, cudaStream_t st) {
+int gemm_tc_grouped(const adaptra_gemm_desc_t* gs, int n, cudaStream_t st, const adaptra_gemm_desc_t* gs2) {
   constexpr int BN = 256;
   using Cfg = TcCfg<2, BN>;
   static const bool off = getenv("ADAPTRA_GEMM_GROUPED") && atoi(getenv("ADAPTRA_GEMM_GROUPED")) == 0;
   bool ok = !off && n > 0 && n <= kMaxGroup;
+  auto fits = [](const adaptra_gemm_desc_t& g) {
+    return g.dtype == ADAPTRA_BF16 && g.Z == 1 && g.epi == ADAPTRA_EPI_ACC_F32 && g.a_mn == 1 && g.b_mn == 1 &&
+           !g.causal && g.N >= 2048 && g.M >= 256 && (g.ldc % 4) == 0 && ((uintptr_t)g.C % 16) == 0 &&
+           (g.lda * 2) % 16 == 0 && (g.ldb * 2) % 16 == 0 && g.K % BK == 0;
+  };
   for (int i = 0; ok && i < n; ++i) {
-    const auto& g = gs[i];
-    ok = g.dtype == ADAPTRA_BF16 && g.Z == 1 && g.epi == ADAPTRA_EPI_ACC_F32 && g.a_mn == 1 && g.b_mn == 1 &&
-         !g.causal && g.N >= 2048 && g.M >= 256 && (g.ldc % 4) == 0 && ((uintptr_t)g.C % 16) == 0 &&
-         (g.lda * 2) % 16 == 0 && (g.ldb * 2) % 16 == 0;
+    ok = fits(gs[i]);
+    if (ok && gs2)
+      ok = fits(gs2[i]) && gs2[i].M == gs[i].M && gs2[i].N == gs[i].N && gs2[i].C == gs[i].C &&
+           gs2[i].ldc == gs[i].ldc && gs2[i].alpha == gs[i].alpha;
   }
   if (!ok) {
     for (int i = 0; i < n; ++i) {
       int rc = gemm_tc(gs[i], st);
+      if (!rc && gs2) rc = gemm_tc(gs2[i], st);
       if (rc) return rc;
     }
     return ADAPTRA_OK;
   }
-  static GroupArgs ga;  // host staging of the kernel parameter (9 KB); launches are serialised per process
+  static GroupArgs ga;  // host staging of the kernel parameter (15 KB); launches are serialised per process
   static std::mutex mu;
   std::lock_guard<std::mutex> lk(mu);
   memset(&ga, 0, sizeof(ga));
@@ -906,12 +916,20 @@ int gemm_tc_grouped(const adaptra_gemm_desc_t* gs, int n, cudaStream_t st) {
     if (!rc) rc = make_map(&ga.tmC[i], g.C, g.M, g.N, g.ldc, 32, 32, true, 128);
     if (rc) return rc;
     ga.m_blocks[i] = (g.M + Cfg::TM - 1) / Cfg::TM;
-    ga.k_blocks[i] = (g.K + BK - 1) / BK;
+    ga.k_blocks[i] = ga.k_split[i] = g.K / BK;
     ga.N[i] = g.N;
     ga.alpha[i] = g.alpha;
     ga.tile_start[i] = tiles;
     tiles += ga.m_blocks[i] * ((g.N + BN - 1) / BN);
     fl += 2.0 * g.M * (double)g.N * g.K;
+    if (gs2) {
+      const auto& h = gs2[i];
+      rc = make_map(&ga.tmA2[i], h.A, h.a_rows, h.a_cols, h.lda, 64, BK);
+      if (!rc) rc = make_map(&ga.tmB2[i], h.B, h.b_rows, h.b_cols, h.ldb, 64, BK);
+      if (rc) return rc;
+      ga.k_blocks[i] += h.K / BK;
+      fl += 2.0 * h.M * (double)h.N * h.K;
+    }
   }
   ga.tile_start[n] = tiles;
   ga.total_tiles = tiles;

@@ -407,15 +407,49 @@ struct StageOps {
     return ADAPTRA_OK;
   }
 
-  int Wop(int slot) {
+  // W of one slot, or of two slots (two consecutive W ops of the stage's
+  // order) as one launch whose products run over K = 2 b T: the fp32
+  // gradient is read-modified-written once per pair instead of once per
+  // microbatch, and every tile's epilogue is amortised over twice the K loop
+  int Wop(int slot, int slot_b = -1) {
+    std::vector<adaptra_gemm_desc_t> dw, dw_b;
+    std::vector<ColsumJob> cs;
+    collect_w(slot, dw, cs);
+    if (slot_b >= 0) collect_w(slot_b, dw_b, cs);
+    if (dt() == ADAPTRA_BF16) {
+      for (size_t i = 0; i < dw.size(); i += 24)
+        TRY(gemm_tc_grouped(dw.data() + i, (int)std::min<size_t>(24, dw.size() - i), st,
+                            slot_b >= 0 ? dw_b.data() + i : nullptr));
+    } else {
+      for (auto& g : dw) TRY(gemm_simt(g, st));
+      for (auto& g : dw_b) TRY(gemm_simt(g, st));
+    }
+    // Column sums: one launch per sum by default.  The grouped launch is 13 %
+    // faster on the W op alone but one ~17k-block kernel crowds co-located
+    // stages' streams (1 GPU, 4 stages: -1.4 % step; 1 stage per GPU: within
+    // noise), so it is opt-in (ADAPTRA_COLSUM_GROUPED=1).
+    static const bool cs_grouped = getenv("ADAPTRA_COLSUM_GROUPED") && atoi(getenv("ADAPTRA_COLSUM_GROUPED")) == 1;
+    const long R = s->R;
+    if (cs_grouped) {
+      TRY(colsum_grouped<T>(cs.data(), (int)cs.size(), (int)R, st));
+    } else {
+      for (const auto& j : cs) {
+        if (j.ln)
+          TRY(ln_param_grad<T>((const T*)j.y, (const T*)j.x, j.mean, j.rstd, j.out_a, j.out_b, (int)R, j.N, st));
+        else
+          TRY(col_sum<T>((const T*)j.y, j.out_a, (int)R, j.N, st));
+      }
+    }
+    return ADAPTRA_OK;
+  }
+
+  void collect_w(int slot, std::vector<adaptra_gemm_desc_t>& dw, std::vector<ColsumJob>& cs) {
     const auto& D = d();
     const long R = s->R, Dm = D.d, Ff = D.d_ff;
     // every dW += X^T dY product of the op is independent: collect them and run
-    // them as grouped persistent launches (bias / LN parameter sums inline)
-    std::vector<adaptra_gemm_desc_t> dw;
+    // them as grouped persistent launches (bias / LN parameter sums after)
     dw.reserve(4 * D.n_layers);
-    std::vector<ColsumJob> cs;  // bias and LN parameter gradients, one grouped launch
-    cs.reserve(6 * D.n_layers);
+    cs.reserve(cs.size() + 6 * D.n_layers);
     for (int l = D.n_layers - 1; l >= 0; --l) {
       ParamOff p = param_off(D, l);
       const T* dy = layer_dy(slot, l);
@@ -454,28 +488,6 @@ struct StageOps {
     }
     dw.erase(std::remove_if(dw.begin(), dw.end(), [](const adaptra_gemm_desc_t& g) { return g.M == 0 || g.N == 0; }),
              dw.end());
-    if (dt() == ADAPTRA_BF16) {
-      for (size_t i = 0; i < dw.size(); i += 24)
-        TRY(gemm_tc_grouped(dw.data() + i, (int)std::min<size_t>(24, dw.size() - i), st));
-    } else {
-      for (auto& g : dw) TRY(gemm_simt(g, st));
-    }
-    // Column sums: one launch per sum by default.  The grouped launch is 13 %
-    // faster on the W op alone but one ~17k-block kernel crowds co-located
-    // stages' streams (1 GPU, 4 stages: -1.4 % step; 1 stage per GPU: within
-    // noise), so it is opt-in (ADAPTRA_COLSUM_GROUPED=1).
-    static const bool cs_grouped = getenv("ADAPTRA_COLSUM_GROUPED") && atoi(getenv("ADAPTRA_COLSUM_GROUPED")) == 1;
-    if (cs_grouped) {
-      TRY(colsum_grouped<T>(cs.data(), (int)cs.size(), (int)R, st));
-    } else {
-      for (const auto& j : cs) {
-        if (j.ln)
-          TRY(ln_param_grad<T>((const T*)j.y, (const T*)j.x, j.mean, j.rstd, j.out_a, j.out_b, (int)R, j.N, st));
-        else
-          TRY(col_sum<T>((const T*)j.y, j.out_a, (int)R, j.N, st));
-      }
-    }
-    return ADAPTRA_OK;
   }
 };
 
@@ -604,6 +616,14 @@ extern "C" int adaptra_stage_W(adaptra_stage_t s, int32_t slot, void* stream) {
   if (!s || slot < 0 || slot >= s->d.n_slots || !s->dy_in[slot]) return set_error(ADAPTRA_EINVAL, "stage_W: bad args");
   if (s->d.dtype == ADAPTRA_BF16) return StageOps<bf16>{s, (cudaStream_t)stream}.Wop(slot);
   return StageOps<float>{s, (cudaStream_t)stream}.Wop(slot);
+}
+
+extern "C" int adaptra_stage_W2(adaptra_stage_t s, int32_t slot_a, int32_t slot_b, void* stream) {
+  if (!s || slot_a < 0 || slot_a >= s->d.n_slots || slot_b < 0 || slot_b >= s->d.n_slots || slot_a == slot_b ||
+      !s->dy_in[slot_a] || !s->dy_in[slot_b])
+    return set_error(ADAPTRA_EINVAL, "stage_W2: bad args");
+  if (s->d.dtype == ADAPTRA_BF16) return StageOps<bf16>{s, (cudaStream_t)stream}.Wop(slot_a, slot_b);
+  return StageOps<float>{s, (cudaStream_t)stream}.Wop(slot_a, slot_b);
 }
 
 extern "C" int adaptra_stage_zero_grads(adaptra_stage_t s, void* stream) {

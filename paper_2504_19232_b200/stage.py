@@ -116,6 +116,10 @@ class Stage:
     def W(self, slot, stream=None):
         L.check(L.lib().adaptra_stage_W(self.handle, slot, self._s(stream)))
 
+    def W2(self, slot_a, slot_b, stream=None):
+        """W of two slots as one launch (K = 2bT), adaptra_stage_W2."""
+        L.check(L.lib().adaptra_stage_W2(self.handle, slot_a, slot_b, self._s(stream)))
+
     def zero_grads(self, stream=None):
         L.check(L.lib().adaptra_stage_zero_grads(self.handle, self._s(stream)))
 

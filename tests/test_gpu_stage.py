@@ -35,9 +35,12 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("pairs", [False, True])
 @pytest.mark.parametrize("last", [False, True])
 @pytest.mark.parametrize("kind,dtype,nl,d,dff,H,b,T,nmb", CASES)
-def test_stage_fbw_vs_oracle(kind, dtype, nl, d, dff, H, b, T, nmb, last):
+def test_stage_fbw_vs_oracle(kind, dtype, nl, d, dff, H, b, T, nmb, last, pairs):
+    if pairs and nmb < 2:
+        pytest.skip("W pairs need two microbatches")
     bf = dtype == L.BF16
     params = (sy.mlp_params(0, 1, nl, d, dff, bf16=bf) if kind == "mlp"
               else sy.gpt_params(0, 1, nl, d, dff, perturb=True, bf16=bf))[0]
@@ -60,7 +63,13 @@ def test_stage_fbw_vs_oracle(kind, dtype, nl, d, dff, H, b, T, nmb, last):
         st.F(j, xin[j], ys[j], tgt[j] if last else None, loss if last else None)
     for j in range(nmb):
         st.B(j, None if last else dyin[j], dxs[j])
-        st.W(j)
+        if not pairs:
+            st.W(j)
+    if pairs:                   # W of slots (0,1), (2,3), ... as K = 2bT launches
+        for j in range(0, nmb - 1, 2):
+            st.W2(j, j + 1)
+        if nmb % 2:
+            st.W(nmb - 1)
     torch.cuda.synchronize()
     # oracle
     tol = TOL[dtype]

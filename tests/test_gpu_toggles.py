@@ -14,11 +14,15 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.mark.parametrize("toggle", [{"ADAPTRA_COLSUM_GROUPED": "1"},
                                     {"ADAPTRA_GEMM_GROUPED": "0"},
-                                    {"ADAPTRA_EPI_IN_LDG": "1"}])
+                                    {"ADAPTRA_EPI_IN_LDG": "1"},
+                                    {"ADAPTRA_W_PAIRS": "0"}])
 def test_stage_parity_under_toggle(toggle):
     env = dict(os.environ, **toggle)
-    cmd = [sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
-           os.path.join(ROOT, "tests/test_gpu_stage.py"), os.path.join(ROOT, "tests/test_gpu_fullsize.py")]
+    files = ["tests/test_gpu_stage.py", "tests/test_gpu_fullsize.py"]
+    if "ADAPTRA_W_PAIRS" in toggle:        # an executor toggle: the pipelined iterations
+        files = ["tests/test_gpu_pipeline.py"]
+    cmd = [sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider"] + [
+        os.path.join(ROOT, f) for f in files]
     r = subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True, timeout=900)
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0
