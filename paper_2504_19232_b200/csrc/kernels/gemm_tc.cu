@@ -46,7 +46,7 @@ constexpr int kWarpProducer = 8, kWarpMma = 9;
 template <int CG, int BN>
 struct TcCfg {
   static constexpr int kBRows = BN / CG;        // B rows held by each CTA
-  static constexpr int kStages = CG == 2 ? 5 : (BN == 256 ? 3 : 5);
+  static constexpr int kStages = CG == 2 ? (BN == 256 ? 5 : 6) : (BN == 256 ? 3 : 5);
   static constexpr int kABytes = BM * BK * 2;    // 16 KB
   static constexpr int kBBytes = kBRows * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
@@ -982,6 +982,23 @@ int gemm_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
   }();
   const bool big = (g.Z == 1 && g.N >= 2048 && g.M >= 256 && g.causal == ADAPTRA_CAUSAL_NONE);
   const int key = g.a_mn * 2 + g.b_mn;
+  // CTA-pair tile width: 256 x 128 tiles by default -- twice the tiles of
+  // 256 x 256, so the stage GEMMs (64-256 wide tiles at T = 2048) fill the 74
+  // pairs in finer waves and most pairs run >= 2 tiles, whose epilogues then
+  // overlap the next tile's main loop; 256 x 256 for the fused row-dot (one
+  // head per epilogue warp) or with ADAPTRA_GEMM_BN=256
+  static const int bn_pref = [] {
+    const char* v = getenv("ADAPTRA_GEMM_BN");
+    return v ? atoi(v) : 128;
+  }();
+  if (big && mode == 1 && bn_pref == 128 && g.epi != ADAPTRA_EPI_STORE_ROWDOT) {
+    switch (key) {
+      case 0: return launch_tc<2, 128, 0, 0>(g, st);
+      case 1: return launch_tc<2, 128, 0, 1>(g, st);
+      case 2: return launch_tc<2, 128, 1, 0>(g, st);
+      default: return launch_tc<2, 128, 1, 1>(g, st);
+    }
+  }
   if (big && mode == 1) {
     switch (key) {
       case 0: return launch_tc<2, 256, 0, 0>(g, st);

@@ -166,8 +166,8 @@ def test_host_io_end_to_end_matches_device_path():
 @pytest.mark.parametrize("arm", ["zb", "adaptive"])
 @pytest.mark.parametrize("kind,dtype,S,N,Lt,d,dff,H,b,T,tol", CFGS)
 def test_stash_offload_matches_device_run(kind, dtype, S, N, Lt, d, dff, H, b, T, tol, arm):
-    """N4: with 3 device F->W slots per stage and the rest in a
-    pinned host pool (Belady spills after B, prefetch before W), the iteration
+    """N4: with as few device F->W slots per stage as the order
+    allows (its peak in-flight forwards) and the rest in a pinned host pool (Belady spills after B, prefetch before W), the iteration
     gives the same loss and gradients as with every slot on the device (bit
     for bit) and as the oracle's full batch; the plan really spilled."""
     ref_pipe, Lref, gref = _setup(kind, dtype, S, N, Lt, d, dff, H, b, T)
@@ -183,7 +183,18 @@ def test_stash_offload_matches_device_run(kind, dtype, S, N, Lt, d, dff, H, b, T
         ref_grads = {i: st.grads() for i, st in ref_pipe.stages.items()}
     finally:
         ref_pipe.close()
-    pipe, _, _ = _setup(kind, dtype, S, N, Lt, d, dff, H, b, T, n_slots=3)
+    # device slots per stage = the order's peak in-flight forwards (F - B):
+    # only slots whose B is done can move to the host; the F->W demand is N
+    peak = []
+    for ops in orders:
+        f = bb = p = 0
+        for k, _ in ops:
+            f += k == "F"
+            bb += k == "B"
+            p = max(p, f - bb)
+        peak.append(max(p, 1))
+    assert min(peak) < N
+    pipe, _, _ = _setup(kind, dtype, S, N, Lt, d, dff, H, b, T, n_slots=peak)
     try:
         pipe.enable_offload(N, window=2)
         if arm == "adaptive":
