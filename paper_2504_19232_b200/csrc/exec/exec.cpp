@@ -453,7 +453,10 @@ struct adaptra_exec {
         // two consecutive W ops of the order run as one launch over K = 2bT
         // (adaptra_stage_W2): same work, half the fp32 gradient traffic; the
         // pair's time is booked on the first op (the second gets zero length)
-        if (w_pairs && !merge && q + 1 < ops.size() && ops[q + 1].kind == ADAPTRA_OP_W && P.slot[q + 1] >= 0) {
+        // (not when the offload plan issues copies between the two: the second
+        // W's slot may be refilled right after the first one frees it)
+        if (w_pairs && !merge && q + 1 < ops.size() && ops[q + 1].kind == ADAPTRA_OP_W && P.slot[q + 1] >= 0 &&
+            P.slot[q + 1] != slot && P.after[q].empty()) {
           if ((rc = pre_op(q + 1))) return rc;
           ADAPTRA_CUDA_TRY(cudaEventRecord(ev_s[q], cs));
           if ((rc = adaptra_stage_W2(d.stage, slot, P.slot[q + 1], cs))) return rc;

@@ -13,8 +13,8 @@
 //   dK += dS^T Q_i, dQ_i^T(partial) = K^T dS_i^T (TMEM) -> TMA reduce-add into
 //   an fp32 dQ^T accumulator.  D_i = rowsum(dO_i o O_i) comes from the epilogue
 //   of the GEMM that produces dO (EPI_STORE_ROWDOT; attn_rowdot elsewhere).
-// Warp roles: 0 TMA producer, 1 TMEM allocator + MMA issuer; forward: 2..9
-// softmax / epilogue warps (lane quadrant x column half); backward: 2..17
+// Warp roles: 0 TMA producer, 1 TMEM allocator + MMA issuer; forward: 2..17
+// softmax / epilogue warps (lane quadrant x column quarter); backward: 2..17
 // gradient warps (lane quadrant x 16-query column group), 18..21 dQ^T drain
 // warps (thread = TMEM lane = tile row).
 #include <cuda.h>
@@ -98,8 +98,9 @@ struct AttnArgs {
 }  // namespace
 
 // ============================================================== forward
-constexpr int kAttnThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 softmax
-constexpr int kFwdRing = 5;        // forward K/V tile ring (~2.5 key blocks of TMA lead)
+constexpr int kSoftWarps = 16;     // 4 per TMEM lane quadrant, each owning 32 of a row's 128 columns
+constexpr int kAttnThreads = 64 + 32 * kSoftWarps;  // warp 0 TMA, warp 1 MMA, warps 2..17 softmax
+constexpr int kFwdRing = 4;        // forward K/V tile ring (2 key blocks of TMA lead)
 constexpr float kLog2e = 1.4426950408889634f;
 
 __device__ __forceinline__ long long gtimer() {
@@ -143,8 +144,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint8_t* sQ = smem;                       // 32 KB
   uint8_t* sRing = sQ + TILE;               // kFwdRing x 32 KB: K V K V ... (tile n in slot n % kFwdRing)
   uint8_t* sP = sRing + kFwdRing * TILE;    // 32 KB
-  float* sMax = (float*)(sP + TILE);        // [2 (block parity)][2 halves][128] half-row maxima
-  uint64_t* bar = (uint64_t*)(sMax + 4 * AT);
+  float* sMax = (float*)(sP + TILE);        // [2 (block parity)][4 quarters][128] quarter-row maxima
+  uint64_t* bar = (uint64_t*)(sMax + 8 * AT);
   uint64_t* q_full = bar + 0;
   uint64_t* t_full = bar + 1;               // [kFwdRing] tile landed
   uint64_t* t_empty = t_full + kFwdRing;    // [kFwdRing] tile consumed by its MMA
@@ -171,9 +172,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 8);
+      mbar_init(&s_empty[i], kSoftWarps);
     }
-    mbar_init(p_full, 8);
+    mbar_init(p_full, kSoftWarps);
     mbar_init(p_empty, 1);
     mbar_init(o_full, 1);
     fence_barrier_init();
@@ -280,18 +281,20 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       item = next;
     }
   } else {
-    // softmax warps: lane quadrant quad (rows), column half (64 keys / head dims).
-    // Online softmax in log2 units against a reference max mref shared by the
-    // two halves of a row (exchanged through sMax every block).  mref moves
-    // only when the running max exceeds it by more than 8, so P <= 2^8 and the
-    // O accumulator in TMEM is rescaled rarely (then by this thread's half).
-    // The next item's first P V (which overwrites O) waits for p_full, which
-    // these warps arrive only after reading O in the epilogue.
-    const int quad = warp & 3, half = (warp - 2) >> 2;
+    // softmax warps: lane quadrant quad (rows), column quarter (32 keys / head
+    // dims): 4 warps per SM sub-partition, so the MUFU / FMA latency of one
+    // warp's exponentials hides behind the others'.  Online softmax in log2
+    // units against a reference max mref shared by the four quarters of a row
+    // (exchanged through sMax every block).  mref moves only when the running
+    // max exceeds it by more than 8, so P <= 2^8 and the O accumulator in TMEM
+    // is rescaled rarely (then by this thread's quarter).  The next item's
+    // first P V (which overwrites O) waits for p_full, which these warps arrive
+    // only after reading O in the epilogue.
+    const int quad = warp & 3, qtr = (warp - 2) >> 2;
     const int r = quad * 32 + lane;           // row within the query block
-    const uint32_t lanes = ((uint32_t)(quad * 32) << 16) + half * 64;
+    const uint32_t lanes = ((uint32_t)(quad * 32) << 16) + qtr * 32;
     const float c2 = a.scale * kLog2e;        // scores in log2 units
-    const int pair_bar = 1 + quad;            // warps quad (half 0) and quad (half 1)
+    const int row_bar = 1 + quad;             // the 4 warps of lane quadrant quad
     int g = 0;
     for (int rr = 0, it = 0;; ++rr, ++it) {
       const int item = fwd_item(rr, cta, G);
@@ -304,100 +307,87 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const int sb = g & 1;
         mbar_wait(&s_full[sb], (g >> 1) & 1);
         tc_fence_after();
-        uint32_t r0[32], r1[32];
+        uint32_t r0[32];
         tmem_ld32(tmem + sb * 128 + lanes, r0);
-        tmem_ld32(tmem + sb * 128 + lanes + 32, r1);
         tmem_ld_wait_regs(r0);
-        tmem_ld_wait_regs(r1);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[sb]);
         if (j == qb) {
-          const int lim = qi - (j * AT + half * 64);  // last visible column of this half
+          const int lim = qi - (j * AT + qtr * 32);  // last visible column of this quarter
 #pragma unroll
-          for (int t = 0; t < 32; ++t) {
+          for (int t = 0; t < 32; ++t)
             if (t > lim) r0[t] = __float_as_uint(-INFINITY);
-            if (t + 32 > lim) r1[t] = __float_as_uint(-INFINITY);
-          }
         }
-        float cm = fmaxf(__uint_as_float(r0[0]), __uint_as_float(r1[0]));
+        float cm = __uint_as_float(r0[0]);
 #pragma unroll
-        for (int t = 1; t < 32; ++t) cm = fmaxf(cm, fmaxf(__uint_as_float(r0[t]), __uint_as_float(r1[t])));
-        float* mx = sMax + sb * 2 * AT;
-        mx[half * AT + r] = cm;
-        named_sync(pair_bar, 64);
+        for (int t = 1; t < 32; ++t) cm = fmaxf(cm, __uint_as_float(r0[t]));
+        float* mx = sMax + sb * 4 * AT;
+        mx[qtr * AT + r] = cm;
+        named_sync(row_bar, 128);
         // every row has key 0 <= qi in block 0 and key j*128 <= qi in block j: mb is finite
-        const float mb = fmaxf(cm, mx[(half ^ 1) * AT + r]) * c2;
+        const float mb = fmaxf(fmaxf(mx[r], mx[AT + r]), fmaxf(mx[2 * AT + r], mx[3 * AT + r])) * c2;
         const bool resc = mb > mref + 8.f;
         float alpha = 1.f;
         if (resc) {
           alpha = ex2(mref - mb);  // 0 on the first block
           mref = mb;
         }
-        uint32_t pk[32];  // P row half as bf16x2
+        uint32_t pk[16];  // P row quarter as bf16x2
         float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
-        for (int t = 0; t < 32; t += 2) {
+        for (int t = 0; t < 32; t += 4) {
           const float e0 = ex2(fmaf(__uint_as_float(r0[t]), c2, -mref));
           const float e1 = ex2(fmaf(__uint_as_float(r0[t + 1]), c2, -mref));
-          const float e2 = ex2(fmaf(__uint_as_float(r1[t]), c2, -mref));
-          const float e3 = ex2(fmaf(__uint_as_float(r1[t + 1]), c2, -mref));
+          const float e2 = ex2(fmaf(__uint_as_float(r0[t + 2]), c2, -mref));
+          const float e3 = ex2(fmaf(__uint_as_float(r0[t + 3]), c2, -mref));
           acc0 += e0 + e1;
           acc1 += e2 + e3;
           pk[t >> 1] = pack_bf16x2(e0, e1);
-          pk[16 + (t >> 1)] = pack_bf16x2(e2, e3);
+          pk[(t >> 1) + 1] = pack_bf16x2(e2, e3);
         }
         l = l * alpha + (acc0 + acc1);
         mbar_wait(p_empty, (g & 1) ^ 1);  // P V of the previous block done: O stable, P buffer free
         if (j > 0 && __any_sync(0xffffffffu, resc)) {
           tc_fence_after();
+          uint32_t o[32];
+          tmem_ld32(tO + lanes, o);
+          tmem_ld_wait_regs(o);
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            uint32_t o[32];
-            tmem_ld32(tO + lanes + 32 * c, o);
-            tmem_ld_wait_regs(o);
-#pragma unroll
-            for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * alpha);
-            tmem_st32(tO + lanes + 32 * c, o);
-          }
+          for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * alpha);
+          tmem_st32(tO + lanes, o);
           tmem_st_wait();
         }
-        st_tile_row32_packed(smem_u32(sP), r, half * 64, pk);
-        st_tile_row32_packed(smem_u32(sP), r, half * 64 + 32, pk + 16);
+        st_tile_row32_packed(smem_u32(sP), r, qtr * 32, pk);
         fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full);
       }
-      // ---- epilogue: O / l -> bf16 (this half of the head dims), LSE (log2 units).
-      // The row sums are exchanged through the sMax buffer of the parity the
-      // last block did not use (both halves finished reading it before the last
-      // block's barrier); the second barrier keeps the next item's first block,
-      // which writes that buffer, behind both reads.
-      float* sL = sMax + (g & 1) * 2 * AT;
-      sL[half * AT + r] = l;
-      named_sync(pair_bar, 64);
-      const float ltot = sL[r] + sL[AT + r];
-      named_sync(pair_bar, 64);
+      // ---- epilogue: O / l -> bf16 (this quarter of the head dims), LSE (log2
+      // units).  The row sums are exchanged through the sMax buffer of the
+      // parity the last block did not use (all quarters finished reading it
+      // before the last block's barrier); the second barrier keeps the next
+      // item's first block, which writes that buffer, behind all reads.
+      float* sL = sMax + (g & 1) * 4 * AT;
+      sL[qtr * AT + r] = l;
+      named_sync(row_bar, 128);
+      const float ltot = (sL[r] + sL[AT + r]) + (sL[2 * AT + r] + sL[3 * AT + r]);
+      named_sync(row_bar, 128);
       const float inv = 1.f / ltot;
       mbar_wait(o_full, it & 1);
       tc_fence_after();
-      uint32_t r0[32], r1[32];
+      uint32_t r0[32];
       tmem_ld32(tO + lanes, r0);
-      tmem_ld32(tO + lanes + 32, r1);
       tmem_ld_wait_regs(r0);
-      tmem_ld_wait_regs(r1);
       tc_fence_before();
-      bf16* orow = a.o + (size_t)(row0 + qi) * a.d + h * AT + half * 64;
-      float v[64];
+      bf16* orow = a.o + (size_t)(row0 + qi) * a.d + h * AT + qtr * 32;
+      float v[32];
 #pragma unroll
-      for (int t = 0; t < 32; ++t) {
-        v[t] = __uint_as_float(r0[t]) * inv;
-        v[32 + t] = __uint_as_float(r1[t]) * inv;
-      }
+      for (int t = 0; t < 32; ++t) v[t] = __uint_as_float(r0[t]) * inv;
 #pragma unroll
-      for (int t = 0; t < 64; t += 8) st_bf16x8(orow + t, v + t);
-      if (half == 0) a.lse[(size_t)z * a.T + qi] = mref + __log2f(ltot);
+      for (int t = 0; t < 32; t += 8) st_bf16x8(orow + t, v + t);
+      if (qtr == 0) a.lse[(size_t)z * a.T + qi] = mref + __log2f(ltot);
     }
   }
   tc_fence_before();
@@ -853,7 +843,7 @@ static int check_launch(const char* w) {
   return ADAPTRA_OK;
 }
 
-constexpr int kFwdSmem = (kFwdRing + 2) * TILE + 4 * AT * 4 + 256;
+constexpr int kFwdSmem = (kFwdRing + 2) * TILE + 8 * AT * 4 + 256;
 static_assert(kFwdSmem <= 232448, "attn fwd shared memory");
 constexpr int kBwdSmem = 2 * TILE + (2 * NQS + 2) * QTILE + 4 * 4096 + 2 * NQS * QB * 4 + 256;
 static_assert(kBwdSmem <= 232448, "attn bwd shared memory");

@@ -982,14 +982,14 @@ int gemm_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
   }();
   const bool big = (g.Z == 1 && g.N >= 2048 && g.M >= 256 && g.causal == ADAPTRA_CAUSAL_NONE);
   const int key = g.a_mn * 2 + g.b_mn;
-  // CTA-pair tile width: 256 x 128 tiles by default -- twice the tiles of
-  // 256 x 256, so the stage GEMMs (64-256 wide tiles at T = 2048) fill the 74
-  // pairs in finer waves and most pairs run >= 2 tiles, whose epilogues then
-  // overlap the next tile's main loop; 256 x 256 for the fused row-dot (one
-  // head per epilogue warp) or with ADAPTRA_GEMM_BN=256
+  // CTA-pair tile width 256 (default).  256 x 128 tiles (ADAPTRA_GEMM_BN=128)
+  // give finer waves over the 74 pairs but were measured 1.3-1.6x slower on
+  // every C1 stage shape (profiles/r02_gemm_bn128_vs_bn256.txt): an M = 256,
+  // N = 128 MMA moves the same A operand from shared memory for half the
+  // FLOPs, so the main loop runs at about half the tensor rate.
   static const int bn_pref = [] {
     const char* v = getenv("ADAPTRA_GEMM_BN");
-    return v ? atoi(v) : 128;
+    return v ? atoi(v) : 256;
   }();
   if (big && mode == 1 && bn_pref == 128 && g.epi != ADAPTRA_EPI_STORE_ROWDOT) {
     switch (key) {
