@@ -13,8 +13,8 @@
 //   dK += dS^T Q_i, dQ_i^T(partial) = K^T dS_i^T (TMEM) -> TMA reduce-add into
 //   an fp32 dQ^T accumulator.  D_i = rowsum(dO_i o O_i) comes from the epilogue
 //   of the GEMM that produces dO (EPI_STORE_ROWDOT; attn_rowdot elsewhere).
-// Warp roles: 0 TMA producer, 1 TMEM allocator + MMA issuer; forward: 2..17
-// softmax / epilogue warps (lane quadrant x column quarter); backward: 2..17
+// Warp roles: 0 TMA producer, 1 TMEM allocator + MMA issuer; forward: 2..9
+// (or 2..17) softmax / epilogue warps (lane quadrant x column group); backward: 2..17
 // gradient warps (lane quadrant x 16-query column group), 18..21 dQ^T drain
 // warps (thread = TMEM lane = tile row).
 #include <cuda.h>
@@ -80,6 +80,13 @@ __device__ __forceinline__ void st_tile_row32_packed(uint32_t tile, int r, int c
     sts128(row + (((p0 + q) ^ (r & 7)) << 4), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
 }
 
+// wait for this thread's outstanding tcgen05.ld into r[0..N) (N multiple of 32)
+template <int N>
+__device__ __forceinline__ void tmem_ld_wait_regs_n(uint32_t (&r)[N]) {
+#pragma unroll
+  for (int c = 0; c < N / 32; ++c) tmem_ld_wait_regs(*reinterpret_cast<uint32_t(*)[32]>(&r[32 * c]));
+}
+
 struct AttnArgs {
   int b, H, T, d;        // sequences, heads, tokens per sequence, model width (= H * 128)
   float scale;           // 1 / sqrt(dh)
@@ -98,9 +105,17 @@ struct AttnArgs {
 }  // namespace
 
 // ============================================================== forward
-constexpr int kSoftWarps = 16;     // 4 per TMEM lane quadrant, each owning 32 of a row's 128 columns
-constexpr int kAttnThreads = 64 + 32 * kSoftWarps;  // warp 0 TMA, warp 1 MMA, warps 2..17 softmax
-constexpr int kFwdRing = 4;        // forward K/V tile ring (2 key blocks of TMA lead)
+// Softmax warps: NQ per TMEM lane quadrant, each owning 128 / NQ of a row's
+// 128 columns (NQ = 2: 8 warps, 64 columns per thread; NQ = 4: 16 warps, 32
+// columns, 4 warps per SM sub-partition; $ADAPTRA_ATTN_FWD_WARPS = 8 | 16).
+template <int NQ>
+struct FwdCfg {
+  static constexpr int kSoftWarps = 4 * NQ;
+  static constexpr int kThreads = 64 + 32 * kSoftWarps;  // warp 0 TMA, warp 1 MMA, then softmax
+  static constexpr int kRing = NQ == 2 ? 5 : 4;         // K/V tile ring (2.5 / 2 key blocks of TMA lead)
+  static constexpr int kCols = 128 / NQ;                 // columns per softmax thread
+  static constexpr int kSmem = (kRing + 2) * TILE + 2 * NQ * AT * 4 + 256;
+};
 constexpr float kLog2e = 1.4426950408889634f;
 
 __device__ __forceinline__ long long gtimer() {
@@ -136,16 +151,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // 26 % of the SM time with one CTA per item, diag 0x400).
 __device__ __forceinline__ int fwd_item(int r, int c, int G) { return (r & 1) ? (r + 1) * G - 1 - c : r * G + c; }
 
-__global__ void __launch_bounds__(kAttnThreads, 1)
+template <int NQ>
+__global__ void __launch_bounds__(FwdCfg<NQ>::kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const AttnArgs a) {
+  constexpr int kFwdRing = FwdCfg<NQ>::kRing, kSoftWarps = FwdCfg<NQ>::kSoftWarps, CW = FwdCfg<NQ>::kCols;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;  // no static shared memory: the window starts 1024-aligned (checked)
   if (threadIdx.x == 0 && (smem_u32(smem) & 1023)) __trap();
   uint8_t* sQ = smem;                       // 32 KB
   uint8_t* sRing = sQ + TILE;               // kFwdRing x 32 KB: K V K V ... (tile n in slot n % kFwdRing)
   uint8_t* sP = sRing + kFwdRing * TILE;    // 32 KB
-  float* sMax = (float*)(sP + TILE);        // [2 (block parity)][4 quarters][128] quarter-row maxima
-  uint64_t* bar = (uint64_t*)(sMax + 8 * AT);
+  float* sMax = (float*)(sP + TILE);        // [2 (block parity)][NQ column groups][128] partial row maxima
+  uint64_t* bar = (uint64_t*)(sMax + 2 * NQ * AT);
   uint64_t* q_full = bar + 0;
   uint64_t* t_full = bar + 1;               // [kFwdRing] tile landed
   uint64_t* t_empty = t_full + kFwdRing;    // [kFwdRing] tile consumed by its MMA
@@ -281,20 +298,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       item = next;
     }
   } else {
-    // softmax warps: lane quadrant quad (rows), column quarter (32 keys / head
-    // dims): 4 warps per SM sub-partition, so the MUFU / FMA latency of one
-    // warp's exponentials hides behind the others'.  Online softmax in log2
-    // units against a reference max mref shared by the four quarters of a row
-    // (exchanged through sMax every block).  mref moves only when the running
-    // max exceeds it by more than 8, so P <= 2^8 and the O accumulator in TMEM
-    // is rescaled rarely (then by this thread's quarter).  The next item's
-    // first P V (which overwrites O) waits for p_full, which these warps arrive
-    // only after reading O in the epilogue.
+    // softmax warps: lane quadrant quad (rows), column group qtr (CW keys /
+    // head dims).  Online softmax in log2 units against a reference max mref
+    // shared by the NQ groups of a row (exchanged through sMax every block).
+    // mref moves only when the running max exceeds it by more than 8, so
+    // P <= 2^8 and the O accumulator in TMEM is rescaled rarely (then by this
+    // thread's group).  The next item's first P V (which overwrites O) waits
+    // for p_full, which these warps arrive only after reading O in the epilogue.
     const int quad = warp & 3, qtr = (warp - 2) >> 2;
     const int r = quad * 32 + lane;           // row within the query block
-    const uint32_t lanes = ((uint32_t)(quad * 32) << 16) + qtr * 32;
+    const uint32_t lanes = ((uint32_t)(quad * 32) << 16) + qtr * CW;
     const float c2 = a.scale * kLog2e;        // scores in log2 units
-    const int row_bar = 1 + quad;             // the 4 warps of lane quadrant quad
+    const int row_bar = 1 + quad;             // the NQ warps of lane quadrant quad
     int g = 0;
     for (int rr = 0, it = 0;; ++rr, ++it) {
       const int item = fwd_item(rr, cta, G);
@@ -307,40 +322,44 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const int sb = g & 1;
         mbar_wait(&s_full[sb], (g >> 1) & 1);
         tc_fence_after();
-        uint32_t r0[32];
-        tmem_ld32(tmem + sb * 128 + lanes, r0);
-        tmem_ld_wait_regs(r0);
+        uint32_t rv[CW];
+#pragma unroll
+        for (int c = 0; c < CW / 32; ++c) tmem_ld32(tmem + sb * 128 + lanes + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(&rv[32 * c]));
+        tmem_ld_wait_regs_n<CW>(rv);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[sb]);
         if (j == qb) {
-          const int lim = qi - (j * AT + qtr * 32);  // last visible column of this quarter
+          const int lim = qi - (j * AT + qtr * CW);  // last visible column of this group
 #pragma unroll
-          for (int t = 0; t < 32; ++t)
-            if (t > lim) r0[t] = __float_as_uint(-INFINITY);
+          for (int t = 0; t < CW; ++t)
+            if (t > lim) rv[t] = __float_as_uint(-INFINITY);
         }
-        float cm = __uint_as_float(r0[0]);
+        float cm = __uint_as_float(rv[0]);
 #pragma unroll
-        for (int t = 1; t < 32; ++t) cm = fmaxf(cm, __uint_as_float(r0[t]));
-        float* mx = sMax + sb * 4 * AT;
+        for (int t = 1; t < CW; ++t) cm = fmaxf(cm, __uint_as_float(rv[t]));
+        float* mx = sMax + sb * NQ * AT;
         mx[qtr * AT + r] = cm;
-        named_sync(row_bar, 128);
+        named_sync(row_bar, 32 * NQ);
         // every row has key 0 <= qi in block 0 and key j*128 <= qi in block j: mb is finite
-        const float mb = fmaxf(fmaxf(mx[r], mx[AT + r]), fmaxf(mx[2 * AT + r], mx[3 * AT + r])) * c2;
+        float mall = mx[r];
+#pragma unroll
+        for (int k = 1; k < NQ; ++k) mall = fmaxf(mall, mx[k * AT + r]);
+        const float mb = mall * c2;
         const bool resc = mb > mref + 8.f;
         float alpha = 1.f;
         if (resc) {
           alpha = ex2(mref - mb);  // 0 on the first block
           mref = mb;
         }
-        uint32_t pk[16];  // P row quarter as bf16x2
+        uint32_t pk[CW / 2];  // P row group as bf16x2
         float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
-        for (int t = 0; t < 32; t += 4) {
-          const float e0 = ex2(fmaf(__uint_as_float(r0[t]), c2, -mref));
-          const float e1 = ex2(fmaf(__uint_as_float(r0[t + 1]), c2, -mref));
-          const float e2 = ex2(fmaf(__uint_as_float(r0[t + 2]), c2, -mref));
-          const float e3 = ex2(fmaf(__uint_as_float(r0[t + 3]), c2, -mref));
+        for (int t = 0; t < CW; t += 4) {
+          const float e0 = ex2(fmaf(__uint_as_float(rv[t]), c2, -mref));
+          const float e1 = ex2(fmaf(__uint_as_float(rv[t + 1]), c2, -mref));
+          const float e2 = ex2(fmaf(__uint_as_float(rv[t + 2]), c2, -mref));
+          const float e3 = ex2(fmaf(__uint_as_float(rv[t + 3]), c2, -mref));
           acc0 += e0 + e1;
           acc1 += e2 + e3;
           pk[t >> 1] = pack_bf16x2(e0, e1);
@@ -350,43 +369,50 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         mbar_wait(p_empty, (g & 1) ^ 1);  // P V of the previous block done: O stable, P buffer free
         if (j > 0 && __any_sync(0xffffffffu, resc)) {
           tc_fence_after();
-          uint32_t o[32];
-          tmem_ld32(tO + lanes, o);
-          tmem_ld_wait_regs(o);
 #pragma unroll
-          for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * alpha);
-          tmem_st32(tO + lanes, o);
+          for (int c = 0; c < CW / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld32(tO + lanes + 32 * c, o);
+            tmem_ld_wait_regs(o);
+#pragma unroll
+            for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * alpha);
+            tmem_st32(tO + lanes + 32 * c, o);
+          }
           tmem_st_wait();
         }
-        st_tile_row32_packed(smem_u32(sP), r, qtr * 32, pk);
+#pragma unroll
+        for (int c = 0; c < CW / 32; ++c) st_tile_row32_packed(smem_u32(sP), r, qtr * CW + 32 * c, pk + 16 * c);
         fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full);
       }
-      // ---- epilogue: O / l -> bf16 (this quarter of the head dims), LSE (log2
+      // ---- epilogue: O / l -> bf16 (this group of the head dims), LSE (log2
       // units).  The row sums are exchanged through the sMax buffer of the
-      // parity the last block did not use (all quarters finished reading it
+      // parity the last block did not use (all groups finished reading it
       // before the last block's barrier); the second barrier keeps the next
       // item's first block, which writes that buffer, behind all reads.
-      float* sL = sMax + (g & 1) * 4 * AT;
+      float* sL = sMax + (g & 1) * NQ * AT;
       sL[qtr * AT + r] = l;
-      named_sync(row_bar, 128);
-      const float ltot = (sL[r] + sL[AT + r]) + (sL[2 * AT + r] + sL[3 * AT + r]);
-      named_sync(row_bar, 128);
+      named_sync(row_bar, 32 * NQ);
+      float ltot = 0.f;
+#pragma unroll
+      for (int k = 0; k < NQ; ++k) ltot += sL[k * AT + r];
+      named_sync(row_bar, 32 * NQ);
       const float inv = 1.f / ltot;
       mbar_wait(o_full, it & 1);
       tc_fence_after();
-      uint32_t r0[32];
-      tmem_ld32(tO + lanes, r0);
-      tmem_ld_wait_regs(r0);
+      uint32_t rv[CW];
+#pragma unroll
+      for (int c = 0; c < CW / 32; ++c) tmem_ld32(tO + lanes + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(&rv[32 * c]));
+      tmem_ld_wait_regs_n<CW>(rv);
       tc_fence_before();
-      bf16* orow = a.o + (size_t)(row0 + qi) * a.d + h * AT + qtr * 32;
-      float v[32];
+      bf16* orow = a.o + (size_t)(row0 + qi) * a.d + h * AT + qtr * CW;
+      float v[CW];
 #pragma unroll
-      for (int t = 0; t < 32; ++t) v[t] = __uint_as_float(r0[t]) * inv;
+      for (int t = 0; t < CW; ++t) v[t] = __uint_as_float(rv[t]) * inv;
 #pragma unroll
-      for (int t = 0; t < 32; t += 8) st_bf16x8(orow + t, v + t);
+      for (int t = 0; t < CW; t += 8) st_bf16x8(orow + t, v + t);
       if (qtr == 0) a.lse[(size_t)z * a.T + qi] = mref + __log2f(ltot);
     }
   }
@@ -843,8 +869,7 @@ static int check_launch(const char* w) {
   return ADAPTRA_OK;
 }
 
-constexpr int kFwdSmem = (kFwdRing + 2) * TILE + 8 * AT * 4 + 256;
-static_assert(kFwdSmem <= 232448, "attn fwd shared memory");
+static_assert(FwdCfg<2>::kSmem <= 232448 && FwdCfg<4>::kSmem <= 232448, "attn fwd shared memory");
 constexpr int kBwdSmem = 2 * TILE + (2 * NQS + 2) * QTILE + 4 * 4096 + 2 * NQS * QB * 4 + 256;
 static_assert(kBwdSmem <= 232448, "attn bwd shared memory");
 
@@ -897,11 +922,16 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
   CUtensorMap m;
   int rc = map2d(&m, qkv, (int64_t)b * T, 3LL * d, 3LL * d, 2, 64, AT, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
+  static const int nq = [] {
+    const char* v = getenv("ADAPTRA_ATTN_FWD_WARPS");
+    return (v && atoi(v) == 16) ? 4 : 2;
+  }();
   static std::atomic<unsigned> attr{0};  // per device; stage threads may race here
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(attr.load(std::memory_order_acquire) & (1u << dev))) {
-    cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem);
+    cudaFuncSetAttribute(attn_fwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
+    cudaFuncSetAttribute(attn_fwd_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<4>::kSmem);
     attr.fetch_or(1u << dev, std::memory_order_release);
   }
   AttnArgs a{};
@@ -920,7 +950,10 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
   // ADAPTRA_ATTN_FWD_GRID=items: one CTA per item (the non-persistent launch, for comparison)
   static const bool per_item = getenv("ADAPTRA_ATTN_FWD_GRID") && !strcmp(getenv("ADAPTRA_ATTN_FWD_GRID"), "items");
   const int items = b * H * (T / AT), grid = per_item ? items : std::min(items, n_sm[dev & 31]);
-  attn_fwd_kernel<<<grid, kAttnThreads, kFwdSmem, st>>>(m, a);
+  if (nq == 4)
+    attn_fwd_kernel<4><<<grid, FwdCfg<4>::kThreads, FwdCfg<4>::kSmem, st>>>(m, a);
+  else
+    attn_fwd_kernel<2><<<grid, FwdCfg<2>::kThreads, FwdCfg<2>::kSmem, st>>>(m, a);
   if (fdiag & 0x400) {
     g_nqb = T / AT; g_Z = b * H; g_G = grid;
     cta_summary("attn_fwd", fcta, grid, fwd_blocks, st);
