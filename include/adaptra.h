@@ -290,7 +290,8 @@ int adaptra_prof_collect_ex(int32_t kind, int64_t* n_launches, double* sum_ms, d
  *        and freed at the end of B by the stage itself, in issue order
  *        ("B ... immediately free activation memory").
  *  work  (bytes = adaptra_stage_work_bytes): per-stage scratch (attention
- *        scores), reused by every op issued on the stage's stream.
+ *        work buffers, the deterministic column-sum partials and tickets of
+ *        W), reused by every op issued on the stage's stream.
  */
 #define ADAPTRA_BLOCK_MLP 0
 #define ADAPTRA_BLOCK_GPT 1

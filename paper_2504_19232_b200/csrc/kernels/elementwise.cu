@@ -310,6 +310,93 @@ __global__ void __launch_bounds__(256) colsum_vec_kernel(const T* __restrict__ y
   }
 }
 
+// Deterministic column sums (bias and LN parameter gradients of W), 16 B
+// loads: block = 256 threads over 64 columns x 256 rows (8 column groups of
+// 8 x 32 row lanes, the 8 rows of a thread loaded before any is summed); the
+// block's 64 sums go to part[by][c]; the last block of a column strip (ticket
+// on cnt[bx], reset by it) adds the strip's partials in row-block order to
+// out (out += ...; one writer per column), so the result is bit-reproducible
+// and independent of block scheduling.  LN: out_a += dh * xhat, out_b += dh.
+template <typename T, bool LN>
+__global__ void __launch_bounds__(256) colsum_det_kernel(const T* __restrict__ y, const T* __restrict__ x,
+                                                         const float* __restrict__ mean,
+                                                         const float* __restrict__ rstd, float* __restrict__ out_a,
+                                                         float* __restrict__ out_b, int R, int N,
+                                                         float* __restrict__ part, unsigned* __restrict__ cnt) {
+  __shared__ float sa[32][65], sb[32][65];
+  __shared__ bool last;
+  const int cg = threadIdx.x & 7, rl = threadIdx.x >> 3;
+  const int c0 = blockIdx.x * 64 + cg * 8;
+  const int r0 = blockIdx.y * 256;
+  float a[8] = {}, bsum[8] = {};
+  if (c0 < N) {
+    float v[8][8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int r = r0 + rl + 32 * k;
+      if (r < R) load8(y + (long)r * N + c0, v[k]);
+      else
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[k][j] = 0.f;
+    }
+    if (LN) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int r = r0 + rl + 32 * k;
+        if (r >= R) continue;
+        float xv[8];
+        load8(x + (long)r * N + c0, xv);
+        const float mu = mean[r], rs = rstd[r];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          a[j] += v[k][j] * (xv[j] - mu) * rs;
+          bsum[j] += v[k][j];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[j] += v[k][j];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    sa[rl][cg * 8 + j] = a[j];
+    if (LN) sb[rl][cg * 8 + j] = bsum[j];
+  }
+  __syncthreads();
+  const int c = blockIdx.x * 64 + threadIdx.x;
+  if (threadIdx.x < 64) {
+    float ta = 0.f, tb = 0.f;
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) {
+      ta += sa[k][threadIdx.x];
+      if (LN) tb += sb[k][threadIdx.x];
+    }
+    if (c < N) {
+      part[(size_t)blockIdx.y * N + c] = ta;
+      if (LN) part[(size_t)(gridDim.y + blockIdx.y) * N + c] = tb;
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&cnt[blockIdx.x], 1u) == gridDim.y - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < 64 && c < N) {
+    float ta = 0.f, tb = 0.f;
+    for (int k = 0; k < (int)gridDim.y; ++k) {
+      ta += __ldcg(part + (size_t)k * N + c);
+      if (LN) tb += __ldcg(part + (size_t)(gridDim.y + k) * N + c);
+    }
+    out_a[c] += ta;
+    if (LN) out_b[c] += tb;
+  }
+  if (threadIdx.x == 0) cnt[blockIdx.x] = 0u;
+}
+
 // ---------------------------------------------------------------- attention
 // Row i of batch z: P[i, j] = exp(S[i, j] - max) / sum over j <= i; zeros for
 // i < j < roundup(i + 1, 128) so that tile-granular consumers read zeros.
@@ -435,8 +522,11 @@ int ln_bwd(const T* dh, const T* x, const float* mean, const float* rstd, const 
 }
 template <typename T>
 int ln_param_grad(const T* dh, const T* x, const float* mean, const float* rstd, float* dg, float* db, int R, int d,
-                  cudaStream_t st) {
-  if (d % 8 == 0) {
+                  cudaStream_t st, float* part, unsigned* cnt) {
+  if (d % 8 == 0 && part) {
+    colsum_det_kernel<T, true>
+        <<<dim3((d + 63) / 64, (R + 255) / 256), 256, 0, st>>>(dh, x, mean, rstd, dg, db, R, d, part, cnt);
+  } else if (d % 8 == 0) {
     colsum_vec_kernel<T, true><<<dim3((d + 63) / 64, (R + 255) / 256), 256, 0, st>>>(dh, x, mean, rstd, dg, db, R, d);
   } else {
     int rpb = 256;
@@ -446,8 +536,11 @@ int ln_param_grad(const T* dh, const T* x, const float* mean, const float* rstd,
   return launch_check("ln_param_grad");
 }
 template <typename T>
-int col_sum(const T* y, float* out, int R, int N, cudaStream_t st) {
-  if (N % 8 == 0) {
+int col_sum(const T* y, float* out, int R, int N, cudaStream_t st, float* part, unsigned* cnt) {
+  if (N % 8 == 0 && part) {
+    colsum_det_kernel<T, false><<<dim3((N + 63) / 64, (R + 255) / 256), 256, 0, st>>>(
+        y, nullptr, nullptr, nullptr, out, nullptr, R, N, part, cnt);
+  } else if (N % 8 == 0) {
     colsum_vec_kernel<T, false>
         <<<dim3((N + 63) / 64, (R + 255) / 256), 256, 0, st>>>(y, nullptr, nullptr, nullptr, out, nullptr, R, N);
   } else {
@@ -572,8 +665,8 @@ int colsum_grouped(const ColsumJob* jobs, int n, int R, cudaStream_t st) {
   template int ln_bwd<T>(const T*, const T*, const float*, const float*, const float*, const T*, T*, int, int,    \
                          cudaStream_t);                                                                           \
   template int ln_param_grad<T>(const T*, const T*, const float*, const float*, float*, float*, int, int,        \
-                                cudaStream_t);                                                                    \
-  template int col_sum<T>(const T*, float*, int, int, cudaStream_t);                                              \
+                                cudaStream_t, float*, unsigned*);                                                 \
+  template int col_sum<T>(const T*, float*, int, int, cudaStream_t, float*, unsigned*);                           \
   template int softmax_causal<T>(const float*, T*, int, int, cudaStream_t);                                       \
   template int attn_rowdot<T>(const T*, const T*, float*, int, int, int, int, int, cudaStream_t);                 \
   template int colsum_grouped<T>(const ColsumJob*, int, int, cudaStream_t);                                       \

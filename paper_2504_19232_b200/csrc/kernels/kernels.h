@@ -22,10 +22,13 @@ template <typename T>
 int ln_bwd(const T* dh, const T* x, const float* mean, const float* rstd, const float* g, const T* dres, T* dx, int R,
            int d, cudaStream_t st);
 template <typename T>
+// part / cnt (optional): deterministic two-level reduction workspace, part
+// [2 * ceil(R / 256) * N] fp32, cnt [ceil(N / 64)] zeroed once (self-resetting);
+// without them one atomicAdd per column per block (order not reproducible)
 int ln_param_grad(const T* dh, const T* x, const float* mean, const float* rstd, float* dg, float* db, int R, int d,
-                  cudaStream_t st);
+                  cudaStream_t st, float* part = nullptr, unsigned* cnt = nullptr);
 template <typename T>
-int col_sum(const T* y, float* out, int R, int N, cudaStream_t st);
+int col_sum(const T* y, float* out, int R, int N, cudaStream_t st, float* part = nullptr, unsigned* cnt = nullptr);
 // One launch for many column sums (a W op's bias and LN parameter gradients):
 // ln = 0: out_a[c] += sum_r y[r,c];  ln = 1: out_a[c] += sum_r y (x - mean) rstd,
 // out_b[c] += sum_r y.  y, x row-major [R, N], N % 8 == 0.

@@ -71,7 +71,7 @@ struct SlotLayout {
   long yL, seed, lpart;  // stage-level (after the per-layer block); lpart: loss partials + ticket
   long slot_bytes;
   // work area
-  long w_S, w_dS, w_do, w_D, w_dq, work_bytes;
+  long w_S, w_dS, w_do, w_D, w_dq, w_cs, w_cnt, work_bytes;
   bool flash;  // fused tcgen05 attention (bf16, head dim 128)
 };
 
@@ -178,6 +178,12 @@ static int compute_layout(const adaptra_stage_desc_t& d, SlotLayout& L) {
     L.w_dq = align256(L.w_D + (long)d.b * d.n_heads * d.T * 4);
     w = L.flash ? align256(L.w_dq + R * D * 4) : L.w_dq;
   }
+  // deterministic column-sum workspace (bias / LN parameter gradients of W):
+  // partials [2][ceil(R/256)][max N] fp32 and one ticket per 64-column strip
+  const long maxN = std::max<long>(3 * D, F);
+  L.w_cs = align256(w);
+  L.w_cnt = align256(L.w_cs + 2 * ((R + 255) / 256) * maxN * 4);
+  w = align256(L.w_cnt + ((maxN + 63) / 64) * 4);
   L.work_bytes = w;
   return ADAPTRA_OK;
 }
@@ -434,10 +440,13 @@ struct StageOps {
       TRY(colsum_grouped<T>(cs.data(), (int)cs.size(), (int)R, st));
     } else {
       for (const auto& j : cs) {
+        float* part = (float*)((char*)s->d.work + s->L.w_cs);
+        unsigned* cnt = (unsigned*)((char*)s->d.work + s->L.w_cnt);
         if (j.ln)
-          TRY(ln_param_grad<T>((const T*)j.y, (const T*)j.x, j.mean, j.rstd, j.out_a, j.out_b, (int)R, j.N, st));
+          TRY(ln_param_grad<T>((const T*)j.y, (const T*)j.x, j.mean, j.rstd, j.out_a, j.out_b, (int)R, j.N, st, part,
+                               cnt));
         else
-          TRY(col_sum<T>((const T*)j.y, j.out_a, (int)R, j.N, st));
+          TRY(col_sum<T>((const T*)j.y, j.out_a, (int)R, j.N, st, part, cnt));
       }
     }
     return ADAPTRA_OK;
@@ -553,7 +562,7 @@ extern "C" int adaptra_stage_create(const adaptra_stage_desc_t* d, adaptra_stage
   }
   if (!d->wts || !d->vecs || !d->gwts || !d->gvecs || !d->stash || d->n_slots < 1 || !d->stash_fb ||
       d->n_slots_fb < 1 ||
-      (s->L.work_bytes > 0 && !d->work)) {
+      !d->work) {
     delete s;
     return set_error(ADAPTRA_EINVAL, "stage_create: missing buffers");
   }
@@ -567,8 +576,10 @@ extern "C" int adaptra_stage_create(const adaptra_stage_desc_t* d, adaptra_stage
     // the fused attention backward accumulates dQ with TMA reduce-add; the
     // finalize kernel re-zeroes it after every use
     cudaMemset((char*)d->work + s->L.w_dq, 0, (size_t)s->R * d->d * 4);
-    cudaDeviceSynchronize();
   }
+  // column-sum tickets start at 0 (the last block of a strip resets its own)
+  cudaMemset((char*)d->work + s->L.w_cnt, 0, (size_t)(s->L.work_bytes - s->L.w_cnt));
+  cudaDeviceSynchronize();
   s->fb_of.assign(d->n_slots, -1);
   for (int k = d->n_slots_fb - 1; k >= 0; --k) s->fb_free.push_back(k);
   *out = s;
