@@ -363,9 +363,11 @@ int adaptra_stage_zero_grads(adaptra_stage_t s, void* stream);
  *            slots into the mailbox (H2D, copy engine) and posts the device flag.
  * Outbox (sender side):
  *   dst(mb)  where the producing kernel writes: the peer mailbox slot itself
- *            (DIRECT: the last GEMM epilogue stores over NVLink, no extra copy)
- *            or a local staging slot (P2P: a copy kernel moves it afterwards;
- *            HOST: D2H into the host ring).
+ *            (DIRECT, mailbox on the same GPU: the last GEMM epilogue stores
+ *            into it, no copy) or a local staging slot (DIRECT to another GPU:
+ *            the copy engine moves it over NVLink on the outbox's stream --
+ *            epilogue stores straight into peer memory measured 1.75x slower;
+ *            P2P: a copy kernel moves it; HOST: D2H into the host ring).
  *   send     enqueues the transfer on the outbox's own stream after the
  *            producing op (never on the compute stream) and posts the flag.
  * Flags live in pinned, device-mapped host memory (POSIX shm, so they can be

@@ -275,7 +275,18 @@ struct adaptra_outbox {
   std::atomic<int64_t> n_msgs{0}, sum_delay{0}, max_delay{0};
   std::atomic<int64_t> inflight{0};  // gate items not yet released
   std::atomic<int> force_host{0};    // delegated path by policy (straggler), link still up
+  // DIRECT to a mailbox on another GPU: the producer's epilogue writes a local
+  // staging slot (TMA stores) and the copy engine moves it over NVLink.  An
+  // epilogue storing straight into peer memory ran the FC2 GEMM 1.75x slower
+  // and put 4.5x the payload on NVLink (32 B granules;
+  // profiles/r02_direct_nvlink.txt).  $ADAPTRA_DIRECT_REMOTE_STORES=1 restores it.
+  bool remote_ce = false;
 };
+
+static bool remote_stores_forced() {
+  static const bool v = getenv("ADAPTRA_DIRECT_REMOTE_STORES") && atoi(getenv("ADAPTRA_DIRECT_REMOTE_STORES")) == 1;
+  return v;
+}
 
 // ------------------------------------------------------------ delegate thread
 namespace adaptra {
@@ -483,7 +494,13 @@ static int ensure_staging(adaptra_outbox* ob) {
 static int outbox_common(adaptra_outbox* ob) {
   cudaSetDevice(ob->dev);
   ADAPTRA_CUDA_TRY(cudaStreamCreateWithFlags(&ob->lstream, cudaStreamNonBlocking));
-  if (ob->mode != ADAPTRA_LINK_DIRECT) {
+  if (ob->mode == ADAPTRA_LINK_DIRECT && !remote_stores_forced()) {
+    cudaPointerAttributes pa;
+    if (cudaPointerGetAttributes(&pa, ob->peer_mbox) == cudaSuccess && pa.type == cudaMemoryTypeDevice)
+      ob->remote_ce = pa.device != ob->dev;
+    cudaGetLastError();
+  }
+  if (ob->mode != ADAPTRA_LINK_DIRECT || ob->remote_ce) {
     int rc = ensure_staging(ob);
     if (rc) return rc;
   }
@@ -602,7 +619,7 @@ static bool ob_down(adaptra_outbox_t ob) {
 
 extern "C" void* adaptra_outbox_dst(adaptra_outbox_t ob, int32_t mb) {
   if (!ob || mb < 0 || mb >= ob->n_mb) return nullptr;
-  if (ob->mode == ADAPTRA_LINK_DIRECT && !ob_down(ob)) return ob->peer_mbox + (size_t)mb * ob->bytes;
+  if (ob->mode == ADAPTRA_LINK_DIRECT && !ob->remote_ce && !ob_down(ob)) return ob->peer_mbox + (size_t)mb * ob->bytes;
   return (char*)ob->staging + (size_t)mb * ob->bytes;
 }
 
@@ -637,19 +654,25 @@ extern "C" int adaptra_send(adaptra_outbox_t ob, int32_t mb, void* producer, uin
   volatile uint32_t* hflag_peer = ob->peer_hflags + mb;
   if (mode == ADAPTRA_LINK_DIRECT || mode == ADAPTRA_LINK_P2P) {
     cudaEvent_t ready = ob->ev_prod[mb];
-    if (mode == ADAPTRA_LINK_P2P) {
+    const bool moved = mode == ADAPTRA_LINK_P2P || ob->remote_ce;
+    if (moved) {
       ADAPTRA_CUDA_TRY(cudaStreamWaitEvent(ob->lstream, ob->ev_prod[mb], 0));
-      int rc = copy_async(ob->peer_mbox + (size_t)mb * ob->bytes, (char*)ob->staging + (size_t)mb * ob->bytes,
-                          ob->bytes, ob->lstream);
-      if (rc) return rc;
+      char* dst = ob->peer_mbox + (size_t)mb * ob->bytes;
+      const char* src = (char*)ob->staging + (size_t)mb * ob->bytes;
+      if (mode == ADAPTRA_LINK_P2P) {
+        int rc = copy_async(dst, src, ob->bytes, ob->lstream);  // copy kernel (SM stores)
+        if (rc) return rc;
+      } else {
+        ADAPTRA_CUDA_TRY(cudaMemcpyAsync(dst, src, ob->bytes, cudaMemcpyDeviceToDevice, ob->lstream));  // copy engine
+      }
       ADAPTRA_CUDA_TRY(cudaEventRecord(ob->ev_moved[mb], ob->lstream));
       ready = ob->ev_moved[mb];
     }
     if (lat == 0) {
-      // no injected latency: post the flag right behind the producer (DIRECT)
-      // or behind the copy (P2P), on the same stream (stream order puts it
-      // after the data stores)
-      return stream_write(mode == ADAPTRA_LINK_P2P ? ob->lstream : (cudaStream_t)producer, flag, epoch);
+      // no injected latency: post the flag right behind the producer (DIRECT
+      // within a GPU) or behind the copy, on the same stream (stream order
+      // puts it after the data stores)
+      return stream_write(moved ? ob->lstream : (cudaStream_t)producer, flag, epoch);
     }
     // injected latency: the gate thread posts the flag from the host c ns
     // after the data is in place
