@@ -6,9 +6,11 @@ iteration by iteration on 8 stages, compressed `--compress`x in time (1200 ->
   online    planner fed the transport's measured latencies (lag 1)
   zb        fixed ZB order (Alg. 2 plan at c = 0)
   1f1b      fixed 1F1B order
-  zb-inorder / 1f1b-inorder  the same orders with blocking sends / receives
-            in the compute sequence (the paper's NCCL-in-order
-            baselines, head-of-line blocking)
+  zb-inorder / 1f1b-inorder  the same orders with blocking receives and a
+            bounded send queue in the compute sequence
+  zb-nccl / 1f1b-nccl  the same orders with real NCCL send/recv in the
+            compute sequence (one stage per GPU; N1)
+  adaptive-deleg  adaptive, straggling links moved to the delegated host path
 on the same kernels and transport.  Latencies are scaled per R22 (latency_ms
 in units of the paper's t = 10 ms, times the measured stage t_F); the failed
 link carries its traffic on the delegated host path in every arm (the fixed
@@ -37,6 +39,7 @@ def main():
     ap.add_argument("--width", type=int, default=2048)
     ap.add_argument("--compress", type=int, default=10)
     ap.add_argument("--arms", default="adaptive,online,zb,1f1b")
+    ap.add_argument("--replan-log", default="", help="JSONL of the first adaptive arm's per-iteration plans")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -44,7 +47,6 @@ def main():
     import bench
     import synthetic as sy
     from paper_2504_19232_b200 import _lib as L
-    from paper_2504_19232_b200 import sched as cs
     from paper_2504_19232_b200.online import LinkMonitor, OnlinePlanner
     from paper_2504_19232_b200.pipeline import Arm, ModelCfg, Pipeline
 
@@ -69,24 +71,18 @@ def main():
                  b=1, T=2048, dtype=L.BF16)
     pipe = Pipeline(m, S, N, rank=rank, world=world, device=local, group=group, host_links=True)
     prof = Arm("zb", S, N, [1000] * S, [1000] * S, [1000] * S)
-    for _ in range(2):
-        r = pipe.run(prof.orders)
-    allp = {}
-    for dd in gather({i: [st["op_ns"][k] // max(1, st["op_cnt"][k]) for k in range(3)] for i, st in r.stats.items()}):
-        allp.update(dd)
-    tF = [max(1, allp[i][0] // 1000) * 1000 for i in range(S)]
-    tB = [max(1, allp[i][1] // 1000) * 1000 for i in range(S)]
-    tW = [max(1, allp[i][2] // 1000) * 1000 for i in range(S)]
+    for _ in range(3):
+        pipe.run(prof.orders)
+    tF, tB, tW = pipe.profile(k=2)          # a1: the library's profiler (median, 1 us ticks)
     t_ref = sum(tF) // S
     host_c = max(gather(bench.measure_host_path(pipe, torch) if rank == 0 else 0))
     caps = {}
     for dd in gather({i: st.n_slots_fb for i, st in pipe.stages.items()}):
         caps.update(dd)
     x_cap = [caps[i] for i in range(S)]
-    x_init = cs.plan_init(S, N, x_cap[0], 1)
-    x_init = [min(v, c) for v, c in zip(x_init, x_cap)]
-    for i in range(S - 2, -1, -1):
-        x_init[i] = max(x_init[i], x_init[i + 1])
+    if any(a.endswith("-nccl") for a in args.arms.split(",")):
+        pipe.enable_nccl(host_c)
+    log = []
 
     n_iter = sy.PAPER_TRACE_ITERS // args.compress
     seq = []  # per iteration: (event id or -1, c, down)
@@ -100,13 +96,15 @@ def main():
             seq.append((ev["id"], c, down))
 
     def run(name):
-        base = Arm("adaptive" if name in ("adaptive", "online") else name, S, N, tF, tB, tW,
-                   x_init=x_init if name in ("adaptive", "online") else None, x_cap=x_cap)
+        base = Arm("adaptive" if name == "online" else name, S, N, tF, tB, tW, x_cap=x_cap, mem=(x_cap[0], 1))
+        if base.name == "adaptive" and not base.deleg and rank == 0:
+            log.append({"arm": name, "S": S, "N": N, "tF": tF, "tB": tB, "tW": tW, "x_cap": x_cap,
+                        "mem": [x_cap[0], 1], "ratio": 30, "x_init": base.x_init})
         online = OnlinePlanner(base, t_ref) if name == "online" else None
         mon = LinkMonitor(pipe, gather)
         for l in range(S - 1):
             pipe.set_latency(l, 0)
-        pipe.run(base.plan([0] * (S - 1)), merge_w=base.merge_w, inorder=base.inorder)  # warm-up at nominal
+        pipe.run(base.plan([0] * (S - 1)), merge_w=base.merge_w, inorder=base.inorder, nccl=base.nccl)  # warm-up
         mon.sample()
         if world > 1:
             dist.barrier(group=group)
@@ -117,10 +115,18 @@ def main():
                 want = L.LINK_DOWN if l in down else c[l]
                 if pipe.latency[l] != want:
                     pipe.set_latency(l, want)
+                pipe.set_path(l, base.deleg and c[l] > 0 and l not in down)
             orders = online.orders() if online else base.plan(c)
+            if log and log[0]["arm"] == name and rank == 0:
+                ent = dict(base.last)
+                ent["step"] = len(per_iter)
+                ent["orders"] = [" ".join(f"{kd}{mb}" for kd, mb in o) for o in orders]
+                log.append(ent)
             ev0, ev1 = torch.cuda.Event(True), torch.cuda.Event(True)
             ev0.record()
-            res = pipe.run(orders, merge_w=base.merge_w, inorder=base.inorder)
+            res = pipe.run(orders, merge_w=base.merge_w, inorder=base.inorder, nccl=base.nccl)
+            if base.name == "adaptive":
+                base.set_profile(*pipe.profile(k=5))
             ev1.record()
             torch.cuda.synchronize()
             g = gather((ev0.elapsed_time(ev1), sum(st["busy_ns"] for st in res.stats.values())))
@@ -140,6 +146,10 @@ def main():
     out = {}
     for name in args.arms.split(","):
         out[name] = run(name)
+    if args.replan_log and rank == 0:
+        with open(args.replan_log, "w") as f:
+            for e in log:
+                f.write(json.dumps(e) + "\n")
     if rank == 0:
         meta = {"S": S, "N": N, "gpus": world, "layers": args.layers, "d": args.width,
                 "compress": args.compress, "t_ref_us": t_ref / 1e3, "host_c_us": host_c / 1e3,
