@@ -97,7 +97,7 @@ def main():
 
     def run(name):
         base = Arm("adaptive" if name == "online" else name, S, N, tF, tB, tW, x_cap=x_cap, mem=(x_cap[0], 1))
-        if base.name == "adaptive" and not base.deleg and rank == 0:
+        if name == "adaptive" and not log and rank == 0:
             log.append({"arm": name, "S": S, "N": N, "tF": tF, "tB": tB, "tW": tW, "x_cap": x_cap,
                         "mem": [x_cap[0], 1], "ratio": 30, "x_init": base.x_init})
         online = OnlinePlanner(base, t_ref) if name == "online" else None
