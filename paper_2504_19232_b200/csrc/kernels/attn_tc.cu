@@ -427,6 +427,299 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads, 1)
   }
 }
 
+// ============================================================== forward, ping-pong
+// Two query tiles per work item -- blocks 2p (A) and 2p+1 (B) of one
+// (sequence, head) -- share every K_j / V_j tile, and the tensor pipe
+// alternates between them: S_A(j) = Q_A K_j^T, S_B(j), then O_A += P_A(j) V_j
+// as soon as A's softmax warps have written P_A(j), S_A(j+1), O_B += P_B(j)
+// V_j, S_B(j+1), ...  While one tile's softmax runs, the pipe works on the
+// other's products, so softmax and MMA overlap instead of alternating.
+// P is written back into the S columns of TMEM as bf16 pairs (16 keys per
+// 8 columns) and consumed from there as the A operand of P V (the ts form),
+// so it never touches shared memory.  TMEM: S_A [0,128), S_B [128,256),
+// O_A [256,384), O_B [384,512).  Warps: 0 TMA, 1 MMA, 2..9 softmax of A,
+// 10..17 softmax of B (lane quadrant x column half, as attn_fwd_kernel<2>).
+// The same online softmax (lazy reference max, P <= 2^8), masking and
+// epilogue as attn_fwd_kernel; one S buffer per tile: S_t(j+1) is issued only
+// after P_t(j) V_j, which it overwrites, in the in-order tensor pipe.
+constexpr int kPPThreads = 64 + 32 * 16;
+constexpr int kPPRing = 4;
+constexpr int kPPSmem = (2 + kPPRing) * TILE + 2 * 2 * 2 * AT * 4 + 256;
+static_assert(kPPSmem <= 232448, "attn fwd ping-pong shared memory");
+
+__device__ __forceinline__ int pp_item(int r, int c, int G) { return (r & 1) ? (r + 1) * G - 1 - c : r * G + c; }
+
+__global__ void __launch_bounds__(kPPThreads, 1)
+    attn_fwd_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv, const AttnArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if (threadIdx.x == 0 && (smem_u32(smem) & 1023)) __trap();
+  uint8_t* sQ = smem;                        // [2 tiles] x 32 KB
+  uint8_t* sRing = sQ + 2 * TILE;            // kPPRing x 32 KB: K V K V ...
+  float* sMax = (float*)(sRing + kPPRing * TILE);  // [2 tiles][2 parity][2 halves][128]
+  uint64_t* bar = (uint64_t*)(sMax + 8 * AT);
+  uint64_t* q_full = bar + 0;                // [2]
+  uint64_t* q_empty = q_full + 2;            // [2] the tile's last S MMA of the item read Q
+  uint64_t* t_full = q_empty + 2;            // [kPPRing]
+  uint64_t* t_empty = t_full + kPPRing;      // [kPPRing]
+  uint64_t* s_full = t_empty + kPPRing;      // [2] S_t(j) in TMEM
+  uint64_t* p_full = s_full + 2;             // [2] P_t(j) written (8 warps)
+  uint64_t* o_full = p_full + 2;             // [2] the tile's last P V of the item done
+  uint32_t* tmem_slot = (uint32_t*)(o_full + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int nqb = a.T / AT, npair = nqb / 2, Z = a.b * a.H, n_items = npair * Z;
+  const int G = (int)gridDim.x, cta = (int)blockIdx.x;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_qkv);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&q_full[t], 1);
+      mbar_init(&q_empty[t], 1);
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_full[t], 8);
+      mbar_init(&o_full[t], 1);
+    }
+    for (int i = 0; i < kPPRing; ++i) {
+      mbar_init(&t_full[i], 1);
+      mbar_init(&t_empty[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int slot = 0, ph = 0;
+      for (int r = 0, it = 0;; ++r, ++it) {
+        const int item = pp_item(r, cta, G);
+        if (item >= n_items) break;
+        const int p = npair - 1 - item / Z, z = item % Z;
+        const int s = z / a.H, h = z % a.H, row0 = s * a.T;
+        const int kcol = a.d + h * AT, vcol = 2 * a.d + h * AT;
+        for (int t = 0; t < 2; ++t) {
+          mbar_wait(&q_empty[t], (it & 1) ^ 1);
+          mbar_arrive_expect_tx(&q_full[t], TILE);
+          for (int c = 0; c < 2; ++c)
+            tma_load_2d(sQ + t * TILE + c * CHUNK, &tm_qkv, &q_full[t], h * AT + 64 * c, row0 + (2 * p + t) * AT);
+        }
+        for (int n = 0; n < 2 * (2 * p + 2); ++n) {  // K_j (n = 2j), V_j (n = 2j+1), j = 0 .. 2p+1
+          mbar_wait(&t_empty[slot], ph ^ 1);
+          mbar_arrive_expect_tx(&t_full[slot], TILE);
+          const int col = (n & 1) ? vcol : kcol;
+          for (int c = 0; c < 2; ++c)
+            tma_load_2d(sRing + slot * TILE + c * CHUNK, &tm_qkv, &t_full[slot], col + 64 * c, row0 + (n >> 1) * AT);
+          if (++slot == kPPRing) {
+            slot = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ring tile n (global, counted over items) sits in slot n % kPPRing with
+    // phase (n / kPPRing) & 1; item tile counter n0 advances by 2 (2p + 2)
+    int n0 = 0, gA = 0, gB = 0;  // ring tiles and per-tile blocks of the items before this one
+    for (int r = 0, it = 0;; ++r, ++it) {
+      const int item = pp_item(r, cta, G);
+      if (item >= n_items) break;
+      const int p = npair - 1 - item / Z;
+      const int nb = 2 * p + 2;  // key blocks of tile B (tile A: nb - 1)
+      auto kslot = [&](int j) { return (n0 + 2 * j) % kPPRing; };
+      auto vslot = [&](int j) { return (n0 + 2 * j + 1) % kPPRing; };
+      auto kph = [&](int j) { return (uint32_t)(((n0 + 2 * j) / kPPRing) & 1); };
+      auto vph = [&](int j) { return (uint32_t)(((n0 + 2 * j + 1) / kPPRing) & 1); };
+      auto issue_s = [&](int t, int j, bool release_k) {
+        if (lane == 0) {
+          const uint32_t aQ = smem_u32(sQ + t * TILE), aK = smem_u32(sRing + kslot(j) * TILE);
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks)
+            tc_mma_f16(tmem + t * 128, desc_kmajor(aQ, ks), desc_kmajor(aK, ks), idesc(0, 0), ks > 0 ? 1u : 0u);
+          tc_commit(&s_full[t]);
+          if (release_k) tc_commit(&t_empty[kslot(j)]);
+        }
+        __syncwarp();
+      };
+      auto issue_pv = [&](int t, int j, bool release_v) {
+        if (lane == 0) {
+          const uint32_t aV = smem_u32(sRing + vslot(j) * TILE);
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks)
+            tc_mma_f16_ts(tmem + 256 + t * 128, tmem + t * 128 + 16 * ks, desc_mnmajor(aV, ks), idesc(0, 1),
+                          (j > 0 || ks > 0) ? 1u : 0u);
+          if (release_v) tc_commit(&t_empty[vslot(j)]);
+        }
+        __syncwarp();
+      };
+      mbar_wait(&q_full[0], it & 1);
+      mbar_wait(&q_full[1], it & 1);
+      mbar_wait(&t_full[kslot(0)], kph(0));
+      tc_fence_after();
+      issue_s(0, 0, false);
+      issue_s(1, 0, true);
+      for (int j = 0; j < nb; ++j) {
+        const bool has_a = j < nb - 1;
+        const bool last_a = j == nb - 2, last_b = j == nb - 1;
+        mbar_wait(&t_full[vslot(j)], vph(j));
+        if (has_a) {
+          mbar_wait(&p_full[0], (gA + j) & 1);
+          tc_fence_after();
+          issue_pv(0, j, false);
+          if (last_a) {
+            if (lane == 0) {
+              tc_commit(&o_full[0]);
+              tc_commit(&q_empty[0]);
+            }
+            __syncwarp();
+          } else {
+            mbar_wait(&t_full[kslot(j + 1)], kph(j + 1));
+            tc_fence_after();
+            issue_s(0, j + 1, false);
+          }
+        }
+        mbar_wait(&p_full[1], (gB + j) & 1);
+        tc_fence_after();
+        issue_pv(1, j, true);
+        if (last_b) {
+          if (lane == 0) {
+            tc_commit(&o_full[1]);
+            tc_commit(&q_empty[1]);
+          }
+          __syncwarp();
+        } else {
+          if (!has_a || last_a) {  // tile A done: K_{j+1} is B's alone
+            mbar_wait(&t_full[kslot(j + 1)], kph(j + 1));
+            tc_fence_after();
+          }
+          issue_s(1, j + 1, true);
+        }
+      }
+      n0 += 2 * nb;
+      gA += nb - 1;
+      gB += nb;
+    }
+  } else {
+    const int sw = warp - 2;                  // 0..15
+    const int t = sw >> 3;                    // tile
+    const int quad = warp & 3, half = (sw >> 2) & 1;
+    const int r = quad * 32 + lane;
+    const uint32_t lanes = (uint32_t)(quad * 32) << 16;
+    const uint32_t tS = tmem + t * 128 + lanes, tO = tmem + 256 + t * 128 + lanes;
+    const float c2 = a.scale * kLog2e;
+    const int row_bar = 1 + t * 4 + quad;
+    float* mxb = sMax + t * 4 * AT;           // this tile's [2 parity][2 halves][128]
+    int g = 0;                                // this tile's blocks so far (barrier phases, sMax parity)
+    for (int rr = 0, it = 0;; ++rr, ++it) {
+      const int item = pp_item(rr, cta, G);
+      if (item >= n_items) break;
+      const int p = npair - 1 - item / Z, z = item % Z;
+      const int s = z / a.H, h = z % a.H, row0 = s * a.T;
+      const int qb = 2 * p + t;               // this tile's query block
+      const int qi = qb * AT + r;
+      float mref = -INFINITY, l = 0.f;
+      for (int j = 0; j <= qb; ++j, ++g) {
+        mbar_wait(&s_full[t], g & 1);
+        tc_fence_after();
+        // pass 1: the row max of this half (32 columns at a time, registers
+        // reused; TMEM is read again in pass 2 instead of holding 64 values)
+        const int lim = (j == qb) ? qi - (j * AT + half * 64) : 1 << 20;  // last visible column
+        float cm = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t rv[32];
+          tmem_ld32(tS + half * 64 + 32 * c, rv);
+          tmem_ld_wait_regs(rv);
+#pragma unroll
+          for (int u = 0; u < 32; ++u)
+            if (32 * c + u <= lim) cm = fmaxf(cm, __uint_as_float(rv[u]));
+        }
+        float* mx = mxb + (g & 1) * 2 * AT;
+        mx[half * AT + r] = cm;
+        named_sync(row_bar, 64);
+        const float mb = fmaxf(mx[r], mx[AT + r]) * c2;
+        const bool resc = mb > mref + 8.f;
+        float alpha = 1.f;
+        if (resc) {
+          alpha = ex2(mref - mb);
+          mref = mb;
+        }
+        // O_t is stable here: S_t(j) was issued after P_t(j-1) V_{j-1}
+        if (j > 0 && __any_sync(0xffffffffu, resc)) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            uint32_t o[32];
+            tmem_ld32(tO + half * 64 + 32 * c, o);
+            tmem_ld_wait_regs(o);
+#pragma unroll
+            for (int u = 0; u < 32; ++u) o[u] = __float_as_uint(__uint_as_float(o[u]) * alpha);
+            tmem_st32(tO + half * 64 + 32 * c, o);
+          }
+        }
+        // pass 2: P = 2^(S c2 - mref) -> bf16 pairs over the S columns just read
+        float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t rv[32];
+          tmem_ld32(tS + half * 64 + 32 * c, rv);
+          tmem_ld_wait_regs(rv);
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) {      // 16 keys = one k-step of P V
+            uint32_t pk[8];
+#pragma unroll
+            for (int u = 0; u < 16; u += 2) {
+              const int col = 32 * c + 16 * kk + u;
+              const float e0 = col <= lim ? ex2(fmaf(__uint_as_float(rv[16 * kk + u]), c2, -mref)) : 0.f;
+              const float e1 = col + 1 <= lim ? ex2(fmaf(__uint_as_float(rv[16 * kk + u + 1]), c2, -mref)) : 0.f;
+              if (u & 2) acc1 += e0 + e1; else acc0 += e0 + e1;
+              pk[u >> 1] = pack_bf16x2(e0, e1);
+            }
+            tmem_st8(tS + 16 * (4 * half + 2 * c + kk), pk);
+          }
+        }
+        l = l * alpha + (acc0 + acc1);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[t]);
+      }
+      // epilogue: O / l -> bf16 (this half of the head dims), LSE (log2 units);
+      // row sums through the parity buffer the last block did not use
+      float* sL = mxb + (g & 1) * 2 * AT;
+      sL[half * AT + r] = l;
+      named_sync(row_bar, 64);
+      const float ltot = sL[r] + sL[AT + r];
+      named_sync(row_bar, 64);
+      const float inv = 1.f / ltot;
+      mbar_wait(&o_full[t], it & 1);
+      tc_fence_after();
+      bf16* orow = a.o + (size_t)(row0 + qi) * a.d + h * AT + half * 64;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t rv[32];
+        tmem_ld32(tO + half * 64 + 32 * c, rv);
+        tmem_ld_wait_regs(rv);
+#pragma unroll
+        for (int u = 0; u < 32; u += 8) {
+          float v[8];
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) v[kk] = __uint_as_float(rv[u + kk]) * inv;
+          st_bf16x8(orow + 32 * c + u, v);
+        }
+      }
+      tc_fence_before();
+      if (half == 0) a.lse[(size_t)z * a.T + qi] = mref + __log2f(ltot);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
 // ============================================================== backward
 // One CTA per (z, 128-key block kb), over 64-query blocks i >= 2 kb.
 // TMEM columns: dK [0,128), dV [128,256), SP[2] [256,384) (S^T of block i,
@@ -932,6 +1225,7 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
   if (!(attr.load(std::memory_order_acquire) & (1u << dev))) {
     cudaFuncSetAttribute(attn_fwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
     cudaFuncSetAttribute(attn_fwd_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<4>::kSmem);
+    cudaFuncSetAttribute(attn_fwd_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPPSmem);
     attr.fetch_or(1u << dev, std::memory_order_release);
   }
   AttnArgs a{};
@@ -950,10 +1244,17 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
   // ADAPTRA_ATTN_FWD_GRID=items: one CTA per item (the non-persistent launch, for comparison)
   static const bool per_item = getenv("ADAPTRA_ATTN_FWD_GRID") && !strcmp(getenv("ADAPTRA_ATTN_FWD_GRID"), "items");
   const int items = b * H * (T / AT), grid = per_item ? items : std::min(items, n_sm[dev & 31]);
-  if (nq == 4)
+  // ping-pong over query-block pairs (default; $ADAPTRA_ATTN_FWD=single for
+  // one query tile per item), which needs an even number of query blocks
+  static const bool pp_off = getenv("ADAPTRA_ATTN_FWD") && !strcmp(getenv("ADAPTRA_ATTN_FWD"), "single");
+  if (!pp_off && (T / AT) % 2 == 0 && !per_item) {
+    const int pitems = b * H * (T / AT) / 2;
+    attn_fwd_pp_kernel<<<std::min(pitems, n_sm[dev & 31]), kPPThreads, kPPSmem, st>>>(m, a);
+  } else if (nq == 4) {
     attn_fwd_kernel<4><<<grid, FwdCfg<4>::kThreads, FwdCfg<4>::kSmem, st>>>(m, a);
-  else
+  } else {
     attn_fwd_kernel<2><<<grid, FwdCfg<2>::kThreads, FwdCfg<2>::kSmem, st>>>(m, a);
+  }
   if (fdiag & 0x400) {
     g_nqb = T / AT; g_Z = b * H; g_G = grid;
     cta_summary("attn_fwd", fcta, grid, fwd_blocks, st);
