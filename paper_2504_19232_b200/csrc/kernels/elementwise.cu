@@ -318,26 +318,26 @@ __global__ void __launch_bounds__(256) colsum_vec_kernel(const T* __restrict__ y
 // out (out += ...; one writer per column), so the result is bit-reproducible
 // and independent of block scheduling.  LN: out_a += dh * xhat, out_b += dh.
 template <typename T, bool LN>
-__global__ void __launch_bounds__(256) colsum_det_kernel(const T* __restrict__ y, const T* __restrict__ x,
-                                                         const float* __restrict__ mean,
-                                                         const float* __restrict__ rstd, float* __restrict__ out_a,
-                                                         float* __restrict__ out_b, int R, int N,
-                                                         float* __restrict__ part, unsigned* __restrict__ cnt) {
-  __shared__ float sa[32][65], sb[32][65];
-  __shared__ bool last;
+__device__ __forceinline__ void colsum_block(const T* __restrict__ y, const T* __restrict__ x,
+                                             const float* __restrict__ mean, const float* __restrict__ rstd,
+                                             float* __restrict__ out_a, float* __restrict__ out_b, int R, int N, int bx,
+                                             int by, int nby, float* __restrict__ part, unsigned* __restrict__ cnt,
+                                             float (*sa)[65], float (*sb)[65], bool* last) {
   const int cg = threadIdx.x & 7, rl = threadIdx.x >> 3;
-  const int c0 = blockIdx.x * 64 + cg * 8;
-  const int r0 = blockIdx.y * 256;
+  const int c0 = bx * 64 + cg * 8;
+  const int r0 = by * 256;
   float a[8] = {}, bsum[8] = {};
   if (c0 < N) {
     float v[8][8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int r = r0 + rl + 32 * k;
-      if (r < R) load8(y + (long)r * N + c0, v[k]);
-      else
+      if (r < R) {
+        load8(y + (long)r * N + c0, v[k]);
+      } else {
 #pragma unroll
         for (int j = 0; j < 8; ++j) v[k][j] = 0.f;
+      }
     }
     if (LN) {
 #pragma unroll
@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(256) colsum_det_kernel(const T* __restrict__ y
     if (LN) sb[rl][cg * 8 + j] = bsum[j];
   }
   __syncthreads();
-  const int c = blockIdx.x * 64 + threadIdx.x;
+  const int c = bx * 64 + threadIdx.x;
   if (threadIdx.x < 64) {
     float ta = 0.f, tb = 0.f;
 #pragma unroll 8
@@ -375,26 +375,38 @@ __global__ void __launch_bounds__(256) colsum_det_kernel(const T* __restrict__ y
       if (LN) tb += sb[k][threadIdx.x];
     }
     if (c < N) {
-      part[(size_t)blockIdx.y * N + c] = ta;
-      if (LN) part[(size_t)(gridDim.y + blockIdx.y) * N + c] = tb;
+      part[(size_t)by * N + c] = ta;
+      if (LN) part[(size_t)(nby + by) * N + c] = tb;
     }
     __threadfence();
   }
   __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(&cnt[blockIdx.x], 1u) == gridDim.y - 1;
+  if (threadIdx.x == 0) *last = atomicAdd(&cnt[bx], 1u) == (unsigned)nby - 1;
   __syncthreads();
-  if (!last) return;
+  if (!*last) return;
   __threadfence();
   if (threadIdx.x < 64 && c < N) {
     float ta = 0.f, tb = 0.f;
-    for (int k = 0; k < (int)gridDim.y; ++k) {
+    for (int k = 0; k < nby; ++k) {
       ta += __ldcg(part + (size_t)k * N + c);
-      if (LN) tb += __ldcg(part + (size_t)(gridDim.y + k) * N + c);
+      if (LN) tb += __ldcg(part + (size_t)(nby + k) * N + c);
     }
     out_a[c] += ta;
     if (LN) out_b[c] += tb;
   }
-  if (threadIdx.x == 0) cnt[blockIdx.x] = 0u;
+  if (threadIdx.x == 0) cnt[bx] = 0u;
+}
+
+template <typename T, bool LN>
+__global__ void __launch_bounds__(256) colsum_det_kernel(const T* __restrict__ y, const T* __restrict__ x,
+                                                         const float* __restrict__ mean,
+                                                         const float* __restrict__ rstd, float* __restrict__ out_a,
+                                                         float* __restrict__ out_b, int R, int N,
+                                                         float* __restrict__ part, unsigned* __restrict__ cnt) {
+  __shared__ float sa[32][65], sb[32][65];
+  __shared__ bool last;
+  colsum_block<T, LN>(y, x, mean, rstd, out_a, out_b, R, N, blockIdx.x, blockIdx.y, gridDim.y, part, cnt, sa, sb,
+                      &last);
 }
 
 // ---------------------------------------------------------------- attention
@@ -590,11 +602,23 @@ __global__ void __launch_bounds__(256) colsum_grouped_kernel(const ColsumGroup g
   int j = 0;
   while (j + 1 < g.n && (int)blockIdx.x >= g.job[j + 1].start) ++j;
   const ColsumJob& J = g.job[j];
+  const int nby = (g.R + 255) / 256;
   const int b = blockIdx.x - J.start, bx = b % J.nbx, by = b / J.nbx;
+  __shared__ float sa[32][65], sb[32][65];
+  __shared__ bool last;
+  if (J.part) {
+    if (J.ln)
+      colsum_block<T, true>((const T*)J.y, (const T*)J.x, J.mean, J.rstd, J.out_a, J.out_b, g.R, J.N, bx, by, nby,
+                            J.part, J.cnt, sa, sb, &last);
+    else
+      colsum_block<T, false>((const T*)J.y, nullptr, nullptr, nullptr, J.out_a, nullptr, g.R, J.N, bx, by, nby,
+                             J.part, J.cnt, sa, sb, &last);
+    return;
+  }
+  // atomic fallback (no workspace): one atomicAdd per column per block
   const T* __restrict__ y = (const T*)J.y;
   const T* __restrict__ x = (const T*)J.x;
   const int N = J.N, R = g.R;
-  __shared__ float sa[32][65], sb[32][65];
   const int cg = threadIdx.x & 7, rl = threadIdx.x >> 3;
   const int c0 = bx * 64 + cg * 8;
   const int r0 = by * 256;
@@ -639,18 +663,32 @@ __global__ void __launch_bounds__(256) colsum_grouped_kernel(const ColsumGroup g
   }
 }
 template <typename T>
-int colsum_grouped(const ColsumJob* jobs, int n, int R, cudaStream_t st) {
+int colsum_grouped(const ColsumJob* jobs, int n, int R, cudaStream_t st, float* part, unsigned* cnt, long part_cap,
+                   long cnt_cap) {
+  const int nby = (R + 255) / 256;
   for (int i0 = 0; i0 < n; i0 += kMaxColsum) {
     ColsumGroup g{};
     g.n = std::min(kMaxColsum, n - i0);
     g.R = R;
     int blocks = 0;
+    long poff = 0, coff = 0;  // each job its own partials and tickets (the group's jobs run concurrently)
     for (int k = 0; k < g.n; ++k) {
       g.job[k] = jobs[i0 + k];
       if (g.job[k].N % 8) return set_error(ADAPTRA_EINVAL, "colsum_grouped: N % 8 != 0");
       g.job[k].nbx = (g.job[k].N + 63) / 64;
       g.job[k].start = blocks;
-      blocks += g.job[k].nbx * ((R + 255) / 256);
+      blocks += g.job[k].nbx * nby;
+      g.job[k].part = nullptr;
+      g.job[k].cnt = nullptr;
+      if (part) {
+        const long need = 2L * nby * g.job[k].N;
+        if (poff + need > part_cap || coff + g.job[k].nbx > cnt_cap)
+          return set_error(ADAPTRA_ENOMEM, "colsum_grouped: workspace too small");
+        g.job[k].part = part + poff;
+        g.job[k].cnt = cnt + coff;
+        poff += need;
+        coff += g.job[k].nbx;
+      }
     }
     if (blocks == 0) continue;
     colsum_grouped_kernel<T><<<blocks, 256, 0, st>>>(g);
@@ -669,7 +707,7 @@ int colsum_grouped(const ColsumJob* jobs, int n, int R, cudaStream_t st) {
   template int col_sum<T>(const T*, float*, int, int, cudaStream_t, float*, unsigned*);                           \
   template int softmax_causal<T>(const float*, T*, int, int, cudaStream_t);                                       \
   template int attn_rowdot<T>(const T*, const T*, float*, int, int, int, int, int, cudaStream_t);                 \
-  template int colsum_grouped<T>(const ColsumJob*, int, int, cudaStream_t);                                       \
+  template int colsum_grouped<T>(const ColsumJob*, int, int, cudaStream_t, float*, unsigned*, long, long);        \
   template int mse_loss<T>(const T*, const float*, T*, float*, float*, long, int, cudaStream_t);
 INST(float)
 INST(bf16)

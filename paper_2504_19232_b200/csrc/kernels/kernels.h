@@ -41,6 +41,8 @@ struct ColsumJob {
   float* out_b;
   int N, ln;
   int start, nbx;  // filled by colsum_grouped
+  float* part;     // filled by colsum_grouped: [2][nby][N] partials in the workspace
+  unsigned* cnt;   // [nbx] tickets (zero, self-resetting)
 };
 constexpr int kMaxColsum = 48;
 struct ColsumGroup {
@@ -48,7 +50,10 @@ struct ColsumGroup {
   ColsumJob job[kMaxColsum];
 };
 template <typename T>
-int colsum_grouped(const ColsumJob* jobs, int n, int R, cudaStream_t st);
+// part / cnt: deterministic workspace (colsum_grouped_ws_floats / _tickets);
+// NULL = one atomicAdd per column per block
+int colsum_grouped(const ColsumJob* jobs, int n, int R, cudaStream_t st, float* part = nullptr, unsigned* cnt = nullptr,
+                   long part_cap = 0, long cnt_cap = 0);
 template <typename T>
 int softmax_causal(const float* S, T* P, int Z, int Tn, cudaStream_t st);
 template <typename T>

@@ -71,7 +71,7 @@ struct SlotLayout {
   long yL, seed, lpart;  // stage-level (after the per-layer block); lpart: loss partials + ticket
   long slot_bytes;
   // work area
-  long w_S, w_dS, w_do, w_D, w_dq, w_cs, w_cnt, work_bytes;
+  long w_S, w_dS, w_do, w_D, w_dq, w_cs, w_cnt, cs_floats, cs_tickets, work_bytes;
   bool flash;  // fused tcgen05 attention (bf16, head dim 128)
 };
 
@@ -179,11 +179,15 @@ static int compute_layout(const adaptra_stage_desc_t& d, SlotLayout& L) {
     w = L.flash ? align256(L.w_dq + R * D * 4) : L.w_dq;
   }
   // deterministic column-sum workspace (bias / LN parameter gradients of W):
-  // partials [2][ceil(R/256)][max N] fp32 and one ticket per 64-column strip
-  const long maxN = std::max<long>(3 * D, F);
+  // partials [2][ceil(R/256)][N] fp32 and one ticket per 64-column strip for
+  // every sum of a two-slot W (the grouped launch runs them all at once);
+  // per layer the sums cover 7 d + d_ff columns (GPT; MLP: d + d_ff)
+  const long cols = 2L * d.n_layers * (7 * D + F);
+  L.cs_floats = 2 * ((R + 255) / 256) * cols;
+  L.cs_tickets = cols / 64 + 2L * d.n_layers * 6 + 64;
   L.w_cs = align256(w);
-  L.w_cnt = align256(L.w_cs + 2 * ((R + 255) / 256) * maxN * 4);
-  w = align256(L.w_cnt + ((maxN + 63) / 64) * 4);
+  L.w_cnt = align256(L.w_cs + L.cs_floats * 4);
+  w = align256(L.w_cnt + L.cs_tickets * 4);
   L.work_bytes = w;
   return ADAPTRA_OK;
 }
@@ -430,18 +434,18 @@ struct StageOps {
       for (auto& g : dw) TRY(gemm_simt(g, st));
       for (auto& g : dw_b) TRY(gemm_simt(g, st));
     }
-    // Column sums: one launch per sum by default.  The grouped launch is 13 %
-    // faster on the W op alone but one ~17k-block kernel crowds co-located
-    // stages' streams (1 GPU, 4 stages: -1.4 % step; 1 stage per GPU: within
-    // noise), so it is opt-in (ADAPTRA_COLSUM_GROUPED=1).
-    static const bool cs_grouped = getenv("ADAPTRA_COLSUM_GROUPED") && atoi(getenv("ADAPTRA_COLSUM_GROUPED")) == 1;
+    // Column sums (bias and LN parameter gradients): all of the op's sums in
+    // one deterministic grouped launch by default -- 15 % off a 3-layer C1 W
+    // op against one launch per sum (profiles/r02_op_bench_ab.jsonl);
+    // ADAPTRA_COLSUM_GROUPED=0 for one launch per sum
+    static const bool cs_grouped = !(getenv("ADAPTRA_COLSUM_GROUPED") && atoi(getenv("ADAPTRA_COLSUM_GROUPED")) == 0);
     const long R = s->R;
+    float* part = (float*)((char*)s->d.work + s->L.w_cs);
+    unsigned* cnt = (unsigned*)((char*)s->d.work + s->L.w_cnt);
     if (cs_grouped) {
-      TRY(colsum_grouped<T>(cs.data(), (int)cs.size(), (int)R, st));
+      TRY(colsum_grouped<T>(cs.data(), (int)cs.size(), (int)R, st, part, cnt, s->L.cs_floats, s->L.cs_tickets));
     } else {
       for (const auto& j : cs) {
-        float* part = (float*)((char*)s->d.work + s->L.w_cs);
-        unsigned* cnt = (unsigned*)((char*)s->d.work + s->L.w_cnt);
         if (j.ln)
           TRY(ln_param_grad<T>((const T*)j.y, (const T*)j.x, j.mean, j.rstd, j.out_a, j.out_b, (int)R, j.N, st, part,
                                cnt));

@@ -1,7 +1,8 @@
 """The non-default kernel paths behind environment toggles (read once per
 process by libadaptra) re-run the stage F / B / W parity suites (small and
-full-size) in a fresh process: grouped column sums (opt-in), one dW launch per product instead of
-the grouped GEMM, epilogue inputs by LDG instead of TMA."""
+full-size) in a fresh process: one column-sum launch per sum instead of the
+grouped one, one dW launch per product instead of the grouped GEMM, epilogue
+inputs by LDG instead of TMA, no W pairs, the one-tile attention forward."""
 import os
 import subprocess
 import sys
@@ -12,10 +13,11 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("toggle", [{"ADAPTRA_COLSUM_GROUPED": "1"},
+@pytest.mark.parametrize("toggle", [{"ADAPTRA_COLSUM_GROUPED": "0"},
                                     {"ADAPTRA_GEMM_GROUPED": "0"},
                                     {"ADAPTRA_EPI_IN_LDG": "1"},
-                                    {"ADAPTRA_W_PAIRS": "0"}])
+                                    {"ADAPTRA_W_PAIRS": "0"},
+                                    {"ADAPTRA_ATTN_FWD": "single"}])
 def test_stage_parity_under_toggle(toggle):
     env = dict(os.environ, **toggle)
     files = ["tests/test_gpu_stage.py", "tests/test_gpu_fullsize.py"]
