@@ -1244,10 +1244,13 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
   // ADAPTRA_ATTN_FWD_GRID=items: one CTA per item (the non-persistent launch, for comparison)
   static const bool per_item = getenv("ADAPTRA_ATTN_FWD_GRID") && !strcmp(getenv("ADAPTRA_ATTN_FWD_GRID"), "items");
   const int items = b * H * (T / AT), grid = per_item ? items : std::min(items, n_sm[dev & 31]);
-  // ping-pong over query-block pairs (default; $ADAPTRA_ATTN_FWD=single for
-  // one query tile per item), which needs an even number of query blocks
-  static const bool pp_off = getenv("ADAPTRA_ATTN_FWD") && !strcmp(getenv("ADAPTRA_ATTN_FWD"), "single");
-  if (!pp_off && (T / AT) % 2 == 0 && !per_item) {
+  // ping-pong over query-block pairs: opt-in ($ADAPTRA_ATTN_FWD=pp; needs an
+  // even number of query blocks).  Correct (parity tests), but measured 1.75x
+  // slower than the one-tile kernel on C1 shapes (56 vs 32 us per launch,
+  // profiles/r02_op_bench_pp.jsonl): two softmax groups sharing the SM's
+  // MUFU / issue slots plus the second TMEM pass cost more than the overlap gains
+  static const bool pp_on = getenv("ADAPTRA_ATTN_FWD") && !strcmp(getenv("ADAPTRA_ATTN_FWD"), "pp");
+  if (pp_on && (T / AT) % 2 == 0 && !per_item) {
     const int pitems = b * H * (T / AT) / 2;
     attn_fwd_pp_kernel<<<std::min(pitems, n_sm[dev & 31]), kPPThreads, kPPSmem, st>>>(m, a);
   } else if (nq == 4) {

@@ -423,9 +423,9 @@ struct StageOps {
   // microbatch, and every tile's epilogue is amortised over twice the K loop
   int Wop(int slot, int slot_b = -1) {
     std::vector<adaptra_gemm_desc_t> dw, dw_b;
-    std::vector<ColsumJob> cs;
+    std::vector<ColsumJob> cs, cs_b;  // per slot: the two slots' sums add into the same gradients
     collect_w(slot, dw, cs);
-    if (slot_b >= 0) collect_w(slot_b, dw_b, cs);
+    if (slot_b >= 0) collect_w(slot_b, dw_b, cs_b);
     if (dt() == ADAPTRA_BF16) {
       for (size_t i = 0; i < dw.size(); i += 24)
         TRY(gemm_tc_grouped(dw.data() + i, (int)std::min<size_t>(24, dw.size() - i), st,
@@ -443,8 +443,13 @@ struct StageOps {
     float* part = (float*)((char*)s->d.work + s->L.w_cs);
     unsigned* cnt = (unsigned*)((char*)s->d.work + s->L.w_cnt);
     if (cs_grouped) {
+      // one launch per slot: a launch's jobs must not share an output (the
+      // last block of a strip adds into it without atomics)
       TRY(colsum_grouped<T>(cs.data(), (int)cs.size(), (int)R, st, part, cnt, s->L.cs_floats, s->L.cs_tickets));
+      if (!cs_b.empty())
+        TRY(colsum_grouped<T>(cs_b.data(), (int)cs_b.size(), (int)R, st, part, cnt, s->L.cs_floats, s->L.cs_tickets));
     } else {
+      cs.insert(cs.end(), cs_b.begin(), cs_b.end());
       for (const auto& j : cs) {
         if (j.ln)
           TRY(ln_param_grad<T>((const T*)j.y, (const T*)j.x, j.mean, j.rstd, j.out_a, j.out_b, (int)R, j.N, st, part,

@@ -5,7 +5,7 @@ timeout 300 python -m pytest tests/test_gpu_stage.py -x -q -k "BF16 or 1-" > gpu
 tail -3 gpurun_out/r02_pytest_pp_stage.txt
 timeout 300 python -m pytest tests/test_gpu_fullsize.py -x -q > gpurun_out/r02_pytest_pp_full.txt 2>&1; echo full rc=$?
 tail -3 gpurun_out/r02_pytest_pp_full.txt
-for v in "" "ADAPTRA_ATTN_FWD=single"; do
+for v in "" "ADAPTRA_ATTN_FWD=single" "ADAPTRA_COLSUM_GROUPED=0"; do
   env $v REPS=8 timeout 300 python scripts/op_bench.py >> gpurun_out/r02_op_bench_pp.jsonl 2>&1
   env $v REPS=8 timeout 300 python scripts/op_bench.py >> gpurun_out/r02_op_bench_pp.jsonl 2>&1
 done

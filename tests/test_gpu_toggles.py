@@ -2,7 +2,7 @@
 process by libadaptra) re-run the stage F / B / W parity suites (small and
 full-size) in a fresh process: one column-sum launch per sum instead of the
 grouped one, one dW launch per product instead of the grouped GEMM, epilogue
-inputs by LDG instead of TMA, no W pairs, the one-tile attention forward."""
+inputs by LDG instead of TMA, no W pairs, the ping-pong attention forward (opt-in)."""
 import os
 import subprocess
 import sys
@@ -17,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
                                     {"ADAPTRA_GEMM_GROUPED": "0"},
                                     {"ADAPTRA_EPI_IN_LDG": "1"},
                                     {"ADAPTRA_W_PAIRS": "0"},
-                                    {"ADAPTRA_ATTN_FWD": "single"}])
+                                    {"ADAPTRA_ATTN_FWD": "pp"}])
 def test_stage_parity_under_toggle(toggle):
     env = dict(os.environ, **toggle)
     files = ["tests/test_gpu_stage.py", "tests/test_gpu_fullsize.py"]
