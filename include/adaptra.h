@@ -521,6 +521,14 @@ int adaptra_run_iteration(adaptra_exec_t e, const adaptra_op_t* ops, int32_t n, 
  * when even the host pool cannot hold the order's demand.  n_host_slots = 0
  * disables. */
 int adaptra_exec_set_offload(adaptra_exec_t e, void* host_pool, int32_t n_host_slots, int32_t window);
+/* The executor's offload plan for one stage's op order, as a pure host
+ * function (what adaptra_run_iteration plans internally): n_dev device slots,
+ * n_host host slots, flags ADAPTRA_MERGE_W.  slot_out[n] = device slot each op
+ * uses; actions_out[cap][6] = {spill (1) / prefetch (0), mb, device slot, host
+ * slot, issued after op q, awaited by op q'}; *n_actions_out = total.
+ * ENOMEM when the order cannot run in n_dev + n_host slots. */
+int adaptra_offload_plan(const adaptra_op_t* ops, int32_t n, int32_t N, int32_t n_dev, int32_t n_host, int32_t window,
+                         uint32_t flags, int32_t* slot_out, int32_t* actions_out, int32_t cap, int32_t* n_actions_out);
 /* Spills and prefetches planned for the last iteration; bytes moved since creation. */
 int adaptra_exec_offload_stats(adaptra_exec_t e, int32_t* n_spill, int32_t* n_prefetch, int64_t* bytes);
 

@@ -170,6 +170,7 @@ _SIGS = {
     "adaptra_exec_set_nccl": (_i32, [_vp, _vp, _i32, _i32, _i64]),
     "adaptra_exec_set_offload": (_i32, [_vp, _vp, _i32, _i32]),
     "adaptra_exec_offload_stats": (_i32, [_vp, _P(_i32), _P(_i32), _P(_i64)]),
+    "adaptra_offload_plan": (_i32, [_P(Op), _i32, _i32, _i32, _i32, _i32, _u32, _P(_i32), _P(_i32), _i32, _P(_i32)]),
     "adaptra_nccl_unique_id": (_i32, [_P(C.c_uint8)]),
     "adaptra_nccl_comm_init": (_i32, [_P(C.c_uint8), _i32, _i32, _i32, _P(_vp)]),
     "adaptra_nccl_comm_destroy": (_i32, [_vp]),

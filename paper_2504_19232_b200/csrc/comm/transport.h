@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "../../../include/adaptra.h"
 
 namespace adaptra {
@@ -19,6 +21,18 @@ int nccl_p2p(void* comm, const void* send_buf, int64_t send_bytes, int send_peer
 int64_t outbox_latency(adaptra_outbox_t ob);
 void* outbox_local_slot(adaptra_outbox_t ob, int mb);
 int64_t outbox_bytes(adaptra_outbox_t ob);
+// N4 offload plan of one stage's iteration (exec.cpp)
+struct OffAct {
+  int spill;  // 1 = D2H spill, 0 = H2D prefetch
+  int mb, dslot, hslot, from_slot, id;
+};
+struct SlotPlan {
+  std::vector<int> slot;                   // device slot of op q
+  std::vector<std::vector<OffAct>> after;  // offload actions issued after op q
+  std::vector<std::vector<int>> wait;      // action ids op q waits for
+  int n_spill = 0, n_prefetch = 0;
+};
+int offload_plan(const adaptra_op_t* ops, int n, int N, int D, int H, int window, bool merge, SlotPlan& P);
 // Block the calling host thread until the host-memory flag *p >= v.
 int host_wait_hmem(const volatile uint32_t* p, uint32_t v);
 }  // namespace adaptra

@@ -46,6 +46,145 @@ static const bool g_dbg = getenv("ADAPTRA_DEBUG") != nullptr;
     }                                             \
   } while (0)
 
+namespace adaptra {
+// N4 stash offload: the F->W stash slots of a
+// stage live in D device slots; with a host pool of H slots, slots whose W is
+// far in the op order are spilled there after their B and prefetched back
+// before their W, so the stage can hold more in-flight microbatches than fit
+// in HBM.  The plan is static per iteration (the order is known in advance):
+// Belady eviction (the complete slot whose W is furthest away) when an F
+// needs a slot, the spill D2H issued right after the victim's B, the prefetch
+// H2D up to `window` ops ahead of its W when a device slot is free (and the
+// F ops before that W leave one), at the latest right before the W.
+int offload_plan(const adaptra_op_t* ops, int n, int N, int D, int H, int window, bool merge, SlotPlan& P) {
+  P.slot.assign(n, -1);
+  P.after.assign(n, {});
+  P.wait.assign(n, {});
+  P.n_spill = P.n_prefetch = 0;
+  std::vector<int> bpos(N + 1, INT32_MAX), wpos(N + 1, INT32_MAX), state(N + 1, 0), dsl(N + 1, -1), hsl(N + 1, -1);
+  for (int q = n - 1; q >= 0; --q) {
+    const int mb = ops[q].mb;
+    if (mb < 1 || mb > N || ops[q].kind < 0 || ops[q].kind > 2) return set_error(ADAPTRA_EINVAL, "exec: bad op");
+    if (ops[q].kind == ADAPTRA_OP_B) bpos[mb] = q;
+    if (ops[q].kind == ADAPTRA_OP_W || (merge && ops[q].kind == ADAPTRA_OP_B)) wpos[mb] = q;
+  }
+  std::vector<int> free_dev;
+  // free host slots with the issue position of the prefetch that freed them:
+  // every copy runs in issue order on one offload stream, so a spill may
+  // reuse a host slot only if it is issued at or after that prefetch
+  std::vector<std::pair<int, int>> free_host;
+  for (int k = D - 1; k >= 0; --k) free_dev.push_back(k);
+  for (int k = H - 1; k >= 0; --k) free_host.push_back({k, -1});
+  int next_id = 0;
+  auto evict = [&](int q, int keep) -> int {
+    int best = -1;
+    for (int mb = 1; mb <= N; ++mb)
+      if (state[mb] == 1 && mb != keep && bpos[mb] < q && wpos[mb] > q && (best < 0 || wpos[mb] > wpos[best]))
+        best = mb;
+    if (best < 0) return set_error(ADAPTRA_ENOMEM, "exec: stash slots exhausted (no complete slot to offload)");
+    if (free_host.empty()) return set_error(ADAPTRA_ENOMEM, "exec: stash slots exhausted (host offload pool full)");
+    size_t hk = 0;  // the host slot free the longest
+    for (size_t k = 1; k < free_host.size(); ++k)
+      if (free_host[k].second < free_host[hk].second) hk = k;
+    const int h = free_host[hk].first;
+    // issued right after the victim's B, or after the prefetch that freed h
+    // (always <= q - 1: every prefetch planned so far is issued by then)
+    const int at = std::max(bpos[best], free_host[hk].second);
+    free_host.erase(free_host.begin() + hk);
+    OffAct a{1, best, dsl[best], h, dsl[best], next_id++};
+    P.after[at].push_back(a);
+    P.wait[q].push_back(a.id);
+    P.n_spill++;
+    state[best] = 2;
+    hsl[best] = h;
+    free_dev.push_back(dsl[best]);
+    return ADAPTRA_OK;
+  };
+  auto prefetch = [&](int mb, int after_q, int w_q) {
+    const int s = free_dev.back();
+    free_dev.pop_back();
+    OffAct a{0, mb, s, hsl[mb], -1, next_id++};
+    P.after[after_q].push_back(a);
+    P.wait[w_q].push_back(a.id);
+    P.n_prefetch++;
+    free_host.push_back({hsl[mb], after_q});
+    state[mb] = 1;
+    dsl[mb] = s;
+  };
+  for (int q = 0; q < n; ++q) {
+    const adaptra_op_t& o = ops[q];
+    const int mb = o.mb;
+    if (o.kind == ADAPTRA_OP_F) {
+      if (state[mb] != 0) return set_error(ADAPTRA_EINVAL, "exec: F twice");
+      int rc;
+      if (free_dev.empty() && (rc = evict(q, -1))) return rc;
+      dsl[mb] = free_dev.back();
+      free_dev.pop_back();
+      state[mb] = 1;
+      P.slot[q] = dsl[mb];
+    } else {
+      if (state[mb] == 0) return set_error(ADAPTRA_EINVAL, o.kind == ADAPTRA_OP_B ? "exec: B before F" : "exec: W before F");
+      if (state[mb] == 2) {  // W of a spilled slot not prefetched yet: fetch now
+        int rc;
+        if (free_dev.empty() && (rc = evict(q, mb))) return rc;
+        if (q == 0) return set_error(ADAPTRA_EINVAL, "exec: W first");
+        prefetch(mb, q - 1, q);
+      }
+      P.slot[q] = dsl[mb];
+      if (o.kind == ADAPTRA_OP_W || merge) {
+        free_dev.push_back(dsl[mb]);
+        state[mb] = 0;
+      }
+    }
+    // early prefetch: the spilled slot with the nearest W, if it is within
+    // `window` ops and the F ops before it leave a device slot free
+    while (H > 0 && !free_dev.empty()) {
+      int nb = -1;
+      for (int m = 1; m <= N; ++m)
+        if (state[m] == 2 && (nb < 0 || wpos[m] < wpos[nb])) nb = m;
+      if (nb < 0 || wpos[nb] > q + window) break;
+      int nf = 0;
+      for (int r = q + 1; r < wpos[nb]; ++r) nf += ops[r].kind == ADAPTRA_OP_F;
+      if ((int)free_dev.size() <= nf) break;
+      prefetch(nb, q, wpos[nb]);
+    }
+  }
+  return ADAPTRA_OK;
+}
+}  // namespace adaptra
+
+extern "C" int adaptra_offload_plan(const adaptra_op_t* ops, int32_t n, int32_t N, int32_t n_dev, int32_t n_host,
+                                    int32_t window, uint32_t flags, int32_t* slot_out, int32_t* actions_out,
+                                    int32_t cap, int32_t* n_actions_out) {
+  if (!ops || n < 0 || N < 1 || n_dev < 1 || n_host < 0 || !slot_out || cap < 0 || (cap > 0 && !actions_out) ||
+      !n_actions_out)
+    return set_error(ADAPTRA_EINVAL, "offload_plan: bad args");
+  adaptra::SlotPlan P;
+  int rc = adaptra::offload_plan(ops, n, N, n_dev, n_host, window > 0 ? window : 4, flags & ADAPTRA_MERGE_W, P);
+  if (rc) return rc;
+  for (int q = 0; q < n; ++q) slot_out[q] = P.slot[q];
+  int k = 0;
+  for (int q = 0; q < n; ++q)
+    for (const auto& a : P.after[q]) {
+      if (k < cap) {
+        int32_t* r = actions_out + 6 * k;
+        r[0] = a.spill;
+        r[1] = a.mb;
+        r[2] = a.dslot;
+        r[3] = a.hslot;
+        r[4] = q;  // issued right after op q
+        int w = -1;
+        for (int t = 0; t < n && w < 0; ++t)
+          for (int id : P.wait[t])
+            if (id == a.id) w = t;
+        r[5] = w;  // the op that waits for it
+      }
+      ++k;
+    }
+  *n_actions_out = k;
+  return ADAPTRA_OK;
+}
+
 struct adaptra_exec {
   adaptra_exec_desc_t d{};
   int dev = 0;
@@ -80,16 +219,7 @@ struct adaptra_exec {
   // in advance): Belady eviction (the complete slot whose W is furthest away)
   // when an F needs a slot, spill D2H issued right after the victim's B,
   // prefetch H2D up to `pf_window` ops ahead of its W when a slot is free.
-  struct OffAct {
-    int spill;  // 1 = D2H spill, 0 = H2D prefetch
-    int mb, dslot, hslot, from_slot, id;
-  };
-  struct SlotPlan {
-    std::vector<int> slot;                      // device slot of op q
-    std::vector<std::vector<OffAct>> after;     // offload actions issued after op q
-    std::vector<std::vector<int>> wait;         // action ids op q waits for
-    int n_spill = 0, n_prefetch = 0;
-  } P;
+  adaptra::SlotPlan P;
   char* host_pool = nullptr;
   int n_host = 0, pf_window = 4;
   cudaStream_t off = nullptr;
@@ -98,101 +228,20 @@ struct adaptra_exec {
   int64_t spilled_bytes = 0;
 
   int plan_slots() {
-    const int N = d.n_microbatches, D = stage_n_slots(d.stage), n = (int)ops.size();
-    const bool merge = flags & ADAPTRA_MERGE_W;
-    P.slot.assign(n, -1);
-    P.after.assign(n, {});
-    P.wait.assign(n, {});
-    P.n_spill = P.n_prefetch = 0;
-    std::vector<int> bpos(N + 1, INT32_MAX), wpos(N + 1, INT32_MAX), state(N + 1, 0), dsl(N + 1, -1),
-        hsl(N + 1, -1);
-    for (int q = n - 1; q >= 0; --q) {
-      const int mb = ops[q].mb;
-      if (mb < 1 || mb > N) return set_error(ADAPTRA_EINVAL, "exec: bad microbatch");
-      if (ops[q].kind == ADAPTRA_OP_B) bpos[mb] = q;
-      if (ops[q].kind == ADAPTRA_OP_W || (merge && ops[q].kind == ADAPTRA_OP_B)) wpos[mb] = q;
-    }
-    std::vector<int> free_dev, free_host;
-    for (int k = D - 1; k >= 0; --k) free_dev.push_back(k);
-    for (int k = n_host - 1; k >= 0; --k) free_host.push_back(k);
-    int next_id = 0;
-    auto evict = [&](int q, int keep) -> int {
-      int best = -1;
-      for (int mb = 1; mb <= N; ++mb)
-        if (state[mb] == 1 && mb != keep && bpos[mb] < q && wpos[mb] > q && (best < 0 || wpos[mb] > wpos[best]))
-          best = mb;
-      if (best < 0) return set_error(ADAPTRA_ENOMEM, "exec: stash slots exhausted (no complete slot to offload)");
-      if (free_host.empty()) return set_error(ADAPTRA_ENOMEM, "exec: stash slots exhausted (host offload pool full)");
-      const int h = free_host.back();
-      free_host.pop_back();
-      OffAct a{1, best, dsl[best], h, dsl[best], next_id++};
-      P.after[bpos[best]].push_back(a);
-      P.wait[q].push_back(a.id);
-      P.n_spill++;
-      state[best] = 2;
-      hsl[best] = h;
-      free_dev.push_back(dsl[best]);
-      return ADAPTRA_OK;
-    };
-    auto prefetch = [&](int mb, int after_q, int w_q) {
-      const int s = free_dev.back();
-      free_dev.pop_back();
-      OffAct a{0, mb, s, hsl[mb], -1, next_id++};
-      P.after[after_q].push_back(a);
-      P.wait[w_q].push_back(a.id);
-      P.n_prefetch++;
-      free_host.push_back(hsl[mb]);
-      state[mb] = 1;
-      dsl[mb] = s;
-    };
-    for (int q = 0; q < n; ++q) {
-      const adaptra_op_t& o = ops[q];
-      const int mb = o.mb;
-      if (o.kind == ADAPTRA_OP_F) {
-        if (state[mb] != 0) return set_error(ADAPTRA_EINVAL, "exec: F twice");
-        int rc;
-        if (free_dev.empty() && (rc = evict(q, -1))) return rc;
-        dsl[mb] = free_dev.back();
-        free_dev.pop_back();
-        state[mb] = 1;
-        P.slot[q] = dsl[mb];
-      } else {
-        if (state[mb] == 0) return set_error(ADAPTRA_EINVAL, o.kind == ADAPTRA_OP_B ? "exec: B before F" : "exec: W before F");
-        if (state[mb] == 2) {                 // W of a spilled slot not prefetched yet: fetch now
-          int rc;
-          if (free_dev.empty() && (rc = evict(q, mb))) return rc;
-          if (q == 0) return set_error(ADAPTRA_EINVAL, "exec: W first");
-          prefetch(mb, q - 1, q);
-        }
-        P.slot[q] = dsl[mb];
-        if (o.kind == ADAPTRA_OP_W || merge) {
-          free_dev.push_back(dsl[mb]);
-          state[mb] = 0;
-        }
-      }
-      // early prefetch: the spilled slot with the nearest W, if it is within
-      // pf_window ops and the F ops before it leave a device slot free
-      while (n_host > 0 && !free_dev.empty()) {
-        int nb = -1;
-        for (int m = 1; m <= N; ++m)
-          if (state[m] == 2 && (nb < 0 || wpos[m] < wpos[nb])) nb = m;
-        if (nb < 0 || wpos[nb] > q + pf_window) break;
-        int nf = 0;
-        for (int r = q + 1; r < wpos[nb]; ++r) nf += ops[r].kind == ADAPTRA_OP_F;
-        if ((int)free_dev.size() <= nf) break;
-        prefetch(nb, q, wpos[nb]);
-      }
-    }
-    if (next_id > (int)ev_act.size()) {
+    int rc = adaptra::offload_plan(ops.data(), (int)ops.size(), d.n_microbatches, stage_n_slots(d.stage), n_host,
+                                   pf_window, flags & ADAPTRA_MERGE_W, P);
+    if (rc) return rc;
+    const int n_act = P.n_spill + P.n_prefetch;
+    if (n_act > (int)ev_act.size()) {
       cudaSetDevice(dev);
       const size_t old = ev_act.size();
-      ev_act.resize(next_id);
+      ev_act.resize(n_act);
       for (size_t k = old; k < ev_act.size(); ++k)
         ADAPTRA_CUDA_TRY(cudaEventCreateWithFlags(&ev_act[k], cudaEventDisableTiming));
     }
-    if (next_id > 0 && !off) return set_error(ADAPTRA_EINVAL, "exec: offload planned without a host pool");
-    saved_meta.assign(N + 1, {nullptr, nullptr});
-    from_slot_of.assign(N + 1, -1);
+    if (n_act > 0 && !off) return set_error(ADAPTRA_EINVAL, "exec: offload planned without a host pool");
+    saved_meta.assign(d.n_microbatches + 1, {nullptr, nullptr});
+    from_slot_of.assign(d.n_microbatches + 1, -1);
     return ADAPTRA_OK;
   }
 

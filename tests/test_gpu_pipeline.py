@@ -185,10 +185,12 @@ def test_stash_offload_matches_device_run(kind, dtype, S, N, Lt, d, dff, H, b, T
         ref_pipe.close()
     # device slots per stage = the order's peak in-flight forwards (F - B):
     # only slots whose B is done can move to the host; the F->W demand is N
-    peak = []
+    peak = []                    # incomplete forwards (+ the slot a W brings back)
     for ops in orders:
         f = bb = p = 0
         for k, _ in ops:
+            if k == "W":
+                p = max(p, f - bb + 1)
             f += k == "F"
             bb += k == "B"
             p = max(p, f - bb)
