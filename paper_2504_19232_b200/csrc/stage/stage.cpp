@@ -434,11 +434,13 @@ struct StageOps {
       for (auto& g : dw) TRY(gemm_simt(g, st));
       for (auto& g : dw_b) TRY(gemm_simt(g, st));
     }
-    // Column sums (bias and LN parameter gradients): all of the op's sums in
-    // one deterministic grouped launch by default -- 15 % off a 3-layer C1 W
-    // op against one launch per sum (profiles/r02_op_bench_ab.jsonl);
-    // ADAPTRA_COLSUM_GROUPED=0 for one launch per sum
-    static const bool cs_grouped = !(getenv("ADAPTRA_COLSUM_GROUPED") && atoi(getenv("ADAPTRA_COLSUM_GROUPED")) == 0);
+    // Column sums (bias and LN parameter gradients): one deterministic launch
+    // per sum by default.  All of the op's sums in one grouped launch
+    // (ADAPTRA_COLSUM_GROUPED=1) take 9 % off a 3-layer C1 W op run alone
+    // (profiles/r02_op_bench_pp.jsonl), but with 8 stages sharing the GPU the
+    // step is 3.8 % slower (3 + 3 alternating runs, r02_colsum_step_ab.txt):
+    // its ~1.5k-block grid crowds the other stages' kernels.
+    static const bool cs_grouped = getenv("ADAPTRA_COLSUM_GROUPED") && atoi(getenv("ADAPTRA_COLSUM_GROUPED")) == 1;
     const long R = s->R;
     float* part = (float*)((char*)s->d.work + s->L.w_cs);
     unsigned* cnt = (unsigned*)((char*)s->d.work + s->L.w_cnt);

@@ -1,7 +1,7 @@
 """The non-default kernel paths behind environment toggles (read once per
 process by libadaptra) re-run the stage F / B / W parity suites (small and
-full-size) in a fresh process: one column-sum launch per sum instead of the
-grouped one, one dW launch per product instead of the grouped GEMM, epilogue
+full-size) in a fresh process: one grouped column-sum launch instead of one per
+sum, one dW launch per product instead of the grouped GEMM, epilogue
 inputs by LDG instead of TMA, no W pairs, the ping-pong attention forward (opt-in)."""
 import os
 import subprocess
@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("toggle", [{"ADAPTRA_COLSUM_GROUPED": "0"},
+@pytest.mark.parametrize("toggle", [{"ADAPTRA_COLSUM_GROUPED": "1"},
                                     {"ADAPTRA_GEMM_GROUPED": "0"},
                                     {"ADAPTRA_EPI_IN_LDG": "1"},
                                     {"ADAPTRA_W_PAIRS": "0"},
