@@ -515,29 +515,43 @@ def measure_host_path(pipe, torch):
 
 
 def cpu_baseline(model, S, N, budget_s=15.0):
-    """The oracle as it stands (float64 numpy) on the host cores: a bounded sample
-    = F+B+W of one GPT block on one microbatch (scaled to tokens/s of the whole
-    n_layers-deep model), plus Schedule() of the oracle."""
+    """The oracle as it stands on the host cores: a bounded sample
+    of the same workload = F+B+W of one GPT block on one microbatch in the
+    oracle's float32 mode (numpy, BLAS on all host cores), plus the oracle's
+    Schedule() of the step's plan; tokens/s scaled to the whole step
+    (n_layers blocks x N microbatches + one Schedule())."""
     import numpy as np
     from oracle import numerics as nu
+    from oracle import sched as osc
     import synthetic as sy
     d, T = model.d, model.T
-    p = sy.gpt_params(0, 1, 1, d, 4 * d, perturb=False)[0][0]
-    x = sy.microbatches(1, 1, 1, T, d)[0]
+    Ls = 1
+    p = {k: v.astype(np.float32) for k, v in sy.gpt_params(0, 1, 1, d, 4 * d, perturb=False)[0][0].items()}
+    x = sy.microbatches(1, 1, 1, T, d)[0].astype(np.float32)
     t0 = time.perf_counter()
-    y, cache = nu.block_F("gpt", p, x.astype(np.float64), model.n_heads)
-    dx, gc = nu.block_B("gpt", {k: v.astype(np.float64) for k, v in p.items()}, cache, np.ones_like(y) / y.size,
-                        model.n_heads)
-    nu.block_W("gpt", cache, gc)
-    dt = time.perf_counter() - t0
-    per_token_s = dt * model.n_layers / T
+    h = x
+    caches = []
+    for _ in range(Ls):
+        h, cache = nu.block_F("gpt", p, h, model.n_heads)
+        caches.append(cache)
+    dy = np.ones_like(h) / h.size
+    for cache in reversed(caches):
+        dy, gc = nu.block_B("gpt", p, cache, dy, model.n_heads)
+        nu.block_W("gpt", cache, gc)
+    t_stage = time.perf_counter() - t0
+    t = [10] * S
+    t1 = time.perf_counter()
+    osc.schedule(S, N, t, t, t, [0] * (S - 1), osc.get_adapted_warmup_fwds(S, N, t, t, [0] * (S - 1)), 1)
+    t_sched = time.perf_counter() - t1
+    step_s = t_stage * model.n_layers * N + t_sched
     try:
         cores = len(os.sched_getaffinity(0))
     except Exception:
         cores = os.cpu_count()
-    return {"value": round(1.0 / per_token_s, 3), "unit": "tokens/s", "cores": cores, "kind": "oracle",
-            "sample": f"oracle F+B+W of 1 of {model.n_layers} GPT blocks on 1 microbatch "
-                      f"(T={T}, d={d}), float64 numpy, {dt:.1f}s; tokens/s scaled to the full stack"}
+    return {"value": round(N * model.tokens_per_mb / step_s, 3), "unit": "tokens/s", "cores": cores, "kind": "oracle",
+            "sample": f"oracle float32 F+B+W of one GPT block (T={T}, d={d}) on 1 microbatch: {t_stage:.1f} s, "
+                      f"+ Schedule() of S={S}, N={N}: {t_sched * 1e3:.0f} ms; scaled to {model.n_layers} blocks x "
+                      f"{N} microbatches per step"}
 
 
 def reference_arm(args, rank, world):
