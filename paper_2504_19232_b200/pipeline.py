@@ -446,6 +446,28 @@ class Pipeline:
             st.close()
 
 
+# ---------------------------------------------------------------- metrics
+def iteration_metrics(results, orders):
+    """a11 (R15): bubble rates of one executed iteration from the
+    executor's per-op CUDA-event times.  results = {stage: stats with
+    "op_times"} for every stage (gathered over ranks); orders[i] the stage's
+    (kind, mb) list.  T = last op end - first op start over all stages;
+    utilisation bubble = 1 - sum busy / (S T); interior bubble = sum of each
+    stage's gaps inside its own span / sum of spans."""
+    S = len(orders)
+    t0 = min(st["op_times"][0][0] for st in results.values() if st["op_times"])
+    busy, span = [], []
+    T = 0
+    for i in range(S):
+        times = results[i]["op_times"]
+        busy.append(sum(e - s for s, e in times))
+        span.append((times[-1][1] - times[0][0]) if times else 0)
+        T = max(T, max((e for _, e in times), default=0) - t0)
+    util = 1.0 - sum(busy) / (S * T)
+    interior = (sum(sp - b for sp, b in zip(span, busy)) / sum(span)) if sum(span) else 0.0
+    return {"T_ns": T, "busy_ns": busy, "util_bubble": util, "interior_bubble": interior}
+
+
 # ---------------------------------------------------------------- schedules
 def orders_from(X):
     return [[(k, mb) for (k, mb, _s, _e) in ops] for ops in X]

@@ -214,3 +214,32 @@ def test_stash_offload_matches_device_run(kind, dtype, S, N, Lt, d, dff, H, b, T
         assert sum(v[0] for v in st.values()) > 0 and all(v[0] == v[1] for v in st.values())
     finally:
         pipe.close()
+
+
+def test_bubble_metrics_match_oracle_definition():
+    """a11 (R15): the bubble rates computed from an executed
+    iteration's per-op CUDA-event times equal oracle.sched.metrics on the same
+    times (utilisation and interior forms), under an injected straggler."""
+    from oracle import sched as sc
+    from paper_2504_19232_b200.pipeline import iteration_metrics
+    S, N = 4, 8
+    pipe, _, _ = _setup("gpt", L.BF16, S, N, 4, 256, 1024, 2, 1, 128)
+    try:
+        t = [1000] * S
+        a = Arm("adaptive", S, N, t, t, t)
+        c = [0, 3_000_000, 0]
+        pipe.set_latency(1, c[1])
+        orders = a.plan(c)
+        res = pipe.run(orders, want_times=True)
+        got = iteration_metrics(res.stats, orders)
+        t0 = min(st["op_times"][0][0] for st in res.stats.values())
+        X = [[sc.Op(k, mb, s - t0, e - t0) for (k, mb), (s, e) in zip(orders[i], res.stats[i]["op_times"])]
+             for i in range(S)]
+        ref = sc.metrics(S, X)
+        assert ref["T"] == got["T_ns"] and ref["busy"] == got["busy_ns"]
+        assert abs(ref["util_bubble"] - got["util_bubble"]) < 1e-12
+        assert abs(ref["interior_bubble"] - got["interior_bubble"]) < 1e-12
+        assert got["util_bubble"] > 0.0          # the 3 ms straggler leaves idle time
+    finally:
+        pipe.set_latency(1, 0)
+        pipe.close()
