@@ -220,6 +220,8 @@ def main():
         args.layers, args.d, args.heads = 32, 4096, 32
     model = ModelCfg(block="gpt", n_layers=args.layers, d=args.d, d_ff=4 * args.d, n_heads=args.heads,
                      b=1, T=args.T, dtype=L.BF16)
+    if os.environ.get("ADAPTRA_GEMM_SMS"):          # A/B knob (adaptra_set_tuning)
+        L.check(L.lib().adaptra_set_tuning(L.TUNE_GEMM_SMS, int(os.environ["ADAPTRA_GEMM_SMS"])))
     mode = L.LINK_DIRECT if args.link_mode == "direct" else L.LINK_P2P
     pipe = Pipeline(model, S, N, rank=rank, world=world, device=local_rank, group=group, link_mode=mode,
                     host_links=True, seed=0)

@@ -249,6 +249,14 @@ typedef struct adaptra_gemm_desc {
 
 int adaptra_gemm(const adaptra_gemm_desc_t* g, void* stream);
 
+/* Process-wide tuning knobs (take effect for launches after the call).
+ * ADAPTRA_TUNE_GEMM_SMS: SMs a persistent tcgen05 GEMM launch may occupy
+ * (rounded down to CTA pairs; 0 = all).  When several pipeline stages share a
+ * GPU, a smaller grid leaves SMs to the other stages' kernels and gives each
+ * CTA more tiles over which to pay its prologue and last epilogue. */
+#define ADAPTRA_TUNE_GEMM_SMS 1
+int adaptra_set_tuning(int32_t key, int64_t value);
+
 /* Live kernel timing (bench roofline): when enabled, every tcgen05 GEMM launch
  * is bracketed by CUDA events on its own stream; kind 0 = the stage's linear
  * layers (unbatched), kind 2 = the batched attention products (materialised

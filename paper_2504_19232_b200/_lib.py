@@ -17,6 +17,7 @@ EINVAL, EPLAN, EDEADLOCK, ECUDA, ENOMEM, ELINK, ETOOBIG = -1, -2, -3, -4, -5, -6
 
 OP_F, OP_B, OP_W = 0, 1, 2
 SEL_PAPER, SEL_CAP, MERGE_W = 0, 1, 2
+TUNE_GEMM_SMS = 1
 EXEC_INORDER = 16
 EXEC_NCCL = 32
 NCCL_ID_BYTES = 128
@@ -125,6 +126,7 @@ _SIGS = {
     "adaptra_planner_set_profile": (_i32, [_vp, _P(_i64), _P(_i64), _P(_i64)]),
     "adaptra_planner_step": (_i32, [_vp, _P(_i64), _P(Op), _P(_i32), _P(_i32), _P(_i32), _P(PlanInfo)]),
     "adaptra_gemm": (_i32, [_P(GemmDesc), _vp]),
+    "adaptra_set_tuning": (_i32, [_i32, _i64]),
     "adaptra_prof_enable": (_i32, [_i32]),
     "adaptra_launch_count": (_i64, []),
     "adaptra_p2p_copy": (_i32, [C.c_void_p, C.c_void_p, _i64, C.c_void_p]),

@@ -20,6 +20,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
@@ -545,6 +546,17 @@ static int num_sms() {
   return n;
 }
 
+// SMs a persistent GEMM launch may use (adaptra_set_tuning
+// ADAPTRA_TUNE_GEMM_SMS; 0 = all).  With several stages sharing a GPU the
+// other stages' kernels fill the rest, and each CTA runs more tiles, so its
+// prologue and its last epilogue are paid over more work.
+std::atomic<int> g_gemm_sms{0};
+static int gemm_sms() {
+  const int cap = g_gemm_sms.load(std::memory_order_relaxed);
+  const int n = num_sms();
+  return (cap > 0 && cap < n) ? cap : n;
+}
+
 template <int CG, int BN, int AMN, int BMN>
 static int launch_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
   using Cfg = TcCfg<CG, BN>;
@@ -579,7 +591,7 @@ static int launch_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
                (!g.aux || (g.ldaux % 8 == 0 && (uintptr_t)g.aux % 16 == 0)) &&
                (!g.R || (g.ldr % 8 == 0 && (uintptr_t)g.R % 16 == 0)) && ((uintptr_t)g.bias % 16 == 0) &&
                (g.c_1 % 8 == 0) && (g.c_2 % 8 == 0) && (g.aux_1 % 8 == 0) && (g.aux_2 % 8 == 0);
-  const int slots = num_sms() / CG;
+  const int slots = std::max(1, gemm_sms() / CG);
   int grid = (n_tiles < slots ? n_tiles : slots) * CG;
   if (grid < 1) return ADAPTRA_OK;
   // TMA-store epilogue when C (and the GELU aux output) decompose into 2-D
@@ -941,7 +953,7 @@ int gemm_tc_grouped(const adaptra_gemm_desc_t* gs, int n, cudaStream_t st, const
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
     attr_mask.fetch_or(1u << dev, std::memory_order_release);
   }
-  const int slots = num_sms() / 2;
+  const int slots = std::max(1, gemm_sms() / 2);
   const int grid = (tiles < slots ? tiles : slots) * 2;
   void* pb = prof_on() ? prof_begin(st) : nullptr;
   cudaLaunchConfig_t cfg{};
@@ -1024,3 +1036,14 @@ int gemm_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
 }
 
 }  // namespace adaptra
+
+extern "C" int adaptra_set_tuning(int32_t key, int64_t value) {
+  switch (key) {
+    case ADAPTRA_TUNE_GEMM_SMS:
+      if (value < 0) return adaptra::set_error(ADAPTRA_EINVAL, "set_tuning: SM count must be >= 0");
+      adaptra::g_gemm_sms.store((int)value);
+      return ADAPTRA_OK;
+    default:
+      return adaptra::set_error(ADAPTRA_EINVAL, "set_tuning: unknown key");
+  }
+}
