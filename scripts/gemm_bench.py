@@ -17,6 +17,7 @@ shapes = [
     # name, M, N, K, a_mn, b_mn, epi
     ("F_qkv", T, 3 * d, d, 0, 0, L.EPI_STORE),
     ("F_o", T, d, d, 0, 0, L.EPI_RESID),
+    ("F_o_plain", T, d, d, 0, 0, L.EPI_STORE),
     ("F_fc1", T, f, d, 0, 0, L.EPI_GELU),
     ("F_fc2", T, d, f, 0, 0, L.EPI_RESID),
     ("B_fc2", T, f, d, 0, 1, L.EPI_DGELU),
@@ -40,7 +41,7 @@ for name, M, N, K, amn, bmn, epi in shapes:
         kw["aux"] = torch.randn(M, N, device=dev).to(torch.bfloat16)
     if epi == L.EPI_RESID:
         kw["R"] = torch.randn(M, N, device=dev).to(torch.bfloat16)
-    if epi in (L.EPI_GELU, L.EPI_RESID, L.EPI_STORE):
+    if epi in (L.EPI_GELU, L.EPI_RESID, L.EPI_STORE) and not name.endswith("_plain"):
         kw["bias"] = torch.randn(N, device=dev)
     run = lambda: ops.gemm(A, B, Cm, M=M, N=N, K=K, a_mn=amn, b_mn=bmn, epi=epi, **kw)
     Am = A.t() if amn else A
