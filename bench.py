@@ -143,6 +143,7 @@ def isolated_kernels(model, lib):
     from paper_2504_19232_b200 import _lib as L
     from paper_2504_19232_b200.stage import Stage
 
+    lib.adaptra_set_tuning(L.TUNE_GEMM_SMS, 0)   # alone on the GPU: every SM
     st = Stage(L.BLOCK_GPT, model.dtype, 1, model.d, model.d_ff, model.n_heads, model.b, model.T, False, False,
                2, 2, "cuda")
     g = torch.Generator(device="cuda").manual_seed(0)
@@ -220,8 +221,6 @@ def main():
         args.layers, args.d, args.heads = 32, 4096, 32
     model = ModelCfg(block="gpt", n_layers=args.layers, d=args.d, d_ff=4 * args.d, n_heads=args.heads,
                      b=1, T=args.T, dtype=L.BF16)
-    if os.environ.get("ADAPTRA_GEMM_SMS"):          # A/B knob (adaptra_set_tuning)
-        L.check(L.lib().adaptra_set_tuning(L.TUNE_GEMM_SMS, int(os.environ["ADAPTRA_GEMM_SMS"])))
     mode = L.LINK_DIRECT if args.link_mode == "direct" else L.LINK_P2P
     pipe = Pipeline(model, S, N, rank=rank, world=world, device=local_rank, group=group, link_mode=mode,
                     host_links=True, seed=0)
