@@ -144,6 +144,7 @@ def isolated_kernels(model, lib):
     from paper_2504_19232_b200.stage import Stage
 
     lib.adaptra_set_tuning(L.TUNE_GEMM_SMS, 0)   # alone on the GPU: every SM
+    lib.adaptra_set_tuning(L.TUNE_ATTN_SMS, 0)
     st = Stage(L.BLOCK_GPT, model.dtype, 1, model.d, model.d_ff, model.n_heads, model.b, model.T, False, False,
                2, 2, "cuda")
     g = torch.Generator(device="cuda").manual_seed(0)

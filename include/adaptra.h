@@ -255,6 +255,8 @@ int adaptra_gemm(const adaptra_gemm_desc_t* g, void* stream);
  * GPU, a smaller grid leaves SMs to the other stages' kernels and gives each
  * CTA more tiles over which to pay its prologue and last epilogue. */
 #define ADAPTRA_TUNE_GEMM_SMS 1
+/* ADAPTRA_TUNE_ATTN_SMS: the same cap for the persistent attention forward. */
+#define ADAPTRA_TUNE_ATTN_SMS 2
 int adaptra_set_tuning(int32_t key, int64_t value);
 
 /* Live kernel timing (bench roofline): when enabled, every tcgen05 GEMM launch

@@ -18,6 +18,7 @@ EINVAL, EPLAN, EDEADLOCK, ECUDA, ENOMEM, ELINK, ETOOBIG = -1, -2, -3, -4, -5, -6
 OP_F, OP_B, OP_W = 0, 1, 2
 SEL_PAPER, SEL_CAP, MERGE_W = 0, 1, 2
 TUNE_GEMM_SMS = 1
+TUNE_ATTN_SMS = 2
 EXEC_INORDER = 16
 EXEC_NCCL = 32
 NCCL_ID_BYTES = 128

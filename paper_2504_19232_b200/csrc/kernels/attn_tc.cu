@@ -1210,6 +1210,10 @@ static int fwd_blocks(int c) {  // total key blocks of persistent CTA c (snake d
 }
 static int bwd_blocks(int i) { return g_nqb - (i / g_Z); }
 
+// SMs the persistent attention forward may use (adaptra_set_tuning
+// ADAPTRA_TUNE_ATTN_SMS; 0 = all)
+std::atomic<int> g_attn_sms{0};
+
 int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d, cudaStream_t st) {
   if (d != H * AT || T % AT) return set_error(ADAPTRA_EINVAL, "attn_fwd_tc: head dim 128 and T % 128 required");
   CUtensorMap m;
@@ -1243,7 +1247,9 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
   if (!n_sm[dev & 31]) cudaDeviceGetAttribute(&n_sm[dev & 31], cudaDevAttrMultiProcessorCount, dev);
   // ADAPTRA_ATTN_FWD_GRID=items: one CTA per item (the non-persistent launch, for comparison)
   static const bool per_item = getenv("ADAPTRA_ATTN_FWD_GRID") && !strcmp(getenv("ADAPTRA_ATTN_FWD_GRID"), "items");
-  const int items = b * H * (T / AT), grid = per_item ? items : std::min(items, n_sm[dev & 31]);
+  const int sm_cap = g_attn_sms.load(std::memory_order_relaxed);
+  const int n_use = (sm_cap > 0 && sm_cap < n_sm[dev & 31]) ? sm_cap : n_sm[dev & 31];
+  const int items = b * H * (T / AT), grid = per_item ? items : std::min(items, n_use);
   // ping-pong over query-block pairs: opt-in ($ADAPTRA_ATTN_FWD=pp; needs an
   // even number of query blocks).  Correct (parity tests), but measured 1.75x
   // slower than the one-tile kernel on C1 shapes (56 vs 32 us per launch,
@@ -1252,7 +1258,7 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
   static const bool pp_on = getenv("ADAPTRA_ATTN_FWD") && !strcmp(getenv("ADAPTRA_ATTN_FWD"), "pp");
   if (pp_on && (T / AT) % 2 == 0 && !per_item) {
     const int pitems = b * H * (T / AT) / 2;
-    attn_fwd_pp_kernel<<<std::min(pitems, n_sm[dev & 31]), kPPThreads, kPPSmem, st>>>(m, a);
+    attn_fwd_pp_kernel<<<std::min(pitems, n_use), kPPThreads, kPPSmem, st>>>(m, a);
   } else if (nq == 4) {
     attn_fwd_kernel<4><<<grid, FwdCfg<4>::kThreads, FwdCfg<4>::kSmem, st>>>(m, a);
   } else {

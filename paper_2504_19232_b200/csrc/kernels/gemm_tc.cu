@@ -551,6 +551,7 @@ static int num_sms() {
 // other stages' kernels fill the rest, and each CTA runs more tiles, so its
 // prologue and its last epilogue are paid over more work.
 std::atomic<int> g_gemm_sms{0};
+extern std::atomic<int> g_attn_sms;  // attn_tc.cu
 static int gemm_sms() {
   const int cap = g_gemm_sms.load(std::memory_order_relaxed);
   const int n = num_sms();
@@ -1042,6 +1043,10 @@ extern "C" int adaptra_set_tuning(int32_t key, int64_t value) {
     case ADAPTRA_TUNE_GEMM_SMS:
       if (value < 0) return adaptra::set_error(ADAPTRA_EINVAL, "set_tuning: SM count must be >= 0");
       adaptra::g_gemm_sms.store((int)value);
+      return ADAPTRA_OK;
+    case ADAPTRA_TUNE_ATTN_SMS:
+      if (value < 0) return adaptra::set_error(ADAPTRA_EINVAL, "set_tuning: SM count must be >= 0");
+      adaptra::g_attn_sms.store((int)value);
       return ADAPTRA_OK;
     default:
       return adaptra::set_error(ADAPTRA_EINVAL, "set_tuning: unknown key");

@@ -78,6 +78,8 @@ class Pipeline:
         elif len(self.local) >= 4:
             n_sm = torch.cuda.get_device_properties(device).multi_processor_count
             L.check(lib.adaptra_set_tuning(L.TUNE_GEMM_SMS, n_sm // 2))
+        if "ADAPTRA_ATTN_SMS" in os.environ:
+            L.check(lib.adaptra_set_tuning(L.TUNE_ATTN_SMS, int(os.environ["ADAPTRA_ATTN_SMS"])))
         block = L.BLOCK_GPT if model.block == "gpt" else L.BLOCK_MLP
         # ---------------- stages
         self.stages = {}
