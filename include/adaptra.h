@@ -354,6 +354,9 @@ int adaptra_stage_W(adaptra_stage_t s, int32_t slot, void* stream);
  * the fp32 gradient once (the executor uses it for two consecutive W ops of
  * a stage's order, $ADAPTRA_W_PAIRS=0 disables); bias / LN sums per slot. */
 int adaptra_stage_W2(adaptra_stage_t s, int32_t slot_a, int32_t slot_b, void* stream);
+/* The same for 1..4 slots (K = n b T, slots[0]'s rows first); the executor
+ * groups up to $ADAPTRA_W_GROUP (default 4) consecutive W ops. */
+int adaptra_stage_Wn(adaptra_stage_t s, const int32_t* slots, int32_t n, void* stream);
 int adaptra_stage_zero_grads(adaptra_stage_t s, void* stream);
 
 /* ================================================================ transport

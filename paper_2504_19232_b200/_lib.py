@@ -145,6 +145,7 @@ _SIGS = {
     "adaptra_stage_B": (_i32, [_vp, _i32, _vp, _vp, _vp]),
     "adaptra_stage_W": (_i32, [_vp, _i32, _vp]),
     "adaptra_stage_W2": (_i32, [_vp, _i32, _i32, _vp]),
+    "adaptra_stage_Wn": (_i32, [_vp, _P(_i32), _i32, _vp]),
     "adaptra_stage_zero_grads": (_i32, [_vp, _vp]),
     "adaptra_inbox_create": (_i32, [_i32, _i32, _i64, C.c_char_p, _P(_vp)]),
     "adaptra_inbox_destroy": (_i32, [_vp]),

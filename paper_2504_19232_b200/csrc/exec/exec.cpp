@@ -431,9 +431,14 @@ struct adaptra_exec {
       host_ns = now_ns() - t_start;
       return ADAPTRA_OK;
     }
-    static const bool w_pairs = [] {
-      const char* v = getenv("ADAPTRA_W_PAIRS");
-      return v ? atoi(v) != 0 : true;
+    // consecutive W ops per launch: $ADAPTRA_W_GROUP (1..4, default 4);
+    // ADAPTRA_W_PAIRS=0 (the round-2 pair switch) means 1
+    static const int w_group = [] {
+      const char* g = getenv("ADAPTRA_W_GROUP");
+      const char* p = getenv("ADAPTRA_W_PAIRS");
+      int v = g ? atoi(g) : 4;
+      if (p && atoi(p) == 0) v = 1;
+      return std::max(1, std::min(4, v));
     }();
     static const int lookahead = [] {
       const char* v = getenv("ADAPTRA_LOOKAHEAD");
@@ -499,21 +504,33 @@ struct adaptra_exec {
         const int slot = P.slot[q];
         if (slot < 0) return set_error(ADAPTRA_EINVAL, "exec: W before F");
         if ((rc = pre_op(q))) return rc;
-        // two consecutive W ops of the order run as one launch over K = 2bT
-        // (adaptra_stage_W2): same work, half the fp32 gradient traffic; the
-        // pair's time is booked on the first op (the second gets zero length)
-        // (not when the offload plan issues copies between the two: the second
-        // W's slot may be refilled right after the first one frees it)
-        if (w_pairs && !merge && q + 1 < ops.size() && ops[q + 1].kind == ADAPTRA_OP_W && P.slot[q + 1] >= 0 &&
-            P.slot[q + 1] != slot && P.after[q].empty()) {
-          if ((rc = pre_op(q + 1))) return rc;
+        // up to w_group consecutive W ops of the order run as one launch over
+        // K = n bT (adaptra_stage_Wn): same work, one fp32 gradient
+        // read-modify-write per group; the group's time is booked on its
+        // first op (the others get zero length).  Not across offload copies:
+        // a later W's slot may be refilled right after an earlier one frees it.
+        int32_t grp[4] = {slot, 0, 0, 0};
+        int n_grp = 1;
+        while (!merge && n_grp < w_group && q + n_grp < ops.size() && ops[q + n_grp].kind == ADAPTRA_OP_W &&
+               P.slot[q + n_grp] >= 0 && P.after[q + n_grp - 1].empty()) {
+          const int32_t sl = P.slot[q + n_grp];
+          bool dup = false;
+          for (int k = 0; k < n_grp; ++k) dup = dup || grp[k] == sl;
+          if (dup) break;
+          grp[n_grp++] = sl;
+        }
+        if (n_grp > 1) {
+          for (int k = 1; k < n_grp; ++k)
+            if ((rc = pre_op(q + k))) return rc;
           ADAPTRA_CUDA_TRY(cudaEventRecord(ev_s[q], cs));
-          if ((rc = adaptra_stage_W2(d.stage, slot, P.slot[q + 1], cs))) return rc;
+          if ((rc = adaptra_stage_Wn(d.stage, grp, n_grp, cs))) return rc;
           ADAPTRA_CUDA_TRY(cudaEventRecord(ev_e[q], cs));
-          ADAPTRA_CUDA_TRY(cudaEventRecord(ev_s[q + 1], cs));
-          ADAPTRA_CUDA_TRY(cudaEventRecord(ev_e[q + 1], cs));
-          if ((rc = post_op(q))) return rc;
-          ++q;
+          for (int k = 1; k < n_grp; ++k) {
+            ADAPTRA_CUDA_TRY(cudaEventRecord(ev_s[q + k], cs));
+            ADAPTRA_CUDA_TRY(cudaEventRecord(ev_e[q + k], cs));
+            if ((rc = post_op(q + k - 1))) return rc;
+          }
+          q += n_grp - 1;
           continue;
         }
         ADAPTRA_CUDA_TRY(cudaEventRecord(ev_s[q], cs));

@@ -696,14 +696,17 @@ static int launch_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
 // the same MMA sequence and reduce-add as in gemm_tc_kernel, so the result is
 // the same bit for bit.
 constexpr int kMaxGroup = 24;
+// Up to kMaxSeg K segments per product (W of up to kMaxSeg slots: segment s
+// covers K blocks [s*k_seg, (s+1)*k_seg) from its own A / B tensor maps).
+constexpr int kMaxSeg = 4;
 struct GroupArgs {
-  CUtensorMap tmA[kMaxGroup], tmB[kMaxGroup], tmC[kMaxGroup];
-  CUtensorMap tmA2[kMaxGroup], tmB2[kMaxGroup];  // second K half (two-slot W), if k_split < k_blocks
+  CUtensorMap tmA[kMaxSeg][kMaxGroup], tmB[kMaxSeg][kMaxGroup], tmC[kMaxGroup];
   int n, total_tiles;
   int tile_start[kMaxGroup + 1];
-  int m_blocks[kMaxGroup], k_blocks[kMaxGroup], k_split[kMaxGroup], N[kMaxGroup];
+  int m_blocks[kMaxGroup], k_blocks[kMaxGroup], k_seg[kMaxGroup], N[kMaxGroup];
   float alpha[kMaxGroup];
 };
+static_assert(sizeof(GroupArgs) <= 32000, "grouped GEMM kernel parameter too large");
 
 __device__ __forceinline__ void group_tile(const GroupArgs& ga, int t, int TM_, int& q, int& mb, int& nb) {
   q = 0;
@@ -767,10 +770,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_grouped_kernel(const __gr
           if (rank == 0) mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes * CG);
           uint8_t* a_dst = sA + stage * Cfg::kABytes;
           uint8_t* b_dst = sB + stage * Cfg::kBBytes;
-          const bool second = kb >= ga.k_split[q];
-          const int k0 = (second ? kb - ga.k_split[q] : kb) * BK;
-          const CUtensorMap* mA = second ? &ga.tmA2[q] : &ga.tmA[q];
-          const CUtensorMap* mB = second ? &ga.tmB2[q] : &ga.tmB[q];
+          const int seg = kb / ga.k_seg[q];
+          const int k0 = (kb - seg * ga.k_seg[q]) * BK;
+          const CUtensorMap* mA = &ga.tmA[seg][q];
+          const CUtensorMap* mB = &ga.tmB[seg][q];
 #pragma unroll
           for (int j = 0; j < BM / 64; ++j)
             tma_load_2d_2sm(a_dst + j * (BK * 128), mA, &full[stage], m0 + 64 * j, k0);
@@ -891,7 +894,8 @@ int gemm_tc(const adaptra_gemm_desc_t& g, cudaStream_t st);
 
 // Grouped dW products (see above).  Falls back to one gemm_tc launch per
 // product when a product does not fit the specialisation.
-int gemm_tc_grouped(const adaptra_gemm_desc_t* gs, int n, cudaStream_t st, const adaptra_gemm_desc_t* gs2) {
+int gemm_tc_grouped(const adaptra_gemm_desc_t* gs, int n, cudaStream_t st, const adaptra_gemm_desc_t* const* more,
+                    int n_more) {
   constexpr int BN = 256;
   using Cfg = TcCfg<2, BN>;
   static const bool off = getenv("ADAPTRA_GEMM_GROUPED") && atoi(getenv("ADAPTRA_GEMM_GROUPED")) == 0;
@@ -901,21 +905,24 @@ int gemm_tc_grouped(const adaptra_gemm_desc_t* gs, int n, cudaStream_t st, const
            !g.causal && g.N >= 2048 && g.M >= 256 && (g.ldc % 4) == 0 && ((uintptr_t)g.C % 16) == 0 &&
            (g.lda * 2) % 16 == 0 && (g.ldb * 2) % 16 == 0 && g.K % BK == 0;
   };
+  if (n_more < 0 || n_more > kMaxSeg - 1) return set_error(ADAPTRA_EINVAL, "gemm_tc_grouped: too many K segments");
   for (int i = 0; ok && i < n; ++i) {
     ok = fits(gs[i]);
-    if (ok && gs2)
-      ok = fits(gs2[i]) && gs2[i].M == gs[i].M && gs2[i].N == gs[i].N && gs2[i].C == gs[i].C &&
-           gs2[i].ldc == gs[i].ldc && gs2[i].alpha == gs[i].alpha;
+    for (int m = 0; ok && m < n_more; ++m) {
+      const auto& h = more[m][i];
+      ok = fits(h) && h.M == gs[i].M && h.N == gs[i].N && h.K == gs[i].K && h.C == gs[i].C && h.ldc == gs[i].ldc &&
+           h.alpha == gs[i].alpha;
+    }
   }
   if (!ok) {
     for (int i = 0; i < n; ++i) {
       int rc = gemm_tc(gs[i], st);
-      if (!rc && gs2) rc = gemm_tc(gs2[i], st);
+      for (int m = 0; !rc && m < n_more; ++m) rc = gemm_tc(more[m][i], st);
       if (rc) return rc;
     }
     return ADAPTRA_OK;
   }
-  static GroupArgs ga;  // host staging of the kernel parameter (15 KB); launches are serialised per process
+  static GroupArgs ga;  // host staging of the kernel parameter (~28 KB); launches are serialised per process
   static std::mutex mu;
   std::lock_guard<std::mutex> lk(mu);
   memset(&ga, 0, sizeof(ga));
@@ -924,21 +931,21 @@ int gemm_tc_grouped(const adaptra_gemm_desc_t* gs, int n, cudaStream_t st, const
   double fl = 0;
   for (int i = 0; i < n; ++i) {
     const auto& g = gs[i];
-    int rc = make_map(&ga.tmA[i], g.A, g.a_rows, g.a_cols, g.lda, 64, BK);
-    if (!rc) rc = make_map(&ga.tmB[i], g.B, g.b_rows, g.b_cols, g.ldb, 64, BK);
+    int rc = make_map(&ga.tmA[0][i], g.A, g.a_rows, g.a_cols, g.lda, 64, BK);
+    if (!rc) rc = make_map(&ga.tmB[0][i], g.B, g.b_rows, g.b_cols, g.ldb, 64, BK);
     if (!rc) rc = make_map(&ga.tmC[i], g.C, g.M, g.N, g.ldc, 32, 32, true, 128);
     if (rc) return rc;
     ga.m_blocks[i] = (g.M + Cfg::TM - 1) / Cfg::TM;
-    ga.k_blocks[i] = ga.k_split[i] = g.K / BK;
+    ga.k_blocks[i] = ga.k_seg[i] = g.K / BK;
     ga.N[i] = g.N;
     ga.alpha[i] = g.alpha;
     ga.tile_start[i] = tiles;
     tiles += ga.m_blocks[i] * ((g.N + BN - 1) / BN);
     fl += 2.0 * g.M * (double)g.N * g.K;
-    if (gs2) {
-      const auto& h = gs2[i];
-      rc = make_map(&ga.tmA2[i], h.A, h.a_rows, h.a_cols, h.lda, 64, BK);
-      if (!rc) rc = make_map(&ga.tmB2[i], h.B, h.b_rows, h.b_cols, h.ldb, 64, BK);
+    for (int m = 0; m < n_more; ++m) {
+      const auto& h = more[m][i];
+      rc = make_map(&ga.tmA[m + 1][i], h.A, h.a_rows, h.a_cols, h.lda, 64, BK);
+      if (!rc) rc = make_map(&ga.tmB[m + 1][i], h.B, h.b_rows, h.b_cols, h.ldb, 64, BK);
       if (rc) return rc;
       ga.k_blocks[i] += h.K / BK;
       fl += 2.0 * h.M * (double)h.N * h.K;

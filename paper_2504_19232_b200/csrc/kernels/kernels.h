@@ -11,9 +11,11 @@ typedef __nv_bfloat16 bf16;
 int gemm_tc(const adaptra_gemm_desc_t& g, cudaStream_t st);
 // Independent products in one persistent launch (W op's dW += X^T dY);
 // falls back to one gemm_tc per product outside its specialisation.
-// gs2 (optional, n entries): second K halves -- product i becomes
-// C_i += A_i^T B_i + A2_i^T B2_i in one K loop (same M, N, C; W of two slots)
-int gemm_tc_grouped(const adaptra_gemm_desc_t* gs, int n, cudaStream_t st, const adaptra_gemm_desc_t* gs2 = nullptr);
+// more[0..n_more) (optional, n entries each, n_more <= 3): further K segments --
+// product i becomes C_i += A_i^T B_i + sum_m A_{m,i}^T B_{m,i} in one K loop
+// (same M, N, K, C; the W of up to four slots)
+int gemm_tc_grouped(const adaptra_gemm_desc_t* gs, int n, cudaStream_t st,
+                    const adaptra_gemm_desc_t* const* more = nullptr, int n_more = 0);
 int gemm_simt(const adaptra_gemm_desc_t& g, cudaStream_t st);
 
 template <typename T>

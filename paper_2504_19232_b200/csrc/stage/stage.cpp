@@ -417,22 +417,23 @@ struct StageOps {
     return ADAPTRA_OK;
   }
 
-  // W of one slot, or of two slots (two consecutive W ops of the stage's
-  // order) as one launch whose products run over K = 2 b T: the fp32
-  // gradient is read-modified-written once per pair instead of once per
-  // microbatch, and every tile's epilogue is amortised over twice the K loop
-  int Wop(int slot, int slot_b = -1) {
-    std::vector<adaptra_gemm_desc_t> dw, dw_b;
-    std::vector<ColsumJob> cs, cs_b;  // per slot: the two slots' sums add into the same gradients
-    collect_w(slot, dw, cs);
-    if (slot_b >= 0) collect_w(slot_b, dw_b, cs_b);
+  // W of 1..4 slots (consecutive W ops of the stage's order) as one launch
+  // whose products run over K = n b T: the fp32 gradient is read-modified-
+  // written once per group instead of once per microbatch, and every tile's
+  // epilogue is amortised over n times the K loop
+  int Wop(const int* slots, int n) {
+    std::vector<adaptra_gemm_desc_t> dw[4];
+    std::vector<ColsumJob> cs[4];  // per slot: the slots' sums add into the same gradients
+    for (int k = 0; k < n; ++k) collect_w(slots[k], dw[k], cs[k]);
     if (dt() == ADAPTRA_BF16) {
-      for (size_t i = 0; i < dw.size(); i += 24)
-        TRY(gemm_tc_grouped(dw.data() + i, (int)std::min<size_t>(24, dw.size() - i), st,
-                            slot_b >= 0 ? dw_b.data() + i : nullptr));
+      for (size_t i = 0; i < dw[0].size(); i += 24) {
+        const adaptra_gemm_desc_t* more[3];
+        for (int k = 1; k < n; ++k) more[k - 1] = dw[k].data() + i;
+        TRY(gemm_tc_grouped(dw[0].data() + i, (int)std::min<size_t>(24, dw[0].size() - i), st, more, n - 1));
+      }
     } else {
-      for (auto& g : dw) TRY(gemm_simt(g, st));
-      for (auto& g : dw_b) TRY(gemm_simt(g, st));
+      for (int k = 0; k < n; ++k)
+        for (auto& g : dw[k]) TRY(gemm_simt(g, st));
     }
     // Column sums (bias and LN parameter gradients): one deterministic launch
     // per sum by default.  All of the op's sums in one grouped launch
@@ -444,15 +445,15 @@ struct StageOps {
     const long R = s->R;
     float* part = (float*)((char*)s->d.work + s->L.w_cs);
     unsigned* cnt = (unsigned*)((char*)s->d.work + s->L.w_cnt);
-    if (cs_grouped) {
-      // one launch per slot: a launch's jobs must not share an output (the
-      // last block of a strip adds into it without atomics)
-      TRY(colsum_grouped<T>(cs.data(), (int)cs.size(), (int)R, st, part, cnt, s->L.cs_floats, s->L.cs_tickets));
-      if (!cs_b.empty())
-        TRY(colsum_grouped<T>(cs_b.data(), (int)cs_b.size(), (int)R, st, part, cnt, s->L.cs_floats, s->L.cs_tickets));
-    } else {
-      cs.insert(cs.end(), cs_b.begin(), cs_b.end());
-      for (const auto& j : cs) {
+    for (int k = 0; k < n; ++k) {
+      if (cs_grouped) {
+        // one launch per slot: a launch's jobs must not share an output (the
+        // last block of a strip adds into it without atomics)
+        TRY(colsum_grouped<T>(cs[k].data(), (int)cs[k].size(), (int)R, st, part, cnt, s->L.cs_floats,
+                              s->L.cs_tickets));
+        continue;
+      }
+      for (const auto& j : cs[k]) {
         if (j.ln)
           TRY(ln_param_grad<T>((const T*)j.y, (const T*)j.x, j.mean, j.rstd, j.out_a, j.out_b, (int)R, j.N, st, part,
                                cnt));
@@ -636,16 +637,25 @@ extern "C" int adaptra_stage_B(adaptra_stage_t s, int32_t slot, const void* dy_i
 
 extern "C" int adaptra_stage_W(adaptra_stage_t s, int32_t slot, void* stream) {
   if (!s || slot < 0 || slot >= s->d.n_slots || !s->dy_in[slot]) return set_error(ADAPTRA_EINVAL, "stage_W: bad args");
-  if (s->d.dtype == ADAPTRA_BF16) return StageOps<bf16>{s, (cudaStream_t)stream}.Wop(slot);
-  return StageOps<float>{s, (cudaStream_t)stream}.Wop(slot);
+  if (s->d.dtype == ADAPTRA_BF16) return StageOps<bf16>{s, (cudaStream_t)stream}.Wop(&slot, 1);
+  return StageOps<float>{s, (cudaStream_t)stream}.Wop(&slot, 1);
+}
+
+extern "C" int adaptra_stage_Wn(adaptra_stage_t s, const int32_t* slots, int32_t n, void* stream) {
+  if (!s || !slots || n < 1 || n > 4) return set_error(ADAPTRA_EINVAL, "stage_Wn: 1..4 slots");
+  for (int k = 0; k < n; ++k) {
+    if (slots[k] < 0 || slots[k] >= s->d.n_slots || !s->dy_in[slots[k]]) return set_error(ADAPTRA_EINVAL, "stage_Wn: bad slot");
+    for (int m = 0; m < k; ++m)
+      if (slots[m] == slots[k]) return set_error(ADAPTRA_EINVAL, "stage_Wn: repeated slot");
+  }
+  const int sl[4] = {slots[0], n > 1 ? slots[1] : 0, n > 2 ? slots[2] : 0, n > 3 ? slots[3] : 0};
+  if (s->d.dtype == ADAPTRA_BF16) return StageOps<bf16>{s, (cudaStream_t)stream}.Wop(sl, n);
+  return StageOps<float>{s, (cudaStream_t)stream}.Wop(sl, n);
 }
 
 extern "C" int adaptra_stage_W2(adaptra_stage_t s, int32_t slot_a, int32_t slot_b, void* stream) {
-  if (!s || slot_a < 0 || slot_a >= s->d.n_slots || slot_b < 0 || slot_b >= s->d.n_slots || slot_a == slot_b ||
-      !s->dy_in[slot_a] || !s->dy_in[slot_b])
-    return set_error(ADAPTRA_EINVAL, "stage_W2: bad args");
-  if (s->d.dtype == ADAPTRA_BF16) return StageOps<bf16>{s, (cudaStream_t)stream}.Wop(slot_a, slot_b);
-  return StageOps<float>{s, (cudaStream_t)stream}.Wop(slot_a, slot_b);
+  const int32_t sl[2] = {slot_a, slot_b};
+  return adaptra_stage_Wn(s, sl, 2, stream);
 }
 
 extern "C" int adaptra_stage_zero_grads(adaptra_stage_t s, void* stream) {

@@ -120,6 +120,11 @@ class Stage:
         """W of two slots as one launch (K = 2bT), adaptra_stage_W2."""
         L.check(L.lib().adaptra_stage_W2(self.handle, slot_a, slot_b, self._s(stream)))
 
+    def Wn(self, slots, stream=None):
+        """W of 1..4 slots as one launch (K = n bT), adaptra_stage_Wn."""
+        arr = (C.c_int32 * len(slots))(*slots)
+        L.check(L.lib().adaptra_stage_Wn(self.handle, arr, len(slots), self._s(stream)))
+
     def zero_grads(self, stream=None):
         L.check(L.lib().adaptra_stage_zero_grads(self.handle, self._s(stream)))
 

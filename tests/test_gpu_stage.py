@@ -35,7 +35,8 @@ CASES = [
 ]
 
 
-# W of slot pairs (adaptra_stage_W2) on the cases with >= 2 microbatches
+# W of slot groups (adaptra_stage_W2 / _Wn: 2 slots, or all of them when
+# there are 3+) on the cases with >= 2 microbatches
 CASES_PAIRS = [c + (p,) for c in CASES for p in (False, True) if not (p and c[-1] < 2)]
 
 
@@ -66,7 +67,9 @@ def test_stage_fbw_vs_oracle(kind, dtype, nl, d, dff, H, b, T, nmb, pairs, last)
         st.B(j, None if last else dyin[j], dxs[j])
         if not pairs:
             st.W(j)
-    if pairs:                   # W of slots (0,1), (2,3), ... as K = 2bT launches
+    if pairs and nmb >= 3:      # all slots in one K = nmb bT launch
+        st.Wn(list(range(nmb)))
+    elif pairs:                 # W of slots (0,1), (2,3), ... as K = 2bT launches
         for j in range(0, nmb - 1, 2):
             st.W2(j, j + 1)
         if nmb % 2:

@@ -17,11 +17,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
                                     {"ADAPTRA_GEMM_GROUPED": "0"},
                                     {"ADAPTRA_EPI_IN_LDG": "1"},
                                     {"ADAPTRA_W_PAIRS": "0"},
+                                    {"ADAPTRA_W_GROUP": "2"},
                                     {"ADAPTRA_ATTN_FWD": "pp"}])
 def test_stage_parity_under_toggle(toggle):
     env = dict(os.environ, **toggle)
     files = ["tests/test_gpu_stage.py", "tests/test_gpu_fullsize.py"]
-    if "ADAPTRA_W_PAIRS" in toggle:        # an executor toggle: the pipelined iterations
+    if "ADAPTRA_W_PAIRS" in toggle or "ADAPTRA_W_GROUP" in toggle:   # executor toggles: pipelined iterations
         files = ["tests/test_gpu_pipeline.py"]
     cmd = [sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider"] + [
         os.path.join(ROOT, f) for f in files]
