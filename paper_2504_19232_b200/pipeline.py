@@ -68,14 +68,14 @@ class Pipeline:
         self.local = [i for i in range(S) if self.stage_rank[i] == rank]
         self.msg_bytes = model.tokens_per_mb * model.d * (2 if model.dtype == L.BF16 else 4)
         lib = L.lib()
-        # With many stages sharing this GPU, persistent GEMMs take half the SMs:
+        # With 8 stages sharing this GPU, persistent GEMMs take half the SMs:
         # the other stages fill the rest and each CTA amortises its prologue and
         # last epilogue over twice the tiles (8 co-located stages: +1 % tokens/s
         # at a 9 % lower SM clock under the power cap,
         # profiles/r02_gemm_sms_step_ab.txt).  $ADAPTRA_GEMM_SMS overrides.
         if "ADAPTRA_GEMM_SMS" in os.environ:
             L.check(lib.adaptra_set_tuning(L.TUNE_GEMM_SMS, int(os.environ["ADAPTRA_GEMM_SMS"])))
-        elif len(self.local) >= 4:
+        elif len(self.local) >= 8:     # measured with 8 co-located stages only
             n_sm = torch.cuda.get_device_properties(device).multi_processor_count
             L.check(lib.adaptra_set_tuning(L.TUNE_GEMM_SMS, n_sm // 2))
         if "ADAPTRA_ATTN_SMS" in os.environ:

@@ -19,6 +19,7 @@ from paper_2504_19232_b200.stage import Stage  # noqa: E402
 d, H, T, nl = int(os.environ.get("D", 2048)), 16, 2048, int(os.environ.get("LAYERS", 3))
 nmb, reps = int(os.environ.get("NMB", 4)), int(os.environ.get("REPS", 8))
 w2 = os.environ.get("OPB_W2") == "1"
+wn = int(os.environ.get("OPB_WN", "0"))   # W of NMB slots in groups of wn (adaptra_stage_Wn)
 st = Stage(L.BLOCK_GPT, L.BF16, nl, d, 4 * d, H, 1, T, False, False, nmb, nmb, "cuda")
 g = torch.Generator(device="cuda").manual_seed(0)
 st.wts.copy_((torch.randn(st.wts.numel(), device="cuda", generator=g) * 0.02).to(torch.bfloat16))
@@ -40,7 +41,10 @@ for rep in range(reps + 2):
         st.B(j, dy[j], dx[j])
     ev["B"][1].record()
     ev["W"][0].record()
-    if w2:
+    if wn > 1:
+        for j in range(0, nmb, wn):
+            st.Wn(list(range(j, min(nmb, j + wn))))
+    elif w2:
         for j in range(0, nmb - 1, 2):
             st.W2(j, j + 1)
         if nmb % 2:
@@ -57,7 +61,7 @@ L.lib().adaptra_prof_enable(0)
 res = {k: round(statistics.median(v), 4) for k, v in times.items()}
 gf = 24 * T * d * d * nl / 1e9
 af = 2 * T * T * d * nl / 1e9
-res.update({"layers": nl, "nmb": nmb, "reps": reps, "w2": w2,
+res.update({"layers": nl, "nmb": nmb, "reps": reps, "w2": w2, "wn": wn,
             "env": {k: v for k, v in os.environ.items() if k.startswith("ADAPTRA_")},
             "F_tflops": round((gf + af) / res["F"] / 1e3, 1), "B_tflops": round((gf + 2 * af) / res["B"] / 1e3, 1),
             "W_tflops": round(gf / res["W"] / 1e3, 1)})
