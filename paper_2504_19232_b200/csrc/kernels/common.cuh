@@ -163,6 +163,17 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* m,
       "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(smem_u32(bar) & 0xFEFFFFFFu)
       : "memory");
 }
+// Same, multicast: the box lands at the same shared-memory offset in every
+// CTA of cta_mask, each destination's bytes counted on its pair leader's
+// barrier (2x2 clusters: an A tile shared by two CTA pairs is fetched once).
+__device__ __forceinline__ void tma_load_2d_2sm_mc(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,
+                                                   uint16_t cta_mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+      "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(smem_u32(bar) & 0xFEFFFFFFu), "h"(cta_mask)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_alloc2(uint32_t* dst_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
                "r"(ncols)
@@ -183,12 +194,13 @@ __device__ __forceinline__ void tc_mma_f16_2sm(uint32_t d_tmem, uint64_t adesc, 
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-// MMA completion -> arrive on the barrier at the same offset in both CTAs of the pair.
-__device__ __forceinline__ void tc_commit_2sm_mc(uint64_t* bar) {
+// MMA completion -> arrive on the barrier at the same offset in both CTAs of the pair
+// (or in every CTA of `mask`).
+__device__ __forceinline__ void tc_commit_2sm_mc(uint64_t* bar, uint16_t mask = 3) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
           smem_u32(bar)),
-      "h"((uint16_t)3)
+      "h"(mask)
       : "memory");
 }
 

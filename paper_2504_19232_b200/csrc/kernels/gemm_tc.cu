@@ -89,6 +89,26 @@ __device__ __forceinline__ void tile_coords(int t, const TileInfo& ti, int& mb, 
   z = r / ti.n_blocks;
 }
 
+// Work units of a launch: one tile each, or (MC: 2x2 clusters of CTA pairs)
+// one pair of N-adjacent tiles per cluster, pair pp of the cluster taking
+// tile nb = 2 nbp + pp (both need the same A rows, fetched once, multicast).
+template <int MC>
+__device__ __forceinline__ int n_units(const TileInfo& ti) {
+  return MC ? ti.m_blocks * (ti.n_blocks / 2) * ti.Z : ti.m_blocks * ti.n_blocks * ti.Z;
+}
+template <int MC>
+__device__ __forceinline__ void unit_coords(int u, const TileInfo& ti, int pp, int& mb, int& nb, int& z) {
+  if (!MC) {
+    tile_coords(u, ti, mb, nb, z);
+    return;
+  }
+  const int half = ti.n_blocks / 2;
+  mb = u % ti.m_blocks;
+  const int r = u / ti.m_blocks;
+  nb = 2 * (r % half) + pp;
+  z = r / half;
+}
+
 // K-block range of a tile (causal variants restrict it), and whether it is skipped.
 template <int TM, int BN>
 __device__ __forceinline__ bool tile_range(const adaptra_gemm_desc_t& g, const TileInfo& ti, int mb, int nb,
@@ -109,13 +129,14 @@ __device__ __forceinline__ bool tile_range(const adaptra_gemm_desc_t& g, const T
 // ---------------------------------------------------------------- epilogue
 // Runs in warps 0..7 of every CTA.  Rows of this CTA: tile row0 + rank*128;
 // warp w drains lane quadrant w % 4, columns [(w / 4) BN/2, (w / 4 + 1) BN/2).
-template <int CG, int BN>
+template <int CG, int BN, int MC>
 __device__ __forceinline__ void epilogue_loop(const adaptra_gemm_desc_t& g, const TileInfo& ti, const EpiTma& et,
                                               const CUtensorMap* tmC, const CUtensorMap* tmX, int vec_ok,
                                               uint8_t* sEpi, uint32_t tmem_base, uint64_t* tfull, uint64_t* tempty,
-                                              uint64_t* inbar, int warp, int lane, int cid, int ncl, int rank) {
+                                              uint64_t* inbar, int warp, int lane, int cid, int ncl, int rank, int pp,
+                                              int leader) {
   constexpr int TM = TcCfg<CG, BN>::TM;
-  const int n_tiles = ti.m_blocks * ti.n_blocks * ti.Z;
+  const int n_tiles = n_units<MC>(ti);
   const int quad = warp & 3;  // TMEM lane quadrant this warp may access
   const int co = (warp >> 2) * (BN / 2);  // first column of this warp's half
   constexpr int NC = BN / 64;            // 32-column chunks per warp
@@ -134,7 +155,7 @@ __device__ __forceinline__ void epilogue_loop(const adaptra_gemm_desc_t& g, cons
                        g.epi == ADAPTRA_EPI_STORE_ROWDOT);
   for (int t = cid; t < n_tiles; t += ncl) {
     int mb, nb, z, kb0, kb1;
-    tile_coords(t, ti, mb, nb, z);
+    unit_coords<MC>(t, ti, pp, mb, nb, z);
     if (!tile_range<TM, BN>(g, ti, mb, nb, kb0, kb1)) continue;
     EpiCtx e = make_epi<bf16>(g, z);
     const int rbase = mb * TM + rank * BM + quad * 32;
@@ -289,7 +310,7 @@ __device__ __forceinline__ void epilogue_loop(const adaptra_gemm_desc_t& g, cons
       if (CG == 1)
         mbar_arrive(&tempty[acc]);
       else
-        mbar_arrive_remote(&tempty[acc], 0);  // the leader reuses the accumulator
+        mbar_arrive_remote(&tempty[acc], leader);  // the pair leader reuses the accumulator
     }
     if (++acc == 2) {
       acc = 0;
@@ -300,7 +321,7 @@ __device__ __forceinline__ void epilogue_loop(const adaptra_gemm_desc_t& g, cons
 }
 
 // ---------------------------------------------------------------- kernel
-template <int CG, int BN, int AMN, int BMN>
+template <int CG, int BN, int AMN, int BMN, int MC>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX,
@@ -319,19 +340,26 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* inbar = tempty + 2;  // [kEpiWarps] epilogue input tiles (in_tma)
   uint32_t* tmem_slot = (uint32_t*)(inbar + kEpiWarps);
 
+  static_assert(!MC || (CG == 2 && AMN == 0), "multicast: CTA pairs, K-major A");
+  constexpr int CL = MC ? 4 : CG;  // CTAs per cluster
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
-  const int cid = CG == 2 ? blockIdx.x / 2 : blockIdx.x;
-  const int ncl = CG == 2 ? gridDim.x / 2 : gridDim.x;
-  const int n_tiles = ti.m_blocks * ti.n_blocks * ti.Z;
+  const int crank = CG == 2 ? (int)cluster_ctarank() : 0;
+  const int rank = crank & 1;          // CTA within its pair
+  const int pp = MC ? crank >> 1 : 0;  // pair within the cluster
+  const int leader = crank & ~1;       // cluster rank of this pair's leader
+  const int cid = blockIdx.x / CL;
+  const int ncl = gridDim.x / CL;
+  const int n_tiles = n_units<MC>(ti);
 
   if (warp == kWarpProducer && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     for (int s = 0; s < Cfg::kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      // MC: a stage is refilled only when the MMAs of both pairs are done
+      // with it (the A halves land in both pairs' shared memory)
+      mbar_init(&empty[s], MC ? 2 : 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
@@ -365,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int t = cid; t < n_tiles; t += ncl) {
         int mb, nb, z, kb0, kb1;
-        tile_coords(t, ti, mb, nb, z);
+        unit_coords<MC>(t, ti, pp, mb, nb, z);
         if (!tile_range<TM, BN>(g, ti, mb, nb, kb0, kb1)) continue;
         const int z1 = z / g.zdiv, z2 = z % g.zdiv;
         const int a_r = (int)(z1 * g.a_row1 + z2 * g.a_row2), a_c = (int)(z1 * g.a_col1 + z2 * g.a_col2);
@@ -393,7 +421,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tma_load_2d(b_dst + j * (BK * 128), &tmB, &full[stage], b_c + n0 + 64 * j, b_r + k0);
             }
           } else {
-            if (AMN == 0) {
+            if (MC) {
+              // this CTA fetches half of its A rows (box BM/2) for itself and
+              // its counterpart in the other pair, which fetches the other half
+              const uint16_t mask = (uint16_t)((1u << crank) | (1u << (crank ^ 2)));
+              tma_load_2d_2sm_mc(a_dst + pp * (BM / 2) * 128, &tmA, &full[stage], a_c + k0, a_r + m0 + pp * (BM / 2),
+                                 mask);
+            } else if (AMN == 0) {
               tma_load_2d_2sm(a_dst, &tmA, &full[stage], a_c + k0, a_r + m0);
             } else {
 #pragma unroll
@@ -420,6 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // Instruction descriptor, kind::f16: D f32 (bit 4), A bf16 (bits 7-9 = 1),
     // B bf16 (bits 10-12 = 1), A/B major (bits 15/16), N>>3 (17-22), M>>4 (24-28).
     if (rank == 0) {
+      const uint16_t empty_mask = MC ? 0xF : 3, pair_mask = (uint16_t)(3u << (2 * pp));
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)AMN << 15) | ((uint32_t)BMN << 16) |
                              ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
       int stage = 0;
@@ -428,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t acc_phase = 0;
       for (int t = cid; t < n_tiles; t += ncl) {
         int mb, nb, z, kb0, kb1;
-        tile_coords(t, ti, mb, nb, z);
+        unit_coords<MC>(t, ti, pp, mb, nb, z);
         if (!tile_range<TM, BN>(g, ti, mb, nb, kb0, kb1)) continue;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -455,7 +490,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (CG == 1)
               tc_commit(&empty[stage]);
             else
-              tc_commit_2sm_mc(&empty[stage]);
+              tc_commit_2sm_mc(&empty[stage], empty_mask);
           }
           __syncwarp();
           if (++stage == Cfg::kStages) {
@@ -467,7 +502,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (CG == 1)
             tc_commit(&tfull[acc]);
           else
-            tc_commit_2sm_mc(&tfull[acc]);
+            tc_commit_2sm_mc(&tfull[acc], pair_mask);
         }
         __syncwarp();
         if (++acc == 2) {
@@ -479,8 +514,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
-    epilogue_loop<CG, BN>(g, ti, et, &tmC, &tmX, vec_ok, sEpi, tmem_base, tfull, tempty, &inbar[warp], warp, lane, cid,
-                          ncl, rank);
+    epilogue_loop<CG, BN, MC>(g, ti, et, &tmC, &tmX, vec_ok, sEpi, tmem_base, tfull, tempty, &inbar[warp], warp, lane,
+                              cid, ncl, rank, pp, leader);
   }
   tc_fence_before();
   if (CG == 2)
@@ -558,13 +593,13 @@ static int gemm_sms() {
   return (cap > 0 && cap < n) ? cap : n;
 }
 
-template <int CG, int BN, int AMN, int BMN>
+template <int CG, int BN, int AMN, int BMN, int MC = 0>
 static int launch_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
   using Cfg = TcCfg<CG, BN>;
   CUtensorMap ma, mbm;
   int rc;
   if (AMN == 0)
-    rc = make_map(&ma, g.A, g.a_rows, g.a_cols, g.lda, BK, BM);
+    rc = make_map(&ma, g.A, g.a_rows, g.a_cols, g.lda, BK, MC ? BM / 2 : BM);
   else
     rc = make_map(&ma, g.A, g.a_rows, g.a_cols, g.lda, 64, BK);
   if (rc) return rc;
@@ -578,8 +613,8 @@ static int launch_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
   ti.n_blocks = (g.N + BN - 1) / BN;
   ti.Z = g.Z;
   ti.k_blocks = (g.K + BK - 1) / BK;
-  const int n_tiles = ti.m_blocks * ti.n_blocks * ti.Z;
-  auto kern = gemm_tc_kernel<CG, BN, AMN, BMN>;
+  const int n_tiles = MC ? ti.m_blocks * (ti.n_blocks / 2) * ti.Z : ti.m_blocks * ti.n_blocks * ti.Z;
+  auto kern = gemm_tc_kernel<CG, BN, AMN, BMN, MC>;
   static std::atomic<unsigned> attr_mask{0};  // per device; stage threads may race here
   int dev = 0;
   cudaGetDevice(&dev);
@@ -592,8 +627,9 @@ static int launch_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
                (!g.aux || (g.ldaux % 8 == 0 && (uintptr_t)g.aux % 16 == 0)) &&
                (!g.R || (g.ldr % 8 == 0 && (uintptr_t)g.R % 16 == 0)) && ((uintptr_t)g.bias % 16 == 0) &&
                (g.c_1 % 8 == 0) && (g.c_2 % 8 == 0) && (g.aux_1 % 8 == 0) && (g.aux_2 % 8 == 0);
-  const int slots = std::max(1, gemm_sms() / CG);
-  int grid = (n_tiles < slots ? n_tiles : slots) * CG;
+  constexpr int CL = MC ? 4 : CG;
+  const int slots = std::max(1, gemm_sms() / CL);
+  int grid = (n_tiles < slots ? n_tiles : slots) * CL;
   if (grid < 1) return ADAPTRA_OK;
   // TMA-store epilogue when C (and the GELU aux output) decompose into 2-D
   // coordinates and live on this device (a peer mailbox is written with
@@ -666,7 +702,7 @@ static int launch_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.x = CL;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
@@ -1018,6 +1054,13 @@ int gemm_tc(const adaptra_gemm_desc_t& g, cudaStream_t st) {
       case 2: return launch_tc<2, 128, 1, 0>(g, st);
       default: return launch_tc<2, 128, 1, 1>(g, st);
     }
+  }
+  // 2x2 clusters with the A tile multicast to both CTA pairs
+  // ($ADAPTRA_GEMM_MC=1): needs an even number of 256-column tiles, K-major A
+  static const bool mc_on = getenv("ADAPTRA_GEMM_MC") && atoi(getenv("ADAPTRA_GEMM_MC")) == 1;
+  if (big && mode == 1 && mc_on && g.a_mn == 0 && ((g.N + 255) / 256) % 2 == 0 && g.epi != ADAPTRA_EPI_STORE_ROWDOT) {
+    if (g.b_mn == 0) return launch_tc<2, 256, 0, 0, 1>(g, st);
+    return launch_tc<2, 256, 0, 1, 1>(g, st);
   }
   if (big && mode == 1) {
     switch (key) {
