@@ -91,11 +91,15 @@ extern "C" int adaptra_nccl_comm_destroy(void* comm) {
 }
 
 namespace adaptra {
-int nccl_p2p(void* comm, const void* send_buf, int64_t send_bytes, int send_peer, void* recv_buf,
-             int64_t recv_bytes, int recv_peer, cudaStream_t st) {
+int nccl_p2p(void* comm, const P2POp* ops, int n, cudaStream_t st) {
+  if (n <= 0) return ADAPTRA_OK;
   NCCL_TRY(nccl().groupStart());
-  if (send_buf) NCCL_TRY(nccl().send(send_buf, (size_t)send_bytes, ncclUint8, send_peer, (ncclComm_t)comm, st));
-  if (recv_buf) NCCL_TRY(nccl().recv(recv_buf, (size_t)recv_bytes, ncclUint8, recv_peer, (ncclComm_t)comm, st));
+  for (int k = 0; k < n; ++k) {
+    if (ops[k].send)
+      NCCL_TRY(nccl().send(ops[k].buf, (size_t)ops[k].bytes, ncclUint8, ops[k].peer, (ncclComm_t)comm, st));
+    else
+      NCCL_TRY(nccl().recv(ops[k].buf, (size_t)ops[k].bytes, ncclUint8, ops[k].peer, (ncclComm_t)comm, st));
+  }
   NCCL_TRY(nccl().groupEnd());
   return ADAPTRA_OK;
 }

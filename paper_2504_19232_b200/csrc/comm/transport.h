@@ -13,9 +13,15 @@ int64_t now_ns();
 cudaStream_t signal_stream(int dev);
 // Hold stream `st` for ns nanoseconds of GPU time (NCCL baseline latency).
 int stream_spin(cudaStream_t st, int64_t ns);
-// Grouped ncclSend/ncclRecv on `st` (either buffer may be NULL); comm/nccl.cpp.
-int nccl_p2p(void* comm, const void* send_buf, int64_t send_bytes, int send_peer, void* recv_buf,
-             int64_t recv_bytes, int recv_peer, cudaStream_t st);
+// One ncclSend / ncclRecv of a group.
+struct P2POp {
+  int send;  // 1 = ncclSend, 0 = ncclRecv
+  void* buf;
+  int64_t bytes;
+  int peer;
+};
+// ops[0..n) inside one ncclGroupStart/End on `st` (n == 0: nothing); comm/nccl.cpp.
+int nccl_p2p(void* comm, const P2POp* ops, int n, cudaStream_t st);
 // Outbox internals for the executor's NCCL baseline arm: injected latency
 // (ns, ADAPTRA_LINK_DOWN when failed) and the sender-local staging slot.
 int64_t outbox_latency(adaptra_outbox_t ob);

@@ -185,6 +185,115 @@ extern "C" int adaptra_offload_plan(const adaptra_op_t* ops, int32_t n, int32_t 
   return ADAPTRA_OK;
 }
 
+// NCCL arm receive-posting plan (R39).  Group p of stage i is issued before
+// op p's kernels (p = n_i: the trailing flush) and holds the send of op p-1's
+// output plus the receives of every op q with post_at[q] == p.  Strict
+// rendezvous: an ncclSend/ncclRecv pair matches only while both of their
+// groups are the current ones of their streams, a group ends when all of its
+// operations matched.  Starting from post_at[q] = q, whenever no pair can
+// match, the receive of a blocked send is hoisted into the receiver's current
+// group -- its mailbox slot is private to its microbatch, so posting early is
+// safe -- until every stream reaches its end.
+extern "C" int adaptra_nccl_post_plan(int32_t S, const adaptra_op_t* ops, const int32_t* n_ops, uint32_t flags,
+                                      int32_t* post_at_out) {
+  if (S < 1 || !ops || !n_ops || !post_at_out) return set_error(ADAPTRA_EINVAL, "nccl_post_plan: bad args");
+  const bool merge = flags & ADAPTRA_MERGE_W;
+  std::vector<int64_t> off(S + 1, 0);
+  for (int i = 0; i < S; ++i) {
+    if (n_ops[i] < 0) return set_error(ADAPTRA_EINVAL, "nccl_post_plan: bad n_ops");
+    off[i + 1] = off[i] + n_ops[i];
+  }
+  // channels: 2i = forward activations i -> i+1, 2i+1 = gradients i+1 -> i
+  struct End {
+    int stage, op, mb;
+  };
+  const int n_ch = 2 * std::max(0, S - 1);
+  std::vector<std::vector<End>> snd(n_ch), rcv(n_ch);
+  std::vector<int> r_ch(off[S], -1), r_k(off[S], -1), s_ch(off[S], -1), s_k(off[S], -1);
+  for (int i = 0; i < S; ++i)
+    for (int q = 0; q < n_ops[i]; ++q) {
+      const adaptra_op_t& o = ops[off[i] + q];
+      const int64_t g = off[i] + q;
+      int rc_ = -1, sc = -1;
+      if (o.kind == ADAPTRA_OP_F) {
+        if (i > 0) rc_ = 2 * (i - 1);
+        if (i < S - 1) sc = 2 * i;
+      } else if (o.kind == ADAPTRA_OP_B) {
+        if (i < S - 1) rc_ = 2 * i + 1;
+        if (i > 0) sc = 2 * (i - 1) + 1;
+      } else if (o.kind != ADAPTRA_OP_W || merge) {
+        return set_error(ADAPTRA_EPLAN, "nccl_post_plan: bad op kind");
+      }
+      if (rc_ >= 0) {
+        r_ch[g] = rc_;
+        r_k[g] = (int)rcv[rc_].size();
+        rcv[rc_].push_back({i, q, o.mb});
+      }
+      if (sc >= 0) {
+        s_ch[g] = sc;
+        s_k[g] = (int)snd[sc].size();
+        snd[sc].push_back({i, q, o.mb});
+      }
+    }
+  for (int ch = 0; ch < n_ch; ++ch) {
+    if (snd[ch].size() != rcv[ch].size()) return set_error(ADAPTRA_EPLAN, "nccl_post_plan: send/recv counts differ");
+    for (size_t k = 0; k < snd[ch].size(); ++k)
+      if (snd[ch][k].mb != rcv[ch][k].mb)
+        return set_error(ADAPTRA_EPLAN, "nccl_post_plan: send and receive orders differ on a link");
+  }
+  for (int i = 0; i < S; ++i)
+    for (int q = 0; q < n_ops[i]; ++q) post_at_out[off[i] + q] = r_ch[off[i] + q] >= 0 ? q : -1;
+  std::vector<int> pos(S, 0), nxt(n_ch, 0);
+  // group p of stage i complete: its send (op p-1's) and its receives matched
+  auto complete = [&](int i, int p) {
+    if (p > 0) {
+      const int64_t g = off[i] + p - 1;
+      if (s_ch[g] >= 0 && nxt[s_ch[g]] <= s_k[g]) return false;
+    }
+    for (int q = p; q < n_ops[i]; ++q) {
+      const int64_t g = off[i] + q;
+      if (post_at_out[g] == p && nxt[r_ch[g]] <= r_k[g]) return false;
+    }
+    return true;
+  };
+  for (;;) {
+    bool progress = false, finished = true;
+    for (int ch = 0; ch < n_ch; ++ch)
+      while (nxt[ch] < (int)snd[ch].size()) {
+        const End& a = snd[ch][nxt[ch]];
+        const End& b = rcv[ch][nxt[ch]];
+        if (pos[a.stage] == a.op + 1 && pos[b.stage] == post_at_out[off[b.stage] + b.op]) {
+          ++nxt[ch];
+          progress = true;
+        } else {
+          break;
+        }
+      }
+    for (int i = 0; i < S; ++i) {
+      while (pos[i] <= n_ops[i] && complete(i, pos[i])) {
+        ++pos[i];
+        progress = true;
+      }
+      if (pos[i] <= n_ops[i]) finished = false;
+    }
+    if (finished) return ADAPTRA_OK;
+    if (progress) continue;
+    // deadlock: hoist the receive of the first posted, blocked send
+    bool hoisted = false;
+    for (int ch = 0; ch < n_ch && !hoisted; ++ch) {
+      if (nxt[ch] >= (int)snd[ch].size()) continue;
+      const End& a = snd[ch][nxt[ch]];
+      const End& b = rcv[ch][nxt[ch]];
+      int32_t& pa = post_at_out[off[b.stage] + b.op];
+      if (pos[a.stage] == a.op + 1 && pa > pos[b.stage]) {
+        pa = pos[b.stage];
+        hoisted = true;
+      }
+    }
+    if (!hoisted) return set_error(ADAPTRA_EPLAN, "nccl_post_plan: receives wait on unposted sends (orders violate dependencies)");
+  }
+}
+
 struct adaptra_exec {
   adaptra_exec_desc_t d{};
   int dev = 0;
@@ -282,52 +391,76 @@ struct adaptra_exec {
   int64_t nccl_down_ns = 0;
 
   // ADAPTRA_EXEC_NCCL: the fixed execution plan of Megatron-style runtimes
-  // (P:1801-1813).  Per op, in order on the compute stream: the send of the
-  // previous op's output grouped with the receive of this op's input
-  // (ncclGroupStart/End, as send_forward_recv_backward pairs them), then the
-  // op's kernels.  An injected latency c holds the stream for c before the
-  // send (the transfer occupies the in-order stream); a failed
-  // link costs its measured delegated-path time instead (baselines have no
-  // delegation, so this is generous to them).
+  // (P:1801-1813).  Per op, in order on the compute stream: one group
+  // (ncclGroupStart/End) with the send of the previous op's output and the
+  // receive of this op's input (as send_forward_recv_backward pairs them),
+  // then the op's kernels.  nccl_post (adaptra_exec_set_nccl_post, one-shot)
+  // moves receives into earlier groups where strict rendezvous would
+  // otherwise deadlock (R39).  An injected latency c holds the stream for c
+  // before the send (the transfer occupies the in-order stream,
+  // P:1815-1828); a failed link costs its measured delegated-path time
+  // instead (baselines have no delegation, so this is generous to them).
+  std::vector<int32_t> nccl_post;
   int run_nccl() {
     const int S = d.n_stages, i = d.stage_index, N = d.n_microbatches;
     const bool merge = flags & ADAPTRA_MERGE_W;
+    const size_t n = ops.size();
     int rc;
-    const void* p_buf = nullptr;
-    int64_t p_bytes = 0, p_lat = 0;
-    int p_peer = -1;
-    auto flush = [&](void* r_buf, int64_t r_bytes, int r_peer) -> int {
-      if (!p_buf && !r_buf) return ADAPTRA_OK;
-      if (p_buf && p_lat > 0) {
-        int r = stream_spin(cs, p_lat);
-        if (r) return r;
+    auto has_recv = [&](size_t q) {
+      return (ops[q].kind == ADAPTRA_OP_F && i > 0) || (ops[q].kind == ADAPTRA_OP_B && i < S - 1);
+    };
+    // at[p]: the ops whose receives group p posts
+    std::vector<std::vector<int>> at(n + 1);
+    const bool planned = nccl_post.size() == n;
+    for (size_t q = 0; q < n; ++q) {
+      const int p = planned ? nccl_post[q] : (has_recv(q) ? (int)q : -1);
+      if (has_recv(q) != (p >= 0) || p > (int)q)
+        return set_error(ADAPTRA_EINVAL, "exec: NCCL receive plan does not fit these orders");
+      if (p >= 0) at[p].push_back((int)q);
+    }
+    nccl_post.clear();
+    adaptra::P2POp pend{1, nullptr, 0, -1};
+    int64_t p_lat = 0;
+    std::vector<adaptra::P2POp> grp;
+    auto issue = [&](size_t p) -> int {
+      grp.clear();
+      if (pend.buf) {
+        if (p_lat > 0) {
+          int r = stream_spin(cs, p_lat);
+          if (r) return r;
+        }
+        grp.push_back(pend);
+        pend.buf = nullptr;
       }
-      int r = nccl_p2p(nccl, p_buf, p_bytes, p_peer, r_buf, r_bytes, r_peer, cs);
-      p_buf = nullptr;
-      return r;
+      for (int q : at[p]) {
+        const int m = ops[q].mb;
+        if (m < 1 || m > N) return set_error(ADAPTRA_EINVAL, "exec: bad microbatch");
+        if (ops[q].kind == ADAPTRA_OP_F)
+          grp.push_back({0, adaptra_inbox_slot(d.in_fwd, m - 1), outbox_bytes(d.out_bwd), nccl_prev});
+        else
+          grp.push_back({0, adaptra_inbox_slot(d.in_bwd, m - 1), outbox_bytes(d.out_fwd), nccl_next});
+      }
+      return nccl_p2p(nccl, grp.data(), (int)grp.size(), cs);
     };
     auto lat_of = [&](adaptra_outbox_t ob) {
       int64_t l = outbox_latency(ob);
       return l == ADAPTRA_LINK_DOWN ? nccl_down_ns : l;
     };
-    for (size_t q = 0; q < ops.size(); ++q) {
+    for (size_t q = 0; q < n; ++q) {
       if (q > 0 && (rc = post_op(q - 1))) return rc;
       const adaptra_op_t& o = ops[q];
       const int mb = o.mb;
       if (mb < 1 || mb > N) return set_error(ADAPTRA_EINVAL, "exec: bad microbatch");
+      const int slot = P.slot[q];
+      if (o.kind != ADAPTRA_OP_F && o.kind != ADAPTRA_OP_B && o.kind != ADAPTRA_OP_W)
+        return set_error(ADAPTRA_EINVAL, "exec: bad op kind");
+      if (o.kind != ADAPTRA_OP_F && slot < 0) return set_error(ADAPTRA_EINVAL, "exec: B/W before F");
+      if ((rc = pre_op(q))) return rc;
+      if (o.kind == ADAPTRA_OP_F && i == 0 && host_inputs)
+        ADAPTRA_CUDA_TRY(cudaStreamWaitEvent(cs, ev_in[mb - 1], 0));
+      if ((rc = issue(q))) return rc;
       if (o.kind == ADAPTRA_OP_F) {
-        const int slot = P.slot[q];
-        if ((rc = pre_op(q))) return rc;
-        const void* x = nullptr;
-        if (i == 0) {
-          x = d.inputs[mb - 1];
-          if (host_inputs) ADAPTRA_CUDA_TRY(cudaStreamWaitEvent(cs, ev_in[mb - 1], 0));
-          if ((rc = flush(nullptr, 0, -1))) return rc;
-        } else {
-          void* p = adaptra_inbox_slot(d.in_fwd, mb - 1);
-          if ((rc = flush(p, outbox_bytes(d.out_bwd), nccl_prev))) return rc;
-          x = p;
-        }
+        const void* x = i == 0 ? d.inputs[mb - 1] : adaptra_inbox_slot(d.in_fwd, mb - 1);
         void* y = (i < S - 1) ? outbox_local_slot(d.out_fwd, mb - 1) : nullptr;
         if (i < S - 1 && !y) return set_error(ADAPTRA_ENOMEM, "exec: no send buffer");
         ADAPTRA_CUDA_TRY(cudaEventRecord(ev_s[q], cs));
@@ -336,22 +469,11 @@ struct adaptra_exec {
           return rc;
         ADAPTRA_CUDA_TRY(cudaEventRecord(ev_e[q], cs));
         if (i < S - 1) {
-          p_buf = y;
-          p_bytes = outbox_bytes(d.out_fwd);
-          p_peer = nccl_next;
+          pend = {1, y, outbox_bytes(d.out_fwd), nccl_next};
           p_lat = lat_of(d.out_fwd);
         }
       } else if (o.kind == ADAPTRA_OP_B) {
-        const int slot = P.slot[q];
-        if (slot < 0) return set_error(ADAPTRA_EINVAL, "exec: B before F");
-        if ((rc = pre_op(q))) return rc;
-        void* dy = nullptr;
-        if (i < S - 1) {
-          dy = adaptra_inbox_slot(d.in_bwd, mb - 1);
-          if ((rc = flush(dy, outbox_bytes(d.out_fwd), nccl_next))) return rc;
-        } else if ((rc = flush(nullptr, 0, -1))) {
-          return rc;
-        }
+        void* dy = i < S - 1 ? adaptra_inbox_slot(d.in_bwd, mb - 1) : nullptr;
         void* dx = (i > 0) ? outbox_local_slot(d.out_bwd, mb - 1) : nullptr;
         if (i > 0 && !dx) return set_error(ADAPTRA_ENOMEM, "exec: no send buffer");
         ADAPTRA_CUDA_TRY(cudaEventRecord(ev_s[q], cs));
@@ -361,25 +483,17 @@ struct adaptra_exec {
         }
         ADAPTRA_CUDA_TRY(cudaEventRecord(ev_e[q], cs));
         if (i > 0) {
-          p_buf = dx;
-          p_bytes = outbox_bytes(d.out_bwd);
-          p_peer = nccl_prev;
+          pend = {1, dx, outbox_bytes(d.out_bwd), nccl_prev};
           p_lat = lat_of(d.out_bwd);
         }
-      } else if (o.kind == ADAPTRA_OP_W) {
-        const int slot = P.slot[q];
-        if (slot < 0) return set_error(ADAPTRA_EINVAL, "exec: W before F");
-        if ((rc = pre_op(q))) return rc;
-        if ((rc = flush(nullptr, 0, -1))) return rc;
+      } else {
         ADAPTRA_CUDA_TRY(cudaEventRecord(ev_s[q], cs));
         if ((rc = adaptra_stage_W(d.stage, slot, cs))) return rc;
         ADAPTRA_CUDA_TRY(cudaEventRecord(ev_e[q], cs));
-      } else {
-        return set_error(ADAPTRA_EINVAL, "exec: bad op kind");
       }
     }
-    if (!ops.empty() && (rc = post_op(ops.size() - 1))) return rc;
-    return flush(nullptr, 0, -1);
+    if (n > 0 && (rc = post_op(n - 1))) return rc;
+    return issue(n);
   }
 
   int run_one() {
@@ -619,6 +733,7 @@ extern "C" int adaptra_run_iteration(adaptra_exec_t e, const adaptra_op_t* ops, 
   std::unique_lock<std::mutex> lk(e->mu);
   if (e->busy) return set_error(ADAPTRA_EINVAL, "run_iteration: previous iteration still running");
   e->ops.assign(ops, ops + n);
+  if (!(flags & ADAPTRA_EXEC_NCCL)) e->nccl_post.clear();
   e->epoch = epoch;
   e->flags = flags;
   e->has_job = true;
@@ -678,6 +793,14 @@ extern "C" int adaptra_exec_set_nccl(adaptra_exec_t e, void* comm, int32_t rank_
   e->nccl_prev = rank_prev;
   e->nccl_next = rank_next;
   e->nccl_down_ns = down_ns;
+  return ADAPTRA_OK;
+}
+
+extern "C" int adaptra_exec_set_nccl_post(adaptra_exec_t e, const int32_t* post_at, int32_t n) {
+  if (!e || n < 0 || (n > 0 && !post_at)) return set_error(ADAPTRA_EINVAL, "exec_set_nccl_post: bad args");
+  std::unique_lock<std::mutex> lk(e->mu);
+  if (e->busy) return set_error(ADAPTRA_EINVAL, "exec_set_nccl_post: iteration running");
+  e->nccl_post.assign(post_at, post_at + n);
   return ADAPTRA_OK;
 }
 

@@ -311,6 +311,13 @@ class Pipeline:
         flags = (L.MERGE_W if merge_w else 0) | (L.EXEC_INORDER if inorder else 0) | (L.EXEC_NCCL if nccl else 0)
         self._base_event.record(self._base_stream)
         keep = []
+        if nccl:
+            # R39: receive-posting plan of the blocking NCCL groups, from all
+            # stages' orders (adaptra_nccl_post_plan)
+            post = cs.nccl_post_plan(orders, merge_w)
+            for i in self.local:
+                sl = (C.c_int32 * max(1, len(post[i])))(*post[i])
+                L.check(lib.adaptra_exec_set_nccl_post(self.execs[i], sl, len(post[i])))
         for i in self.local:
             arr = _op_array(orders[i])
             keep.append(arr)

@@ -122,6 +122,25 @@ def default_delta(tF, tB, tW, ratio=30):
                                          ratio)
 
 
+def nccl_post_plan(orders, merge_w=False):
+    """adaptra_nccl_post_plan (R39): per stage, for each op the index of the
+    group that posts its receive (-1: no receive)."""
+    S = len(orders)
+    flat = [o for ops in orders for o in ops]
+    arr = (L.Op * max(1, len(flat)))()
+    for q, (k, mb) in enumerate(flat):
+        arr[q].kind = KIND_ID[k]
+        arr[q].mb = mb
+    post = (C.c_int32 * max(1, len(flat)))()
+    L.check(L.lib().adaptra_nccl_post_plan(S, arr, _arr(C.c_int32, [len(o) for o in orders]),
+                                          _flags("paper", merge_w), post))
+    out, base = [], 0
+    for ops in orders:
+        out.append(list(post[base:base + len(ops)]))
+        base += len(ops)
+    return out
+
+
 class Planner:
     """adaptra_planner_*: one schedule arm (1F1B / ZB / adaptive, R18/R21/R26)."""
 
