@@ -351,6 +351,8 @@ def main():
                "device_bubble": 1.0 - dbusy / (world * ms_max * 1e6),
                "replans": arm.replans, "x_final": arm.x,
                "gpu_launches": sum(x["launches"] for x in g)}
+        if arm.nccl:
+            out["nccl_probe_msgs"], out["nccl_buffered"] = pipe.nccl_probe, pipe.nccl_buffered
         if losses:
             out["loss_last"] = losses[-1]
         out["h2d_bytes"], out["d2h_bytes"] = sum(x["io"][0] for x in g), sum(x["io"][1] for x in g)

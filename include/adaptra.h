@@ -565,24 +565,31 @@ int adaptra_nccl_unique_id(uint8_t* id_out);
 /* ncclCommInitRank on device dev; *comm_out is an ncclComm_t. */
 int adaptra_nccl_comm_init(const uint8_t* id, int32_t nranks, int32_t rank, int32_t dev, void** comm_out);
 int adaptra_nccl_comm_destroy(void* comm);
+/* One ncclSend (send != 0) or ncclRecv of `bytes` at device `buf` with NCCL
+ * rank `peer` on `stream` (a cudaStream_t; NULL = legacy stream).  Used by
+ * the binding's buffering probe (R39). */
+int adaptra_nccl_p2p(void* comm, int32_t send, void* buf, int64_t bytes, int32_t peer, void* stream);
 /* Communicator and the NCCL ranks of stages i-1 / i+1 (-1 if none). */
 int adaptra_exec_set_nccl(adaptra_exec_t e, void* comm, int32_t rank_prev, int32_t rank_next, int64_t down_ns);
-/* Receive-posting plan (R39).  Blocking send/recv groups can deadlock under
- * strict rendezvous (messages above NCCL's staging buffer): Alg. 2's adapted
- * orders -- and ZB orders on unequal stages -- have stage i blocked sending to
- * i+1 while i+1 is blocked sending to i.  The paper's adaptation assumes no
- * such stalls (Sec. 5 intro).  Stage i's group p is issued before op
- * p's kernels (p = n_ops[i]: the trailing flush) and holds op p-1's send plus
- * the receives of the ops q with post_at[q] == p.  From post_at[q] = q (-1 for
- * ops without a receive) the plan simulates the groups of all S stages under
- * strict rendezvous and, whenever none can proceed, moves a blocked send's
- * receive into the receiver's current group (the receive's mailbox slot is
- * its microbatch's own, so posting early is safe).  ops: the S orders back to
- * back (stage i's n_ops[i] ops after stage i-1's), post_at_out the same
- * layout.  EPLAN if the send and receive orders of a link differ or the
- * orders violate dependencies. */
+/* Receive-posting plan (R39).  Blocking send/recv groups deadlock once a
+ * link's NCCL buffers are full: orders with many warm-up forwards (Alg. 2's
+ * adapted orders, the greedy ZB orders) have stage i blocked sending to i+1
+ * while i+1 is blocked sending to i.  The paper's adaptation assumes no such
+ * stalls (Sec. 5 intro).  Stage i's group p is issued before op p's
+ * kernels (p = n_ops[i]: the trailing flush) and holds op p-1's send plus the
+ * receives of the ops q with post_at[q] == p.  A send completes once its
+ * receive is posted, or on its own while fewer than `buffered` earlier
+ * messages of the link are unreceived (0 = strict rendezvous).  From
+ * post_at[q] = q (-1 for ops without a receive) the plan simulates the groups
+ * of all S stages and, whenever none can proceed, moves the oldest unreceived
+ * message's receive into the receiver's current group (the receive's mailbox
+ * slot is its microbatch's own, so posting early is safe) -- only where the
+ * buffers cannot absorb the orders.  ops: the S orders back to back (stage
+ * i's n_ops[i] ops after stage i-1's), post_at_out the same layout.  EPLAN if
+ * the send and receive orders of a link differ or the orders violate
+ * dependencies. */
 int adaptra_nccl_post_plan(int32_t S, const adaptra_op_t* ops, const int32_t* n_ops, uint32_t flags,
-                           int32_t* post_at_out);
+                           int32_t buffered, int32_t* post_at_out);
 /* Stage's slice of that plan for the NEXT iteration only (n = its op count;
  * without it each receive is posted with its own op).  EINVAL at run time if
  * it does not fit the orders. */

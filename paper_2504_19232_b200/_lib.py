@@ -172,8 +172,9 @@ _SIGS = {
     "adaptra_exec_set_time_base": (_i32, [_vp, _vp]),
     "adaptra_exec_set_host_io": (_i32, [_vp, _P(_vp), _i64, _vp]),
     "adaptra_exec_set_nccl": (_i32, [_vp, _vp, _i32, _i32, _i64]),
-    "adaptra_nccl_post_plan": (_i32, [_i32, _P(Op), _P(_i32), _u32, _P(_i32)]),
+    "adaptra_nccl_post_plan": (_i32, [_i32, _P(Op), _P(_i32), _u32, _i32, _P(_i32)]),
     "adaptra_exec_set_nccl_post": (_i32, [_vp, _P(_i32), _i32]),
+    "adaptra_nccl_p2p": (_i32, [_vp, _i32, _vp, _i64, _i32, _vp]),
     "adaptra_exec_set_offload": (_i32, [_vp, _vp, _i32, _i32]),
     "adaptra_exec_offload_stats": (_i32, [_vp, _P(_i32), _P(_i32), _P(_i64)]),
     "adaptra_offload_plan": (_i32, [_P(Op), _i32, _i32, _i32, _i32, _i32, _u32, _P(_i32), _P(_i32), _i32, _P(_i32)]),

@@ -84,6 +84,12 @@ extern "C" int adaptra_nccl_comm_init(const uint8_t* id, int32_t nranks, int32_t
   return ADAPTRA_OK;
 }
 
+extern "C" int adaptra_nccl_p2p(void* comm, int32_t send, void* buf, int64_t bytes, int32_t peer, void* stream) {
+  if (!comm || !buf || bytes <= 0 || peer < 0) return set_error(ADAPTRA_EINVAL, "nccl_p2p: bad args");
+  adaptra::P2POp op{send ? 1 : 0, buf, bytes, peer};
+  return adaptra::nccl_p2p(comm, &op, 1, (cudaStream_t)stream);
+}
+
 extern "C" int adaptra_nccl_comm_destroy(void* comm) {
   if (!comm) return ADAPTRA_OK;
   NCCL_TRY(nccl().commDestroy((ncclComm_t)comm));

@@ -187,16 +187,19 @@ extern "C" int adaptra_offload_plan(const adaptra_op_t* ops, int32_t n, int32_t 
 
 // NCCL arm receive-posting plan (R39).  Group p of stage i is issued before
 // op p's kernels (p = n_i: the trailing flush) and holds the send of op p-1's
-// output plus the receives of every op q with post_at[q] == p.  Strict
-// rendezvous: an ncclSend/ncclRecv pair matches only while both of their
-// groups are the current ones of their streams, a group ends when all of its
-// operations matched.  Starting from post_at[q] = q, whenever no pair can
-// match, the receive of a blocked send is hoisted into the receiver's current
-// group -- its mailbox slot is private to its microbatch, so posting early is
-// safe -- until every stream reaches its end.
+// output plus the receives of every op q with post_at[q] == p; a group ends
+// when all of its operations have completed.  A send completes once its
+// receive is posted, or on its own while fewer than `buffered` earlier
+// messages of its link sit unreceived in NCCL's buffers (0: strict
+// rendezvous); a receive completes once posted and its send has completed.
+// Starting from post_at[q] = q, whenever no stream can move, the oldest
+// unreceived message of a link whose sender is blocked has its receive
+// hoisted into the receiver's current group -- the receive's mailbox slot is
+// its microbatch's own, so posting early is safe -- until every stream ends.
 extern "C" int adaptra_nccl_post_plan(int32_t S, const adaptra_op_t* ops, const int32_t* n_ops, uint32_t flags,
-                                      int32_t* post_at_out) {
-  if (S < 1 || !ops || !n_ops || !post_at_out) return set_error(ADAPTRA_EINVAL, "nccl_post_plan: bad args");
+                                      int32_t buffered, int32_t* post_at_out) {
+  if (S < 1 || !ops || !n_ops || !post_at_out || buffered < 0)
+    return set_error(ADAPTRA_EINVAL, "nccl_post_plan: bad args");
   const bool merge = flags & ADAPTRA_MERGE_W;
   std::vector<int64_t> off(S + 1, 0);
   for (int i = 0; i < S; ++i) {
@@ -243,32 +246,39 @@ extern "C" int adaptra_nccl_post_plan(int32_t S, const adaptra_op_t* ops, const 
   }
   for (int i = 0; i < S; ++i)
     for (int q = 0; q < n_ops[i]; ++q) post_at_out[off[i] + q] = r_ch[off[i] + q] >= 0 ? q : -1;
-  std::vector<int> pos(S, 0), nxt(n_ch, 0);
-  // group p of stage i complete: its send (op p-1's) and its receives matched
+  // ns / nr: sends / receives of each link completed so far (both complete in
+  // link order: one stream issues them in that order)
+  std::vector<int> pos(S, 0), ns(n_ch, 0), nr(n_ch, 0);
+  auto posted = [&](const End& b) { return pos[b.stage] == post_at_out[off[b.stage] + b.op]; };
   auto complete = [&](int i, int p) {
     if (p > 0) {
       const int64_t g = off[i] + p - 1;
-      if (s_ch[g] >= 0 && nxt[s_ch[g]] <= s_k[g]) return false;
+      if (s_ch[g] >= 0 && ns[s_ch[g]] <= s_k[g]) return false;
     }
     for (int q = p; q < n_ops[i]; ++q) {
       const int64_t g = off[i] + q;
-      if (post_at_out[g] == p && nxt[r_ch[g]] <= r_k[g]) return false;
+      if (post_at_out[g] == p && nr[r_ch[g]] <= r_k[g]) return false;
     }
     return true;
   };
   for (;;) {
     bool progress = false, finished = true;
-    for (int ch = 0; ch < n_ch; ++ch)
-      while (nxt[ch] < (int)snd[ch].size()) {
-        const End& a = snd[ch][nxt[ch]];
-        const End& b = rcv[ch][nxt[ch]];
-        if (pos[a.stage] == a.op + 1 && pos[b.stage] == post_at_out[off[b.stage] + b.op]) {
-          ++nxt[ch];
-          progress = true;
-        } else {
-          break;
+    for (int ch = 0; ch < n_ch; ++ch) {
+      for (bool moved = true; moved;) {
+        moved = false;
+        const int k = ns[ch];
+        if (k < (int)snd[ch].size() && pos[snd[ch][k].stage] == snd[ch][k].op + 1 &&
+            (k - nr[ch] < buffered || (nr[ch] == k && posted(rcv[ch][k])))) {
+          ++ns[ch];
+          moved = true;
         }
+        if (nr[ch] < ns[ch] && posted(rcv[ch][nr[ch]])) {
+          ++nr[ch];
+          moved = true;
+        }
+        progress |= moved;
       }
+    }
     for (int i = 0; i < S; ++i) {
       while (pos[i] <= n_ops[i] && complete(i, pos[i])) {
         ++pos[i];
@@ -278,14 +288,15 @@ extern "C" int adaptra_nccl_post_plan(int32_t S, const adaptra_op_t* ops, const 
     }
     if (finished) return ADAPTRA_OK;
     if (progress) continue;
-    // deadlock: hoist the receive of the first posted, blocked send
+    // no stream can move: hoist the oldest unreceived message of the first
+    // link whose sender is blocked on it
     bool hoisted = false;
     for (int ch = 0; ch < n_ch && !hoisted; ++ch) {
-      if (nxt[ch] >= (int)snd[ch].size()) continue;
-      const End& a = snd[ch][nxt[ch]];
-      const End& b = rcv[ch][nxt[ch]];
+      const int k = ns[ch];
+      if (k >= (int)snd[ch].size() || pos[snd[ch][k].stage] != snd[ch][k].op + 1) continue;
+      const End& b = rcv[ch][nr[ch]];
       int32_t& pa = post_at_out[off[b.stage] + b.op];
-      if (pos[a.stage] == a.op + 1 && pa > pos[b.stage]) {
+      if (pa > pos[b.stage]) {
         pa = pos[b.stage];
         hoisted = true;
       }

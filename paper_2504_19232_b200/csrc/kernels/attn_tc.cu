@@ -133,6 +133,21 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x on the FMA / ALU pipes, to take part of the softmax off the MUFU unit
+// (16 ex2 per clock per SM): x = j + f with j = rint(x) (the 1.5 * 2^23
+// round-to-integer trick; j lands in t's low mantissa bits), 2^f on
+// [-0.5, 0.5] by a degree-3 polynomial (relative error 7.5e-5, below the
+// 2^-9 of the bf16 P it feeds), 2^j added into the exponent field.  x is
+// clamped at -126 (masked keys, -inf, give ~2^-126 instead of 0).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = __fadd_rn(x, 12582912.f);
+  const float f = __fsub_rn(x, __fsub_rn(t, 12582912.f));
+  float p = fmaf(0.0551716648f, f, 0.2426111251f);
+  p = fmaf(p, f, 0.6932609677f);
+  p = fmaf(p, f, 0.9999280572f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 // 1-D bulk copy global -> shared, completion counted on an mbarrier (16 B multiple)
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -151,7 +166,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // 26 % of the SM time with one CTA per item, diag 0x400).
 __device__ __forceinline__ int fwd_item(int r, int c, int G) { return (r & 1) ? (r + 1) * G - 1 - c : r * G + c; }
 
-template <int NQ>
+// POLY of every 4 exponentials per thread go through ex2_poly ($ADAPTRA_ATTN_POLY).
+template <int NQ, int POLY>
 __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const AttnArgs a) {
   constexpr int kFwdRing = FwdCfg<NQ>::kRing, kSoftWarps = FwdCfg<NQ>::kSoftWarps, CW = FwdCfg<NQ>::kCols;
@@ -358,8 +374,10 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads, 1)
         for (int t = 0; t < CW; t += 4) {
           const float e0 = ex2(fmaf(__uint_as_float(rv[t]), c2, -mref));
           const float e1 = ex2(fmaf(__uint_as_float(rv[t + 1]), c2, -mref));
-          const float e2 = ex2(fmaf(__uint_as_float(rv[t + 2]), c2, -mref));
-          const float e3 = ex2(fmaf(__uint_as_float(rv[t + 3]), c2, -mref));
+          const float x2 = fmaf(__uint_as_float(rv[t + 2]), c2, -mref);
+          const float x3 = fmaf(__uint_as_float(rv[t + 3]), c2, -mref);
+          const float e2 = POLY >= 2 ? ex2_poly(x2) : ex2(x2);
+          const float e3 = POLY >= 1 ? ex2_poly(x3) : ex2(x3);
           acc0 += e0 + e1;
           acc1 += e2 + e3;
           pk[t >> 1] = pack_bf16x2(e0, e1);
@@ -1223,12 +1241,19 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
     const char* v = getenv("ADAPTRA_ATTN_FWD_WARPS");
     return (v && atoi(v) == 16) ? 4 : 2;
   }();
+  // exponentials per 4 on the FMA pipe (ex2_poly): $ADAPTRA_ATTN_POLY = 0 | 1 | 2
+  static const int poly = [] {
+    const char* v = getenv("ADAPTRA_ATTN_POLY");
+    return v ? std::max(0, std::min(2, atoi(v))) : 0;
+  }();
   static std::atomic<unsigned> attr{0};  // per device; stage threads may race here
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(attr.load(std::memory_order_acquire) & (1u << dev))) {
-    cudaFuncSetAttribute(attn_fwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
-    cudaFuncSetAttribute(attn_fwd_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<4>::kSmem);
+    cudaFuncSetAttribute(attn_fwd_kernel<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
+    cudaFuncSetAttribute(attn_fwd_kernel<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
+    cudaFuncSetAttribute(attn_fwd_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
+    cudaFuncSetAttribute(attn_fwd_kernel<4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<4>::kSmem);
     cudaFuncSetAttribute(attn_fwd_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPPSmem);
     attr.fetch_or(1u << dev, std::memory_order_release);
   }
@@ -1260,9 +1285,13 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
     const int pitems = b * H * (T / AT) / 2;
     attn_fwd_pp_kernel<<<std::min(pitems, n_use), kPPThreads, kPPSmem, st>>>(m, a);
   } else if (nq == 4) {
-    attn_fwd_kernel<4><<<grid, FwdCfg<4>::kThreads, FwdCfg<4>::kSmem, st>>>(m, a);
+    attn_fwd_kernel<4, 0><<<grid, FwdCfg<4>::kThreads, FwdCfg<4>::kSmem, st>>>(m, a);
+  } else if (poly == 2) {
+    attn_fwd_kernel<2, 2><<<grid, FwdCfg<2>::kThreads, FwdCfg<2>::kSmem, st>>>(m, a);
+  } else if (poly == 1) {
+    attn_fwd_kernel<2, 1><<<grid, FwdCfg<2>::kThreads, FwdCfg<2>::kSmem, st>>>(m, a);
   } else {
-    attn_fwd_kernel<2><<<grid, FwdCfg<2>::kThreads, FwdCfg<2>::kSmem, st>>>(m, a);
+    attn_fwd_kernel<2, 0><<<grid, FwdCfg<2>::kThreads, FwdCfg<2>::kSmem, st>>>(m, a);
   }
   if (fdiag & 0x400) {
     g_nqb = T / AT; g_Z = b * H; g_G = grid;

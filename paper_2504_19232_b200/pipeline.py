@@ -277,6 +277,47 @@ class Pipeline:
         prev = self.stage_rank[i - 1] if i > 0 else -1
         nxt = self.stage_rank[i + 1] if i < self.S - 1 else -1
         L.check(lib.adaptra_exec_set_nccl(self.execs[i], comm, prev, nxt, int(down_ns)))
+        self.nccl_buffered = self._probe_nccl_buffering()
+
+    def _probe_nccl_buffering(self, m=16, wait_s=0.5):
+        """R39: how many messages of msg_bytes a link holds before a posted
+        receive.  Rank 0 issues m sends to rank 1 while rank 1 posts nothing;
+        after wait_s the sends that completed are the buffered count K.  Then
+        rank 1 posts the m receives (nothing is left blocked) and K goes to
+        every rank; the NCCL arm's receive plan assumes K (minus one for
+        margin, at least 0)."""
+        import time
+        import torch.distributed as dist
+        lib = L.lib()
+        k = 0
+        if self.rank in (0, 1):
+            st = torch.cuda.Stream(device=self.device)
+            buf = [torch.empty(self.msg_bytes, dtype=torch.uint8, device=self.device) for _ in range(m)]
+            # one matched message first: NCCL connects peers lazily, on both sides
+            L.check(lib.adaptra_nccl_p2p(self._nccl, int(self.rank == 0), C.c_void_p(buf[0].data_ptr()),
+                                         self.msg_bytes, 1 - self.rank, C.c_void_p(st.cuda_stream)))
+            st.synchronize()
+            if self.rank == 0:
+                evs = []
+                for b in buf:
+                    L.check(lib.adaptra_nccl_p2p(self._nccl, 1, C.c_void_p(b.data_ptr()), self.msg_bytes, 1,
+                                                 C.c_void_p(st.cuda_stream)))
+                    e = torch.cuda.Event()
+                    e.record(st)
+                    evs.append(e)
+                time.sleep(wait_s)
+                k = sum(1 for e in evs if e.query())
+            self._barrier()
+            if self.rank == 1:
+                for b in buf:
+                    L.check(lib.adaptra_nccl_p2p(self._nccl, 0, C.c_void_p(b.data_ptr()), self.msg_bytes, 0,
+                                                 C.c_void_p(st.cuda_stream)))
+            st.synchronize()
+        else:
+            self._barrier()
+        k = int(self._bcast(k))
+        self.nccl_probe = k
+        return max(0, k - 1)
 
     def set_path(self, link: int, host: bool):
         """Delegation policy: move both directions of `link` to
@@ -314,7 +355,7 @@ class Pipeline:
         if nccl:
             # R39: receive-posting plan of the blocking NCCL groups, from all
             # stages' orders (adaptra_nccl_post_plan)
-            post = cs.nccl_post_plan(orders, merge_w)
+            post = cs.nccl_post_plan(orders, merge_w, getattr(self, "nccl_buffered", 0))
             for i in self.local:
                 sl = (C.c_int32 * max(1, len(post[i])))(*post[i])
                 L.check(lib.adaptra_exec_set_nccl_post(self.execs[i], sl, len(post[i])))

@@ -122,9 +122,10 @@ def default_delta(tF, tB, tW, ratio=30):
                                          ratio)
 
 
-def nccl_post_plan(orders, merge_w=False):
+def nccl_post_plan(orders, merge_w=False, buffered=0):
     """adaptra_nccl_post_plan (R39): per stage, for each op the index of the
-    group that posts its receive (-1: no receive)."""
+    group that posts its receive (-1: no receive); `buffered` = messages a
+    link holds without a posted receive."""
     S = len(orders)
     flat = [o for ops in orders for o in ops]
     arr = (L.Op * max(1, len(flat)))()
@@ -133,7 +134,7 @@ def nccl_post_plan(orders, merge_w=False):
         arr[q].mb = mb
     post = (C.c_int32 * max(1, len(flat)))()
     L.check(L.lib().adaptra_nccl_post_plan(S, arr, _arr(C.c_int32, [len(o) for o in orders]),
-                                          _flags("paper", merge_w), post))
+                                          _flags("paper", merge_w), int(buffered), post))
     out, base = [], 0
     for ops in orders:
         out.append(list(post[base:base + len(ops)]))

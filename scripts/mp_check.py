@@ -74,6 +74,8 @@ def main():
                         S2, N, params=params, inputs=xs, targets=tg, rank=rank, world=world, device=local,
                         group=grp, link_mode=mode)
         pipe.enable_nccl(500_000)
+        print(f"rank {rank} NCCL buffering probe: {pipe.nccl_probe} of 16 messages of {pipe.msg_bytes} B "
+              f"completed unreceived", flush=True)
         Lref, gref, _ = nu.full_batch("gpt", params, xs, tg, H)
         t = [1000] * S2
         for arm_name, lat in (("zb-nccl", None), ("1f1b-nccl", None), ("zb-nccl", (0, 2_000_000)),

@@ -141,7 +141,8 @@ def main():
         return {"arm": name, "iterations": len(per_iter),
                 "tokens_per_s": round(len(per_iter) * N * m.tokens_per_mb / (tot / 1e3), 1),
                 "ms_per_iter": round(tot / len(per_iter), 2),
-                "bubble": round(1 - busy_tot / (S * tot * 1e6), 4), "replans": base.replans}, per_iter
+                "bubble": round(1 - busy_tot / (S * tot * 1e6), 4), "replans": base.replans,
+                **({"nccl_probe_msgs": pipe.nccl_probe, "nccl_buffered": pipe.nccl_buffered} if base.nccl else {})}, per_iter
 
     out = {}
     for name in args.arms.split(","):

@@ -3,7 +3,8 @@ process by libadaptra) re-run the stage F / B / W parity suites (small and
 full-size) in a fresh process: one grouped column-sum launch instead of one per
 sum, one dW launch per product instead of the grouped GEMM, epilogue
 inputs by LDG instead of TMA, no W pairs, the ping-pong attention forward (opt-in), 2x2-cluster GEMMs
-with the A tile multicast (opt-in)."""
+with the A tile multicast (opt-in), half of the attention forward's
+exponentials on the FMA pipe (ex2_poly)."""
 import os
 import subprocess
 import sys
@@ -20,7 +21,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
                                     {"ADAPTRA_W_PAIRS": "0"},
                                     {"ADAPTRA_W_GROUP": "2"},
                                     {"ADAPTRA_ATTN_FWD": "pp"},
-                                    {"ADAPTRA_GEMM_MC": "1"}])
+                                    {"ADAPTRA_GEMM_MC": "1"},
+                                    {"ADAPTRA_ATTN_POLY": "2"}])
 def test_stage_parity_under_toggle(toggle):
     env = dict(os.environ, **toggle)
     files = ["tests/test_gpu_stage.py", "tests/test_gpu_fullsize.py"]

@@ -2,26 +2,26 @@
 pattern checked on CPU for every arm's per-stage orders.  Per op, the
 executor groups the previous op's send with this op's receive
 (ncclGroupStart/End); NCCL matches point-to-point operations between two
-ranks in issue order and a group completes only when all of its operations
-have matched.  So (1) on every link and direction the sends must carry the
-microbatches in the order the receiver posts its receives (else data would
-land in the wrong mailbox slot), and (2) the groups must never deadlock.
-A discrete simulation of the blocking groups checks both, in two models:
-"rendezvous" (a send completes only once its receive is posted -- NCCL's
-behaviour for messages above its staging buffer, e.g. the bench's 8 MiB
-activations) and "eager" (a send completes on its own -- small messages
-that fit the buffer).
+ranks in issue order and a group -- one kernel on the stage's stream --
+completes only when all of its operations have.  So (1) on every link and
+direction the sends must carry the microbatches in the order the receiver
+posts its receives (else data would land in the wrong mailbox slot), and (2)
+the groups must never deadlock.  A discrete simulation of the blocking
+groups checks both.  Its model: a send completes once its receive is posted,
+or on its own while fewer than K earlier messages of its link sit unreceived
+in NCCL's buffers (K = 0: strict rendezvous; K = None: unbounded); a receive
+completes once posted and its send has completed.
 
 Finding (DESIGN R39): with each receive posted alongside its own op, 1F1B
-never deadlocks under rendezvous but the adapted orders (and ZB orders on
-unequal stages) can -- Alg. 2 raises stage 0's warm-up forwards past what
-the downstream stage receives before its first backward send, a cycle of
-blocking sends.  The paper's adaptation assumes exactly
-this away: "we assume no HOL blocking stalls -- which is guaranteed by our
-second design" (Sec. 5 intro), the decoupled data plane of
-Sec. 6.  The executor therefore takes a receive-posting plan
-(adaptra_nccl_post_plan) that hoists the receive of a blocked send into the
-receiver's current group; the simulator checks that plan from the outside."""
+never deadlocks even at K = 0, but orders with many warm-up forwards (Alg.
+2's adapted orders, the greedy ZB orders) need K of several messages --
+stage 0 blocked sending F_k while stage 1 is blocked sending B_1.  The
+paper's adaptation assumes this away: "we assume no HOL blocking stalls --
+which is guaranteed by our second design" (Sec. 5 intro).
+The executor therefore takes a receive-posting plan (adaptra_nccl_post_plan,
+given the K the binding measures on the live communicator) that hoists a
+receive into the receiver's current group only where K does not absorb the
+orders; the simulator checks that plan from the outside."""
 import pytest
 from hypothesis import given, settings, strategies as st
 
@@ -65,7 +65,7 @@ def groups(order, i, S, merge, post=None):
     return out
 
 
-def simulate(orders, S, merge, eager=False, post=None):
+def simulate(orders, S, merge, buffered=0, post=None):
     G = [groups(orders[i], i, S, merge, post[i] if post else None) for i in range(S)]
     # (1) per channel (src, dst, dir) the sends carry the microbatches in the
     # order the receiver posts its receives
@@ -81,18 +81,20 @@ def simulate(orders, S, merge, eager=False, post=None):
                 where[(ch, len(recvd.setdefault(ch, [])), "r")] = (i, gi)
                 recvd[ch].append(mb)
     assert sent == recvd, "send and receive orders differ on a link"
-    # (2) rendezvous: an operation completes once its counterpart (the k-th
-    # op on the other side of its channel) is posted, i.e. in the group the
-    # peer's stream has reached; a group -- one kernel -- ends when all of its
-    # operations have completed, and only then does the stream move on
-    mate = {}
-    for (ch, k, role), loc in where.items():
-        mate[(ch, k, role)] = (where[(ch, k, "r" if role == "s" else "s")], (ch, k, "r" if role == "s" else "s"))
+    # (2) the blocking groups, operation by operation
     members = [[[] for _ in G[i]] for i in range(S)]
     for key, (i, gi) in where.items():
         members[i][gi].append(key)
     done = set()
     pos = [0] * S
+
+    def is_posted(key):
+        i, gi = where[key]
+        return pos[i] == gi
+
+    def unreceived(ch, k):   # messages before k on ch sent but not yet received
+        return sum(1 for kk in range(k) if (ch, kk, "s") in done and (ch, kk, "r") not in done)
+
     while any(pos[i] < len(G[i]) for i in range(S)):
         progress = False
         for i in range(S):
@@ -101,22 +103,28 @@ def simulate(orders, S, merge, eager=False, post=None):
             for key in members[i][pos[i]]:
                 if key in done:
                     continue
-                (j, gj), other = mate[key]
-                if eager and key[2] == "s":
-                    done.add(key)           # buffered: completes on its own
-                    progress = True
-                elif eager and key[2] == "r" and (pos[j] > gj or (pos[j] == gj and other in done)):
-                    done.add(key)           # its send was buffered earlier
-                    progress = True
-                elif not eager and pos[j] == gj:
+                ch, k, role = key
+                if role == "s":
+                    r = (ch, k, "r")
+                    if is_posted(r) and all((ch, kk, "r") in done for kk in range(k)):
+                        done.add(key)                      # matched
+                        progress = True
+                    elif buffered is None or unreceived(ch, k) < buffered:
+                        done.add(key)                      # absorbed by the buffers
+                        progress = True
+                elif (ch, k, "s") in done:
                     done.add(key)
-                    done.add(other)
                     progress = True
         for i in range(S):
             if pos[i] < len(G[i]) and all(k in done for k in members[i][pos[i]]):
                 pos[i] += 1
                 progress = True
-        assert progress, f"NCCL rendezvous deadlock at group positions {pos}"
+        assert progress, f"NCCL deadlock at group positions {pos}"
+
+
+def hoisted(orders, post, S):
+    return sum(1 for i in range(S) for q, (k, _) in enumerate(orders[i])
+               if recv_of(k, i, S) and post[i][q] != q)
 
 
 @st.composite
@@ -132,42 +140,63 @@ def cases(draw):
 
 
 @settings(max_examples=200, deadline=None)
-@given(cases())
-def test_nccl_issue_pattern_matches_and_never_deadlocks(case):
-    """Every arm's orders match per channel and never deadlock with eager
-    sends; with the receive-posting plan of adaptra_nccl_post_plan they never
-    deadlock under strict rendezvous either, and the plan only moves
-    receives earlier."""
+@given(cases(), st.sampled_from([0, 1, 2, 4]))
+def test_nccl_issue_pattern_matches_and_never_deadlocks(case, K):
+    """Every arm's orders match per channel and never deadlock with unbounded
+    buffers; with the receive-posting plan for K buffered messages they never
+    deadlock at K either; the plan only moves receives earlier, and not at
+    all where K already absorbs the orders (the baseline is not slowed by
+    needless early receives)."""
     orders, S, merge, arm = case
-    simulate(orders, S, merge, eager=True)
-    post = cs.nccl_post_plan(orders, merge)
+    simulate(orders, S, merge, buffered=None)
+    post = cs.nccl_post_plan(orders, merge, K)
     for i in range(S):
         for q, (k, _) in enumerate(orders[i]):
             if recv_of(k, i, S):
                 assert 0 <= post[i][q] <= q
             else:
                 assert post[i][q] == -1
-    simulate(orders, S, merge, post=post)
+    simulate(orders, S, merge, buffered=K, post=post)
+    try:
+        simulate(orders, S, merge, buffered=K)
+    except AssertionError:
+        assert hoisted(orders, post, S) > 0
+    else:
+        assert hoisted(orders, post, S) == 0
+
+
+def test_1f1b_needs_no_buffering():
+    """1F1B's pairing (send_forward_recv_backward) is deadlock-free even at
+    strict rendezvous, so its plan is the identity."""
+    for S, N in ((2, 4), (4, 16), (8, 32)):
+        t = [1000] * S
+        a = Arm("1f1b", S, N, t, t, t)
+        orders = a.plan([0] * (S - 1))
+        simulate(orders, S, a.merge_w, buffered=0)
+        assert hoisted(orders, cs.nccl_post_plan(orders, a.merge_w, 0), S) == 0
 
 
 def test_adapted_orders_deadlock_without_the_receive_plan():
     """R39: the 2-stage case with a 3 ms link on N=6: Alg. 2 gives stage 0
-    six warm-up forwards; with each receive posted with its own op, stage 1
-    blocks sending B1 (stage 0 receives it only after F6) while stage 0
-    blocks sending F3 (stage 1 posts that receive only after its B2 send)
-    -- a cycle.  The plan posts stage 1's receives of F3..F5 in its group 2
-    (with the B1 send), so stage 0's warm-up forwards flow on."""
+    six warm-up forwards; with each receive posted with its own op and no
+    buffering, stage 1 blocks sending B1 (stage 0 receives it only after F6)
+    while stage 0 blocks sending F3 (stage 1 posts that receive only after
+    its B2 send) -- a cycle.  The K = 0 plan posts stage 1's receives of
+    F3..F5 in its group 2 (with the B1 send), so stage 0's warm-up forwards
+    flow on; with K = 3 buffered messages nothing needs to move."""
     S, N, t = 2, 6, [1000, 1000]
     a = Arm("adaptive", S, N, t, t, t)
     orders = a.plan([3000])
     assert [k for k, _ in orders[0][:7]] == ["F"] * 6 + ["B"]
-    simulate(orders, S, a.merge_w, eager=True)
+    simulate(orders, S, a.merge_w, buffered=None)
     with pytest.raises(AssertionError, match="deadlock"):
-        simulate(orders, S, a.merge_w)
-    post = cs.nccl_post_plan(orders, a.merge_w)
+        simulate(orders, S, a.merge_w, buffered=0)
+    post = cs.nccl_post_plan(orders, a.merge_w, 0)
     f = {mb: q for q, (k, mb) in enumerate(orders[1]) if k == "F"}
     assert [post[1][f[m]] for m in (3, 4, 5)] == [2, 2, 2]
-    simulate(orders, S, a.merge_w, post=post)
+    simulate(orders, S, a.merge_w, buffered=0, post=post)
+    simulate(orders, S, a.merge_w, buffered=3)
+    assert hoisted(orders, cs.nccl_post_plan(orders, a.merge_w, 3), S) == 0
 
 
 def test_post_plan_rejects_mismatched_orders():
@@ -177,18 +206,19 @@ def test_post_plan_rejects_mismatched_orders():
 
 
 def test_simulator_detects_a_deadlock():
-    """A crossed pair of blocking groups (each stage first sends what the
-    other receives last) must be reported."""
+    """A crossed pair of orders is reported, and so is a blocking cycle."""
     S = 2
     crossed = [[("F", 1), ("F", 2), ("B", 2), ("B", 1)], [("F", 2), ("F", 1), ("B", 1), ("B", 2)]]
     with pytest.raises(AssertionError, match="orders differ"):
         simulate(crossed, S, False)
     # stage 0 sends three forwards before its first backward, stage 1 is
-    # 1F1B: the channel orders match, but with receives posted per op stage
-    # 0 blocks sending F3 while stage 1 blocks sending B1
+    # 1F1B: the channel orders match, but with receives posted per op and
+    # no buffering stage 0 blocks sending F3 while stage 1 blocks sending B1;
+    # one buffered message absorbs it
     cyc = [[("F", m) for m in range(1, 5)] + [("B", m) for m in range(1, 5)],
            [(k, m) for m in range(1, 5) for k in "FB"]]
-    simulate(cyc, S, True, eager=True)
+    simulate(cyc, S, True, buffered=None)
     with pytest.raises(AssertionError, match="deadlock"):
-        simulate(cyc, S, True)
-    simulate(cyc, S, True, post=cs.nccl_post_plan(cyc, True))
+        simulate(cyc, S, True, buffered=0)
+    simulate(cyc, S, True, buffered=1)
+    simulate(cyc, S, True, buffered=0, post=cs.nccl_post_plan(cyc, True, 0))
