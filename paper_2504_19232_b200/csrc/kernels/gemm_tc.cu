@@ -11,7 +11,8 @@
 //   warp 8      TMA producer (one elected lane) -> smem ring of kStages stages
 //   warp 9      TMEM allocator + MMA issuer (one elected lane, tcgen05.mma
 //               kind::f16, (128 CG) x BN x 16 per instruction, fp32 accumulate)
-//   warps 10,11 idle (complete the setmaxnreg-decreased warpgroup)
+//   warps 10,11 idle (complete the setmaxnreg-decreased warpgroup); in the
+//               grouped dW kernel warp 10 sums the dY tiles into db
 // Two TMEM accumulators (2 x BN columns) let the epilogue of tile t overlap
 // the main loop of tile t+1.  gemm_tc_grouped_kernel runs all dW products of
 // a W op as one persistent launch over the union of their tiles.  Operands may be K-major or MN-major (SWIZZLE_128B
@@ -43,6 +44,7 @@ constexpr int BK = 64;  // 64 bf16 = 128 B = one SWIZZLE_128B row
 constexpr int kThreads = 384;
 constexpr int kEpiWarps = 8;
 constexpr int kWarpProducer = 8, kWarpMma = 9;
+constexpr int kWarpSum = 10;  // gemm_tc_grouped_kernel: fused bias-gradient column sums
 
 template <int CG, int BN>
 struct TcCfg {
@@ -739,8 +741,10 @@ struct GroupArgs {
   CUtensorMap tmA[kMaxSeg][kMaxGroup], tmB[kMaxSeg][kMaxGroup], tmC[kMaxGroup];
   int n, total_tiles;
   int tile_start[kMaxGroup + 1];
-  int m_blocks[kMaxGroup], k_blocks[kMaxGroup], k_seg[kMaxGroup], N[kMaxGroup];
+  int m_blocks[kMaxGroup], k_blocks[kMaxGroup], k_seg[kMaxGroup], N[kMaxGroup], M[kMaxGroup];
   float alpha[kMaxGroup];
+  float* dbias[kMaxGroup];  // db += column sums of A (= dY) over K, or NULL
+  int sum_mode;             // 1: the column-sum warp runs (some dbias set)
 };
 static_assert(sizeof(GroupArgs) <= 32000, "grouped GEMM kernel parameter too large");
 
@@ -767,7 +771,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_grouped_kernel(const __gr
   uint64_t* empty = full + Cfg::kStages;
   uint64_t* tfull = empty + Cfg::kStages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 2 + kEpiWarps);
+  uint64_t* sfull = tempty + 2 + kEpiWarps;  // [kStages] stage landed, for the column-sum warp
+  uint32_t* tmem_slot = (uint32_t*)(sfull + Cfg::kStages);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -777,7 +782,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_grouped_kernel(const __gr
   if (warp == kWarpProducer && lane == 0) {
     for (int s = 0; s < Cfg::kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      // the pair's MMA commit (+ this CTA's column-sum warp when it runs)
+      mbar_init(&empty[s], ga.sum_mode ? 2 : 1);
+      mbar_init(&sfull[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
@@ -792,7 +799,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_grouped_kernel(const __gr
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp >= kEpiWarps) {
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory");
+  // 56, not 40: the column-sum warp's loop spills at 40 (the epilogue's 208
+  // still fits: 128 x 112 released >= 256 x 40 taken)
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
   if (warp == kWarpProducer) {
     if (lane == 0) {
       int stage = 0;
@@ -849,6 +858,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_grouped_kernel(const __gr
               tc_mma_f16_2sm(d_tmem, umma_desc_sw128(a_addr + k * 2048, BK * 128, 1024),
                              umma_desc_sw128(b_addr + k * 2048, BK * 128, 1024), idesc, (kb > 0 || k > 0) ? 1u : 0u);
             tc_commit_2sm_mc(&empty[stage]);
+            // the stage's MMAs done: each CTA's column-sum warp may read its
+            // half (a hardware arrive on both CTAs -- a thread-issued
+            // cluster-scope arrive per stage throttled the whole pipeline)
+            if (ga.sum_mode) tc_commit_2sm_mc(&sfull[stage]);
           }
           __syncwarp();
           if (++stage == Cfg::kStages) {
@@ -862,6 +875,63 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_grouped_kernel(const __gr
           acc = 0;
           acc_phase ^= 1;
         }
+      }
+    }
+  } else if (warp == kWarpSum) {
+    // Bias gradients fused into the dW products (db += sum_t dY):
+    // A is dY, MN-major, so the tiles of column block 0 see every token of
+    // their 256 output features.  This CTA's half (128 features, two 64-wide
+    // SWIZZLE_128B boxes of BK tokens) is summed from shared memory once the
+    // stage's MMAs are done (sfull, committed by the MMA issuer to both CTAs)
+    // and before the producer may refill it (empty counts this warp): lane l
+    // owns 4 features of box l / 16; per-stage partials, then a running sum
+    // -- a fixed order, so the result is deterministic.  Tiles of other
+    // column blocks only pass the stage on.
+    const int fb = lane >> 4, f4 = (lane & 15) * 4;
+    const uint32_t chunk = (uint32_t)(f4 >> 3), hoff = (uint32_t)(f4 & 7) * 2;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = ga.sum_mode ? cid : ga.total_tiles; t < ga.total_tiles; t += ncl) {
+      int q, mb, nb;
+      group_tile(ga, t, TM, q, mb, nb);
+      const bool on = nb == 0 && ga.dbias[q] != nullptr;
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+      for (int kb = 0; kb < ga.k_blocks[q]; ++kb) {
+        mbar_wait(&sfull[stage], phase);
+        if (on) {
+          const uint32_t box = smem_u32(sA + stage * Cfg::kABytes) + fb * (BK * 128);
+          float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
+#pragma unroll 16
+          for (int k = 0; k < BK; ++k) {
+            uint32_t x, y;
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
+                         : "=r"(x), "=r"(y)
+                         : "r"(box + k * 128 + (((chunk ^ (uint32_t)(k & 7)) << 4) | hoff)));
+            p0 += __uint_as_float(x << 16);
+            p1 += __uint_as_float(x & 0xffff0000u);
+            p2 += __uint_as_float(y << 16);
+            p3 += __uint_as_float(y & 0xffff0000u);
+          }
+          s0 += p0;
+          s1 += p1;
+          s2 += p2;
+          s3 += p3;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == Cfg::kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (on) {
+        const int m = mb * TM + rank * BM + fb * 64 + f4;
+        float* db = ga.dbias[q] + m;
+        const int lim = ga.M[q] - m;
+        if (lim > 0) db[0] += s0;
+        if (lim > 1) db[1] += s1;
+        if (lim > 2) db[2] += s2;
+        if (lim > 3) db[3] += s3;
       }
     }
   }
@@ -931,7 +1001,8 @@ int gemm_tc(const adaptra_gemm_desc_t& g, cudaStream_t st);
 // Grouped dW products (see above).  Falls back to one gemm_tc launch per
 // product when a product does not fit the specialisation.
 int gemm_tc_grouped(const adaptra_gemm_desc_t* gs, int n, cudaStream_t st, const adaptra_gemm_desc_t* const* more,
-                    int n_more) {
+                    int n_more, float* const* dbias, bool* fused) {
+  if (fused) *fused = false;
   constexpr int BN = 256;
   using Cfg = TcCfg<2, BN>;
   static const bool off = getenv("ADAPTRA_GEMM_GROUPED") && atoi(getenv("ADAPTRA_GEMM_GROUPED")) == 0;
@@ -974,7 +1045,10 @@ int gemm_tc_grouped(const adaptra_gemm_desc_t* gs, int n, cudaStream_t st, const
     ga.m_blocks[i] = (g.M + Cfg::TM - 1) / Cfg::TM;
     ga.k_blocks[i] = ga.k_seg[i] = g.K / BK;
     ga.N[i] = g.N;
+    ga.M[i] = g.M;
     ga.alpha[i] = g.alpha;
+    ga.dbias[i] = dbias ? dbias[i] : nullptr;
+    if (dbias && dbias[i]) ga.sum_mode = 1;
     ga.tile_start[i] = tiles;
     tiles += ga.m_blocks[i] * ((g.N + BN - 1) / BN);
     fl += 2.0 * g.M * (double)g.N * g.K;
@@ -1017,6 +1091,7 @@ int gemm_tc_grouped(const adaptra_gemm_desc_t* gs, int n, cudaStream_t st, const
   if (pb) prof_end(pb, st, PROF_GEMM_TC, fl, 0);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(ADAPTRA_ECUDA, std::string("gemm_tc_grouped launch: ") + cudaGetErrorString(e));
+  if (fused) *fused = dbias != nullptr;
   return ADAPTRA_OK;
 }
 

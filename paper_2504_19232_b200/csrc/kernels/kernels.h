@@ -13,9 +13,13 @@ int gemm_tc(const adaptra_gemm_desc_t& g, cudaStream_t st);
 // falls back to one gemm_tc per product outside its specialisation.
 // more[0..n_more) (optional, n entries each, n_more <= 3): further K segments --
 // product i becomes C_i += A_i^T B_i + sum_m A_{m,i}^T B_{m,i} in one K loop
-// (same M, N, K, C; the W of up to four slots)
+// (same M, N, K, C; the W of up to four slots).  dbias[i] (optional, fp32,
+// M_i entries): db_i += the column sums of A_i over all K segments, summed
+// from the staged dY tiles inside the same launch; *fused says whether that
+// happened (false on the per-product fallback: the caller sums instead).
 int gemm_tc_grouped(const adaptra_gemm_desc_t* gs, int n, cudaStream_t st,
-                    const adaptra_gemm_desc_t* const* more = nullptr, int n_more = 0);
+                    const adaptra_gemm_desc_t* const* more = nullptr, int n_more = 0, float* const* dbias = nullptr,
+                    bool* fused = nullptr);
 int gemm_simt(const adaptra_gemm_desc_t& g, cudaStream_t st);
 
 template <typename T>

@@ -423,37 +423,49 @@ struct StageOps {
   // epilogue is amortised over n times the K loop
   int Wop(const int* slots, int n) {
     std::vector<adaptra_gemm_desc_t> dw[4];
+    std::vector<float*> db[4];     // per product: its bias gradient (A = dY of the product)
     std::vector<ColsumJob> cs[4];  // per slot: the slots' sums add into the same gradients
-    for (int k = 0; k < n; ++k) collect_w(slots[k], dw[k], cs[k]);
+    for (int k = 0; k < n; ++k) collect_w(slots[k], dw[k], cs[k], db[k]);
+    // bias gradients summed inside the grouped dW launch from its staged dY
+    // tiles ($ADAPTRA_DB_FUSED=0: separate column-sum launches, as before)
+    static const bool db_fused = !(getenv("ADAPTRA_DB_FUSED") && atoi(getenv("ADAPTRA_DB_FUSED")) == 0);
+    std::vector<float*> fused_db;
     if (dt() == ADAPTRA_BF16) {
       for (size_t i = 0; i < dw[0].size(); i += 24) {
         const adaptra_gemm_desc_t* more[3];
         for (int k = 1; k < n; ++k) more[k - 1] = dw[k].data() + i;
-        TRY(gemm_tc_grouped(dw[0].data() + i, (int)std::min<size_t>(24, dw[0].size() - i), st, more, n - 1));
+        const int m = (int)std::min<size_t>(24, dw[0].size() - i);
+        bool fused = false;
+        TRY(gemm_tc_grouped(dw[0].data() + i, m, st, more, n - 1, db_fused ? db[0].data() + i : nullptr, &fused));
+        if (fused) fused_db.insert(fused_db.end(), db[0].begin() + i, db[0].begin() + i + m);
       }
     } else {
       for (int k = 0; k < n; ++k)
         for (auto& g : dw[k]) TRY(gemm_simt(g, st));
     }
-    // Column sums (bias and LN parameter gradients): one deterministic launch
-    // per sum by default.  All of the op's sums in one grouped launch
-    // (ADAPTRA_COLSUM_GROUPED=1) take 9 % off a 3-layer C1 W op run alone
-    // (profiles/r02_op_bench_pp.jsonl), but with 8 stages sharing the GPU the
-    // step is 3.8 % slower (3 + 3 alternating runs, r02_colsum_step_ab.txt):
-    // its ~1.5k-block grid crowds the other stages' kernels.
+    // Column sums (bias gradients not fused above, LN parameter gradients):
+    // one deterministic launch per sum by default.  All of the op's sums in
+    // one grouped launch (ADAPTRA_COLSUM_GROUPED=1) take 9 % off a 3-layer C1
+    // W op run alone (profiles/r02_op_bench_pp.jsonl), but with 8 stages
+    // sharing the GPU the step is 3.8 % slower (3 + 3 alternating runs,
+    // r02_colsum_step_ab.txt): its ~1.5k-block grid crowds the other stages.
     static const bool cs_grouped = getenv("ADAPTRA_COLSUM_GROUPED") && atoi(getenv("ADAPTRA_COLSUM_GROUPED")) == 1;
     const long R = s->R;
     float* part = (float*)((char*)s->d.work + s->L.w_cs);
     unsigned* cnt = (unsigned*)((char*)s->d.work + s->L.w_cnt);
     for (int k = 0; k < n; ++k) {
+      std::vector<ColsumJob> jobs;
+      for (const auto& j : cs[k])
+        if (j.ln || std::find(fused_db.begin(), fused_db.end(), j.out_a) == fused_db.end()) jobs.push_back(j);
       if (cs_grouped) {
         // one launch per slot: a launch's jobs must not share an output (the
         // last block of a strip adds into it without atomics)
-        TRY(colsum_grouped<T>(cs[k].data(), (int)cs[k].size(), (int)R, st, part, cnt, s->L.cs_floats,
-                              s->L.cs_tickets));
+        if (!jobs.empty())
+          TRY(colsum_grouped<T>(jobs.data(), (int)jobs.size(), (int)R, st, part, cnt, s->L.cs_floats,
+                                s->L.cs_tickets));
         continue;
       }
-      for (const auto& j : cs[k]) {
+      for (const auto& j : jobs) {
         if (j.ln)
           TRY(ln_param_grad<T>((const T*)j.y, (const T*)j.x, j.mean, j.rstd, j.out_a, j.out_b, (int)R, j.N, st, part,
                                cnt));
@@ -464,7 +476,7 @@ struct StageOps {
     return ADAPTRA_OK;
   }
 
-  void collect_w(int slot, std::vector<adaptra_gemm_desc_t>& dw, std::vector<ColsumJob>& cs) {
+  void collect_w(int slot, std::vector<adaptra_gemm_desc_t>& dw, std::vector<ColsumJob>& cs, std::vector<float*>& db) {
     const auto& D = d();
     const long R = s->R, Dm = D.d, Ff = D.d_ff;
     // every dW += X^T dY product of the op is independent: collect them and run
@@ -480,10 +492,12 @@ struct StageOps {
       // dW2 += dy^T g ; db2 += sum dy
       dw.push_back(GB(dt()).shape(Dm, Ff, R).A(dy, Dm, R, Dm, 1).B(g, Ff, R, Ff, 1).C(GW(p.W2), Ff)
               .epi(ADAPTRA_EPI_ACC_F32).g);
+      db.push_back(GV(p.b2));
       cs.push_back(ColsumJob{dy, nullptr, nullptr, nullptr, GV(p.b2), nullptr, (int)(Dm), 0, 0, 0});
       if (D.block == ADAPTRA_BLOCK_MLP) {
         dw.push_back(GB(dt()).shape(Ff, Dm, R).A(da, Ff, R, Ff, 1).B(x, Dm, R, Dm, 1).C(GW(p.W1), Dm)
                 .epi(ADAPTRA_EPI_ACC_F32).g);
+        db.push_back(GV(p.b1));
         cs.push_back(ColsumJob{da, nullptr, nullptr, nullptr, GV(p.b1), nullptr, (int)(Ff), 0, 0, 0});
         continue;
       }
@@ -497,18 +511,28 @@ struct StageOps {
       T* dh1 = buf(slot, l, s->L.dh1);
       dw.push_back(GB(dt()).shape(Ff, Dm, R).A(da, Ff, R, Ff, 1).B(h2, Dm, R, Dm, 1).C(GW(p.W1), Dm)
               .epi(ADAPTRA_EPI_ACC_F32).g);
+      db.push_back(GV(p.b1));
       cs.push_back(ColsumJob{da, nullptr, nullptr, nullptr, GV(p.b1), nullptr, (int)(Ff), 0, 0, 0});
       cs.push_back(ColsumJob{dh2, y1, fbuf(slot, l, s->L.mean2), fbuf(slot, l, s->L.rstd2), GV(p.ln2_g), GV(p.ln2_b), (int)Dm, 1, 0, 0});
       dw.push_back(GB(dt()).shape(Dm, Dm, R).A(dy1, Dm, R, Dm, 1).B(o, Dm, R, Dm, 1).C(GW(p.Wo), Dm)
               .epi(ADAPTRA_EPI_ACC_F32).g);
+      db.push_back(GV(p.bo));
       cs.push_back(ColsumJob{dy1, nullptr, nullptr, nullptr, GV(p.bo), nullptr, (int)(Dm), 0, 0, 0});
       dw.push_back(GB(dt()).shape(3 * Dm, Dm, R).A(dqkv, 3 * Dm, R, 3 * Dm, 1).B(h1, Dm, R, Dm, 1).C(GW(p.Wqkv), Dm)
               .epi(ADAPTRA_EPI_ACC_F32).g);
+      db.push_back(GV(p.bqkv));
       cs.push_back(ColsumJob{dqkv, nullptr, nullptr, nullptr, GV(p.bqkv), nullptr, (int)(3 * Dm), 0, 0, 0});
       cs.push_back(ColsumJob{dh1, x, fbuf(slot, l, s->L.mean1), fbuf(slot, l, s->L.rstd1), GV(p.ln1_g), GV(p.ln1_b), (int)Dm, 1, 0, 0});
     }
-    dw.erase(std::remove_if(dw.begin(), dw.end(), [](const adaptra_gemm_desc_t& g) { return g.M == 0 || g.N == 0; }),
-             dw.end());
+    // drop empty products (and their bias entries, kept parallel)
+    size_t w = 0;
+    for (size_t i = 0; i < dw.size(); ++i)
+      if (dw[i].M != 0 && dw[i].N != 0) {
+        dw[w] = dw[i];
+        db[w++] = db[i];
+      }
+    dw.resize(w);
+    db.resize(w);
   }
 };
 

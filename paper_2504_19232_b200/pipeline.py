@@ -279,20 +279,22 @@ class Pipeline:
         L.check(lib.adaptra_exec_set_nccl(self.execs[i], comm, prev, nxt, int(down_ns)))
         self.nccl_buffered = self._probe_nccl_buffering()
 
-    def _probe_nccl_buffering(self, m=16, wait_s=0.5):
+    def _probe_nccl_buffering(self, wait_s=0.5):
         """R39: how many messages of msg_bytes a link holds before a posted
-        receive.  Rank 0 issues m sends to rank 1 while rank 1 posts nothing;
-        after wait_s the sends that completed are the buffered count K.  Then
-        rank 1 posts the m receives (nothing is left blocked) and K goes to
-        every rank; the NCCL arm's receive plan assumes K (minus one for
-        margin, at least 0)."""
+        receive.  Rank 0 issues m = max(16, N) sends to rank 1 while rank 1
+        posts nothing; after wait_s the sends that completed are the buffered
+        count K.  Then rank 1 posts the m receives (nothing is left blocked)
+        and K goes to every rank.  The NCCL arm's receive plan assumes K - 1
+        (a margin), or no limit when all m completed (a link never carries
+        more than N messages per iteration)."""
         import time
-        import torch.distributed as dist
+        m = max(16, self.N)
         lib = L.lib()
         k = 0
         if self.rank in (0, 1):
-            st = torch.cuda.Stream(device=self.device)
-            buf = [torch.empty(self.msg_bytes, dtype=torch.uint8, device=self.device) for _ in range(m)]
+            dev = torch.device("cuda", self.dev)
+            st = torch.cuda.Stream(device=dev)
+            buf = [torch.empty(self.msg_bytes, dtype=torch.uint8, device=dev) for _ in range(m)]
             # one matched message first: NCCL connects peers lazily, on both sides
             L.check(lib.adaptra_nccl_p2p(self._nccl, int(self.rank == 0), C.c_void_p(buf[0].data_ptr()),
                                          self.msg_bytes, 1 - self.rank, C.c_void_p(st.cuda_stream)))
@@ -317,7 +319,7 @@ class Pipeline:
             self._barrier()
         k = int(self._bcast(k))
         self.nccl_probe = k
-        return max(0, k - 1)
+        return 1 << 20 if k >= m else max(0, k - 1)
 
     def set_path(self, link: int, host: bool):
         """Delegation policy: move both directions of `link` to
