@@ -30,7 +30,6 @@ def main():
     import torch.distributed as dist
 
     from paper_2504_19232_b200 import _lib as L
-    from paper_2504_19232_b200 import sched as cs
     from paper_2504_19232_b200.pipeline import Arm, ModelCfg, Pipeline
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -53,25 +52,18 @@ def main():
     for cfg in args.configs.split(","):
         S, N = (int(v) for v in cfg.split("x"))
         pipe = Pipeline(m, S, N, rank=rank, world=world, device=local, group=group, host_links=True)
+        # a1 as in bench.py: the library profiler (median of the last
+        # iterations, 1 us ticks) on the ZB order at c = 0; Alg. 1's memory
+        # input and the R26 clamp from each stage's F->B stash capacity
         prof = Arm("zb", S, N, [1000] * S, [1000] * S, [1000] * S)
-        for _ in range(2):
-            r = pipe.run(prof.orders)
-        allp = {}
-        for dd in gather({i: [st["op_ns"][k] // max(1, st["op_cnt"][k]) for k in range(3)]
-                          for i, st in r.stats.items()}):
-            allp.update(dd)
-        tF = [max(1, allp[i][0] // 1000) * 1000 for i in range(S)]
-        tB = [max(1, allp[i][1] // 1000) * 1000 for i in range(S)]
-        tW = [max(1, allp[i][2] // 1000) * 1000 for i in range(S)]
+        for _ in range(3):
+            pipe.run(prof.orders)
+        tF, tB, tW = pipe.profile(k=2)
         t_ref = sum(tF) // S
         caps = {}
         for dd in gather({i: st.n_slots_fb for i, st in pipe.stages.items()}):
             caps.update(dd)
         x_cap = [caps[i] for i in range(S)]
-        x_init = cs.plan_init(S, N, x_cap[0], 1)
-        x_init = [min(v, c) for v, c in zip(x_init, x_cap)]
-        for i in range(S - 2, -1, -1):
-            x_init[i] = max(x_init[i], x_init[i + 1])
         for cond in ("nominal", "straggler"):
             c = [0] * (S - 1)
             if cond == "straggler":
@@ -79,7 +71,7 @@ def main():
             for l in range(S - 1):
                 pipe.set_latency(l, c[l])
             for name in ("adaptive", "zb", "1f1b"):
-                arm = Arm(name, S, N, tF, tB, tW, x_init=x_init if name == "adaptive" else None, x_cap=x_cap)
+                arm = Arm(name, S, N, tF, tB, tW, x_cap=x_cap, mem=(x_cap[0], 1))
                 orders = arm.plan(c)
                 pipe.run(orders, merge_w=arm.merge_w)
                 if world > 1:
