@@ -167,7 +167,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ int fwd_item(int r, int c, int G) { return (r & 1) ? (r + 1) * G - 1 - c : r * G + c; }
 
 // POLY of every 4 exponentials per thread go through ex2_poly ($ADAPTRA_ATTN_POLY).
-template <int NQ, int POLY>
+// PT = 1: P stays in TMEM -- written as bf16 pairs over the S columns each
+// thread has read (k-step ks of P V reads columns [16 ks, 16 ks + 8) of the S
+// buffer) and consumed as the A operand of P V from there (the ts form): the
+// M = 128 MMAs no longer read P from shared memory (and nothing writes it
+// there), which with Q, K, V and the TMA fills is the shared-memory traffic
+// that bounds the block.  The S buffer is then released by P V's commit.
+template <int NQ, int POLY, int PT = 0>
 __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const AttnArgs a) {
   constexpr int kFwdRing = FwdCfg<NQ>::kRing, kSoftWarps = FwdCfg<NQ>::kSoftWarps, CW = FwdCfg<NQ>::kCols;
@@ -205,7 +211,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], kSoftWarps);
+      mbar_init(&s_empty[i], PT ? 1 : kSoftWarps);
     }
     mbar_init(p_full, kSoftWarps);
     mbar_init(p_empty, 1);
@@ -292,10 +298,16 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads, 1)
         if (lane == 0) {
           const uint32_t aV = smem_u32(sRing + vslot * TILE);
 #pragma unroll
-          for (int ks = 0; ks < 8; ++ks)
-            tc_mma_f16(tO, desc_kmajor(aP, ks), desc_mnmajor(aV, ks), idesc(0, 1), (j > 0 || ks > 0) ? 1u : 0u);
+          for (int ks = 0; ks < 8; ++ks) {
+            if (PT)
+              tc_mma_f16_ts(tO, tmem + (g & 1) * 128 + 16 * ks, desc_mnmajor(aV, ks), idesc(0, 1),
+                            (j > 0 || ks > 0) ? 1u : 0u);
+            else
+              tc_mma_f16(tO, desc_kmajor(aP, ks), desc_mnmajor(aV, ks), idesc(0, 1), (j > 0 || ks > 0) ? 1u : 0u);
+          }
           tc_commit(&t_empty[vslot]);
           tc_commit(p_empty);
+          if (PT) tc_commit(&s_empty[g & 1]);  // P (in the S buffer) consumed
         }
         __syncwarp();
       }
@@ -344,7 +356,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads, 1)
         tmem_ld_wait_regs_n<CW>(rv);
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&s_empty[sb]);
+        if (!PT && lane == 0) mbar_arrive(&s_empty[sb]);
         if (j == qb) {
           const int lim = qi - (j * AT + qtr * CW);  // last visible column of this group
 #pragma unroll
@@ -398,9 +410,15 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads, 1)
           }
           tmem_st_wait();
         }
+        if (PT) {
 #pragma unroll
-        for (int c = 0; c < CW / 32; ++c) st_tile_row32_packed(smem_u32(sP), r, qtr * CW + 32 * c, pk + 16 * c);
-        fence_proxy_async_smem();
+          for (int c = 0; c < CW / 16; ++c) tmem_st8(tmem + sb * 128 + lanes + 16 * c, pk + 8 * c);
+          tmem_st_wait();
+        } else {
+#pragma unroll
+          for (int c = 0; c < CW / 32; ++c) st_tile_row32_packed(smem_u32(sP), r, qtr * CW + 32 * c, pk + 16 * c);
+          fence_proxy_async_smem();
+        }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full);
@@ -1254,6 +1272,7 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
     cudaFuncSetAttribute(attn_fwd_kernel<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
     cudaFuncSetAttribute(attn_fwd_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
     cudaFuncSetAttribute(attn_fwd_kernel<4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<4>::kSmem);
+    cudaFuncSetAttribute(attn_fwd_kernel<2, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
     cudaFuncSetAttribute(attn_fwd_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPPSmem);
     attr.fetch_or(1u << dev, std::memory_order_release);
   }
@@ -1281,9 +1300,14 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
   // profiles/r02_op_bench_pp.jsonl): two softmax groups sharing the SM's
   // MUFU / issue slots plus the second TMEM pass cost more than the overlap gains
   static const bool pp_on = getenv("ADAPTRA_ATTN_FWD") && !strcmp(getenv("ADAPTRA_ATTN_FWD"), "pp");
+  // P kept in TMEM for P V (default: 30.2 vs 32.7 us per C1 launch,
+  // profiles/r02_attn_ptmem_ab.jsonl); $ADAPTRA_ATTN_FWD=smem: P through shared memory
+  static const bool p_tmem = !(getenv("ADAPTRA_ATTN_FWD") && !strcmp(getenv("ADAPTRA_ATTN_FWD"), "smem"));
   if (pp_on && (T / AT) % 2 == 0 && !per_item) {
     const int pitems = b * H * (T / AT) / 2;
     attn_fwd_pp_kernel<<<std::min(pitems, n_use), kPPThreads, kPPSmem, st>>>(m, a);
+  } else if (p_tmem && nq == 2 && poly == 0) {
+    attn_fwd_kernel<2, 0, 1><<<grid, FwdCfg<2>::kThreads, FwdCfg<2>::kSmem, st>>>(m, a);
   } else if (nq == 4) {
     attn_fwd_kernel<4, 0><<<grid, FwdCfg<4>::kThreads, FwdCfg<4>::kSmem, st>>>(m, a);
   } else if (poly == 2) {
