@@ -24,4 +24,4 @@ def test_two_rank_pipeline_matches_oracle(mode):
     print(r.stdout[-6000:], r.stderr[-4000:])
     assert r.returncode == 0
     assert "FAIL" not in r.stdout
-    assert r.stdout.count("OK") == (16 if n >= 2 else 8)
+    assert r.stdout.count("OK") == (18 if n >= 2 else 8)
