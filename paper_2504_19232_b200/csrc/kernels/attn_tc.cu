@@ -173,8 +173,13 @@ __device__ __forceinline__ int fwd_item(int r, int c, int G) { return (r & 1) ? 
 // M = 128 MMAs no longer read P from shared memory (and nothing writes it
 // there), which with Q, K, V and the TMA fills is the shared-memory traffic
 // that bounds the block.  The S buffer is then released by P V's commit.
-template <int NQ, int POLY, int PT = 0>
-__global__ void __launch_bounds__(FwdCfg<NQ>::kThreads, 1)
+// QT = 1 (with PT): Q moves to TMEM too (columns [384, 512): two 64-column
+// buffers, one per item parity) and S = Q K^T runs in the ts form, so the
+// S MMAs read only K from shared memory.  Four more warps copy each item's Q
+// from its TMA tile into TMEM (thread = query row) once the item two back has
+// issued its last S; the Q tile in shared memory is free right after.
+template <int NQ, int POLY, int PT = 0, int QT = 0>
+__global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const AttnArgs a) {
   constexpr int kFwdRing = FwdCfg<NQ>::kRing, kSoftWarps = FwdCfg<NQ>::kSoftWarps, CW = FwdCfg<NQ>::kCols;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -193,8 +198,10 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads, 1)
   uint64_t* p_full = s_empty + 2;
   uint64_t* p_empty = p_full + 1;
   uint64_t* o_full = p_empty + 1;
-  uint64_t* q_empty = o_full + 1;           // the item's last S MMA read Q
-  uint32_t* tmem_slot = (uint32_t*)(q_empty + 1);
+  uint64_t* q_empty = o_full + 1;           // the item's last S MMA read Q (QT: the copy warps read it)
+  uint64_t* qt_full = q_empty + 1;          // QT: [2] Q of the item in TMEM buffer it & 1
+  uint64_t* qt_empty = qt_full + 2;         // QT: [2] that item's last S MMA done
+  uint32_t* tmem_slot = (uint32_t*)(qt_empty + 2);
 
   const long long cta_t0 = (a.diag & 0x400) ? gtimer() : 0;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -204,7 +211,11 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm_qkv);
     mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
+    mbar_init(q_empty, QT ? 4 : 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&qt_full[i], 4);
+      mbar_init(&qt_empty[i], 1);
+    }
     for (int i = 0; i < kFwdRing; ++i) {
       mbar_init(&t_full[i], 1);
       mbar_init(&t_empty[i], 1);
@@ -256,7 +267,8 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads, 1)
     // block follows this item's last P V.  Global block g: S buffer
     // g & 1, K tile 2g and V tile 2g+1 of the ring.
     const uint32_t aQ = smem_u32(sQ), aP = smem_u32(sP);
-    auto issue_s = [&](int g) {
+    // S of global block g; QT: Q from TMEM buffer qb
+    auto issue_s = [&](int g, int qb) {
       const int st = g & 1;
       const int slot = (2 * g) % kFwdRing;
       mbar_wait(&t_full[slot], ((2 * g) / kFwdRing) & 1);
@@ -265,20 +277,32 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads, 1)
       if (lane == 0) {
         const uint32_t aK = smem_u32(sRing + slot * TILE);
 #pragma unroll
-        for (int ks = 0; ks < 8; ++ks)
-          tc_mma_f16(tmem + st * 128, desc_kmajor(aQ, ks), desc_kmajor(aK, ks), idesc(0, 0), ks > 0 ? 1u : 0u);
+        for (int ks = 0; ks < 8; ++ks) {
+          if (QT)
+            tc_mma_f16_ts(tmem + st * 128, tmem + 384 + qb * 64 + 8 * ks, desc_kmajor(aK, ks), idesc(0, 0),
+                          ks > 0 ? 1u : 0u);
+          else
+            tc_mma_f16(tmem + st * 128, desc_kmajor(aQ, ks), desc_kmajor(aK, ks), idesc(0, 0), ks > 0 ? 1u : 0u);
+        }
         tc_commit(&s_full[st]);
         tc_commit(&t_empty[slot]);
       }
       __syncwarp();
     };
+    // the item's Q is ready for its S MMAs
+    auto wait_q = [&](int it) {
+      if (QT)
+        mbar_wait(&qt_full[it & 1], (it >> 1) & 1);
+      else
+        mbar_wait(q_full, it & 1);
+      tc_fence_after();
+    };
     int g0 = 0;  // global index of the item's first block
     int it = 0;
     int item = fwd_item(0, cta, G);
     if (item < n_items) {
-      mbar_wait(q_full, 0);
-      tc_fence_after();
-      issue_s(0);
+      wait_q(0);
+      issue_s(0, 0);
     }
     while (item < n_items) {
       const int nb = nqb - item / Z;  // key blocks of this item
@@ -286,9 +310,10 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads, 1)
       for (int j = 0; j < nb; ++j) {
         const int g = g0 + j;
         if (j + 1 < nb) {
-          issue_s(g + 1);
+          issue_s(g + 1, it & 1);
         } else {
-          if (lane == 0) tc_commit(q_empty);  // after the item's last S: Q may be replaced
+          // after the item's last S: Q may be replaced
+          if (lane == 0) tc_commit(QT ? &qt_empty[it & 1] : q_empty);
           __syncwarp();
         }
         const int vslot = (2 * g + 1) % kFwdRing;
@@ -317,13 +342,43 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads, 1)
       // finished, so it lands while the softmax warps run the last block and
       // the epilogue (waiting here before the last P V would put it on the path)
       if (next < n_items) {
-        mbar_wait(q_full, (it + 1) & 1);
-        tc_fence_after();
-        issue_s(g0 + nb);
+        wait_q(it + 1);
+        issue_s(g0 + nb, (it + 1) & 1);
       }
       g0 += nb;
       ++it;
       item = next;
+    }
+  } else if (QT && warp >= 2 + kSoftWarps) {
+    // Q copy warps (QT): thread = query row r; its two 128-byte rows of the
+    // K-major SWIZZLE_128B Q tile (logical 16-byte piece p at p ^ (r & 7))
+    // become 64 TMEM columns of bf16 pairs, the A layout of the ts-form S MMA
+    const int quad = warp & 3, r = quad * 32 + lane;
+    const uint32_t lanes = (uint32_t)(quad * 32) << 16;
+    for (int rr = 0, it = 0;; ++rr, ++it) {
+      if (fwd_item(rr, cta, G) >= n_items) break;
+      const int b = it & 1;
+      mbar_wait(q_full, it & 1);
+      mbar_wait(&qt_empty[b], ((it >> 1) & 1) ^ 1);  // item it - 2's last S done with this buffer
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t w[32];
+        const uint32_t row = smem_u32(sQ) + c * CHUNK + r * 128;
+#pragma unroll
+        for (int p = 0; p < 8; ++p)
+          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(w[4 * p]), "=r"(w[4 * p + 1]), "=r"(w[4 * p + 2]), "=r"(w[4 * p + 3])
+                       : "r"(row + ((p ^ (r & 7)) << 4)));
+        tmem_st32(tmem + 384 + b * 64 + lanes + 32 * c, w);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&qt_full[b]);
+        mbar_arrive(q_empty);  // the Q tile in shared memory is free
+      }
     }
   } else {
     // softmax warps: lane quadrant quad (rows), column group qtr (CW keys /
@@ -1273,6 +1328,7 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
     cudaFuncSetAttribute(attn_fwd_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
     cudaFuncSetAttribute(attn_fwd_kernel<4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<4>::kSmem);
     cudaFuncSetAttribute(attn_fwd_kernel<2, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
+    cudaFuncSetAttribute(attn_fwd_kernel<2, 0, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
     cudaFuncSetAttribute(attn_fwd_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPPSmem);
     attr.fetch_or(1u << dev, std::memory_order_release);
   }
@@ -1303,9 +1359,13 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
   // P kept in TMEM for P V (default: 30.2 vs 32.7 us per C1 launch,
   // profiles/r02_attn_ptmem_ab.jsonl); $ADAPTRA_ATTN_FWD=smem: P through shared memory
   static const bool p_tmem = !(getenv("ADAPTRA_ATTN_FWD") && !strcmp(getenv("ADAPTRA_ATTN_FWD"), "smem"));
+  // Q kept in TMEM as well ($ADAPTRA_ATTN_FWD=qtmem)
+  static const bool q_tmem = getenv("ADAPTRA_ATTN_FWD") && !strcmp(getenv("ADAPTRA_ATTN_FWD"), "qtmem");
   if (pp_on && (T / AT) % 2 == 0 && !per_item) {
     const int pitems = b * H * (T / AT) / 2;
     attn_fwd_pp_kernel<<<std::min(pitems, n_use), kPPThreads, kPPSmem, st>>>(m, a);
+  } else if (q_tmem && nq == 2 && poly == 0) {
+    attn_fwd_kernel<2, 0, 1, 1><<<grid, FwdCfg<2>::kThreads + 128, FwdCfg<2>::kSmem, st>>>(m, a);
   } else if (p_tmem && nq == 2 && poly == 0) {
     attn_fwd_kernel<2, 0, 1><<<grid, FwdCfg<2>::kThreads, FwdCfg<2>::kSmem, st>>>(m, a);
   } else if (nq == 4) {
