@@ -451,8 +451,13 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
           pk[(t >> 1) + 1] = pack_bf16x2(e2, e3);
         }
         l = l * alpha + (acc0 + acc1);
-        mbar_wait(p_empty, (g & 1) ^ 1);  // P V of the previous block done: O stable, P buffer free
-        if (j > 0 && __any_sync(0xffffffffu, resc)) {
+        // P V of the previous block done: O stable (and, without PT, the P
+        // buffer free).  With PT, P goes into this block's own S buffer, so
+        // only a rescale of O has to wait -- the softmax of block g then
+        // overlaps P V of block g - 1 instead of following it.
+        const bool resc_o = j > 0 && __any_sync(0xffffffffu, resc);
+        if (!PT || resc_o) mbar_wait(p_empty, (g & 1) ^ 1);
+        if (resc_o) {
           tc_fence_after();
 #pragma unroll
           for (int c = 0; c < CW / 32; ++c) {
@@ -1329,6 +1334,7 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
     cudaFuncSetAttribute(attn_fwd_kernel<4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<4>::kSmem);
     cudaFuncSetAttribute(attn_fwd_kernel<2, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
     cudaFuncSetAttribute(attn_fwd_kernel<2, 0, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
+    cudaFuncSetAttribute(attn_fwd_kernel<4, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<4>::kSmem);
     cudaFuncSetAttribute(attn_fwd_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPPSmem);
     attr.fetch_or(1u << dev, std::memory_order_release);
   }
@@ -1368,6 +1374,8 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
     attn_fwd_kernel<2, 0, 1, 1><<<grid, FwdCfg<2>::kThreads + 128, FwdCfg<2>::kSmem, st>>>(m, a);
   } else if (p_tmem && nq == 2 && poly == 0) {
     attn_fwd_kernel<2, 0, 1><<<grid, FwdCfg<2>::kThreads, FwdCfg<2>::kSmem, st>>>(m, a);
+  } else if (nq == 4 && p_tmem) {
+    attn_fwd_kernel<4, 0, 1><<<grid, FwdCfg<4>::kThreads, FwdCfg<4>::kSmem, st>>>(m, a);
   } else if (nq == 4) {
     attn_fwd_kernel<4, 0><<<grid, FwdCfg<4>::kThreads, FwdCfg<4>::kSmem, st>>>(m, a);
   } else if (poly == 2) {
