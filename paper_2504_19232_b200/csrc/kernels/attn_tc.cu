@@ -182,6 +182,10 @@ template <int NQ, int POLY, int PT = 0, int QT = 0>
 __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const AttnArgs a) {
   constexpr int kFwdRing = FwdCfg<NQ>::kRing, kSoftWarps = FwdCfg<NQ>::kSoftWarps, CW = FwdCfg<NQ>::kCols;
+  // S buffers in TMEM: with P in TMEM a buffer is busy until its P V is done,
+  // so S(g + 1) with two buffers would wait for P V(g - 1) to drain the tensor
+  // pipe; three keep it fed (O then sits at column 384; QT needs 384+ for Q)
+  constexpr int NS = (PT && !QT) ? 3 : 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;  // no static shared memory: the window starts 1024-aligned (checked)
   if (threadIdx.x == 0 && (smem_u32(smem) & 1023)) __trap();
@@ -193,9 +197,9 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
   uint64_t* q_full = bar + 0;
   uint64_t* t_full = bar + 1;               // [kFwdRing] tile landed
   uint64_t* t_empty = t_full + kFwdRing;    // [kFwdRing] tile consumed by its MMA
-  uint64_t* s_full = t_empty + kFwdRing;    // [2]
-  uint64_t* s_empty = s_full + 2;           // [2]
-  uint64_t* p_full = s_empty + 2;
+  uint64_t* s_full = t_empty + kFwdRing;    // [NS]
+  uint64_t* s_empty = s_full + NS;          // [NS]
+  uint64_t* p_full = s_empty + NS;
   uint64_t* p_empty = p_full + 1;
   uint64_t* o_full = p_empty + 1;
   uint64_t* q_empty = o_full + 1;           // the item's last S MMA read Q (QT: the copy warps read it)
@@ -220,7 +224,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
       mbar_init(&t_full[i], 1);
       mbar_init(&t_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NS; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], PT ? 1 : kSoftWarps);
     }
@@ -234,7 +238,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tO = tmem + 256;
+  const uint32_t tO = tmem + NS * 128;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -265,14 +269,14 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
     // S of block j+1 is issued before waiting for P of block j, so the softmax
     // warps overlap the tensor pipe; across items, S of the next item's first
     // block follows this item's last P V.  Global block g: S buffer
-    // g & 1, K tile 2g and V tile 2g+1 of the ring.
+    // g % NS, K tile 2g and V tile 2g+1 of the ring.
     const uint32_t aQ = smem_u32(sQ), aP = smem_u32(sP);
     // S of global block g; QT: Q from TMEM buffer qb
     auto issue_s = [&](int g, int qb) {
-      const int st = g & 1;
+      const int st = g % NS;
       const int slot = (2 * g) % kFwdRing;
       mbar_wait(&t_full[slot], ((2 * g) / kFwdRing) & 1);
-      mbar_wait(&s_empty[st], ((g >> 1) & 1) ^ 1);
+      mbar_wait(&s_empty[st], ((g / NS) & 1) ^ 1);
       tc_fence_after();
       if (lane == 0) {
         const uint32_t aK = smem_u32(sRing + slot * TILE);
@@ -304,6 +308,12 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
       wait_q(0);
       issue_s(0, 0);
     }
+    // diag 0x200: clock64 stamps of CTA 0's first 64 blocks ([g][16]): 0 S(g+1)
+    // issued, 1 P(g) seen, 2 P V(g) issued; softmax warp 2: 3 S(g) seen, 4 S
+    // loaded, 5 row max exchanged, 6 exponentials done, 7 O ready, 8 P written
+    const bool trm = (a.diag & 0x200) && blockIdx.x == 0 && lane == 0;
+#define FTRACE(on, g, ev) \
+  if ((on) && (g) < 64) a.trace[(g) * 16 + (ev)] = clock64();
     while (item < n_items) {
       const int nb = nqb - item / Z;  // key blocks of this item
       const int next = fwd_item(it + 1, cta, G);
@@ -311,6 +321,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
         const int g = g0 + j;
         if (j + 1 < nb) {
           issue_s(g + 1, it & 1);
+          FTRACE(trm, g, 0)
         } else {
           // after the item's last S: Q may be replaced
           if (lane == 0) tc_commit(QT ? &qt_empty[it & 1] : q_empty);
@@ -318,6 +329,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
         }
         const int vslot = (2 * g + 1) % kFwdRing;
         mbar_wait(p_full, g & 1);
+        FTRACE(trm, g, 1)
         mbar_wait(&t_full[vslot], ((2 * g + 1) / kFwdRing) & 1);
         tc_fence_after();
         if (lane == 0) {
@@ -325,15 +337,16 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks) {
             if (PT)
-              tc_mma_f16_ts(tO, tmem + (g & 1) * 128 + 16 * ks, desc_mnmajor(aV, ks), idesc(0, 1),
+              tc_mma_f16_ts(tO, tmem + (g % NS) * 128 + 16 * ks, desc_mnmajor(aV, ks), idesc(0, 1),
                             (j > 0 || ks > 0) ? 1u : 0u);
             else
               tc_mma_f16(tO, desc_kmajor(aP, ks), desc_mnmajor(aV, ks), idesc(0, 1), (j > 0 || ks > 0) ? 1u : 0u);
           }
           tc_commit(&t_empty[vslot]);
           tc_commit(p_empty);
-          if (PT) tc_commit(&s_empty[g & 1]);  // P (in the S buffer) consumed
+          if (PT) tc_commit(&s_empty[g % NS]);  // P (in the S buffer) consumed
         }
+        FTRACE(trm, g, 2)
         __syncwarp();
       }
       if (lane == 0) tc_commit(o_full);
@@ -402,16 +415,20 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
       const int qi = qb * AT + r;             // query position in the sequence
       float mref = -INFINITY, l = 0.f;
       for (int j = 0; j <= qb; ++j, ++g) {
-        const int sb = g & 1;
-        mbar_wait(&s_full[sb], (g >> 1) & 1);
+        const int sb = g & 1;   // row-max exchange parity
+        const int tb = g % NS;  // TMEM S buffer
+        const bool trs = (a.diag & 0x200) && blockIdx.x == 0 && warp == 2 && lane == 0;
+        mbar_wait(&s_full[tb], (g / NS) & 1);
+        FTRACE(trs, g, 3)
         tc_fence_after();
         uint32_t rv[CW];
 #pragma unroll
-        for (int c = 0; c < CW / 32; ++c) tmem_ld32(tmem + sb * 128 + lanes + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(&rv[32 * c]));
+        for (int c = 0; c < CW / 32; ++c) tmem_ld32(tmem + tb * 128 + lanes + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(&rv[32 * c]));
         tmem_ld_wait_regs_n<CW>(rv);
+        FTRACE(trs, g, 4)
         tc_fence_before();
         __syncwarp();
-        if (!PT && lane == 0) mbar_arrive(&s_empty[sb]);
+        if (!PT && lane == 0) mbar_arrive(&s_empty[tb]);
         if (j == qb) {
           const int lim = qi - (j * AT + qtr * CW);  // last visible column of this group
 #pragma unroll
@@ -429,6 +446,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
 #pragma unroll
         for (int k = 1; k < NQ; ++k) mall = fmaxf(mall, mx[k * AT + r]);
         const float mb = mall * c2;
+        FTRACE(trs, g, 5)
         const bool resc = mb > mref + 8.f;
         float alpha = 1.f;
         if (resc) {
@@ -451,6 +469,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
           pk[(t >> 1) + 1] = pack_bf16x2(e2, e3);
         }
         l = l * alpha + (acc0 + acc1);
+        FTRACE(trs, g, 6)
         // P V of the previous block done: O stable (and, without PT, the P
         // buffer free).  With PT, P goes into this block's own S buffer, so
         // only a rescale of O has to wait -- the softmax of block g then
@@ -470,9 +489,10 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
           }
           tmem_st_wait();
         }
+        FTRACE(trs, g, 7)
         if (PT) {
 #pragma unroll
-          for (int c = 0; c < CW / 16; ++c) tmem_st8(tmem + sb * 128 + lanes + 16 * c, pk + 8 * c);
+          for (int c = 0; c < CW / 16; ++c) tmem_st8(tmem + tb * 128 + lanes + 16 * c, pk + 8 * c);
           tmem_st_wait();
         } else {
 #pragma unroll
@@ -481,6 +501,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
         }
         tc_fence_before();
         __syncwarp();
+        FTRACE(trs, g, 8)
         if (lane == 0) mbar_arrive(p_full);
       }
       // ---- epilogue: O / l -> bf16 (this group of the head dims), LSE (log2
@@ -523,6 +544,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
   }
 }
 
+#undef FTRACE
 // ============================================================== forward, ping-pong
 // Two query tiles per work item -- blocks 2p (A) and 2p+1 (B) of one
 // (sequence, head) -- share every K_j / V_j tile, and the tensor pipe
@@ -1335,6 +1357,8 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
     cudaFuncSetAttribute(attn_fwd_kernel<2, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
     cudaFuncSetAttribute(attn_fwd_kernel<2, 0, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
     cudaFuncSetAttribute(attn_fwd_kernel<4, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<4>::kSmem);
+    cudaFuncSetAttribute(attn_fwd_kernel<2, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
+    cudaFuncSetAttribute(attn_fwd_kernel<2, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
     cudaFuncSetAttribute(attn_fwd_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPPSmem);
     attr.fetch_or(1u << dev, std::memory_order_release);
   }
@@ -1345,7 +1369,10 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
   a.lse = lse;
   void* pb = prof_on() ? prof_begin(st) : nullptr;
   static const int fdiag = getenv("ADAPTRA_ATTN_DIAG") ? atoi(getenv("ADAPTRA_ATTN_DIAG")) : 0;
-  a.diag = fdiag & 0x400;
+  a.diag = fdiag & 0x600;
+  static long long* ftrace = nullptr;
+  if ((fdiag & 0x200) && !ftrace) cudaMalloc(&ftrace, 64 * 16 * sizeof(long long));
+  a.trace = ftrace;
   static long long* fcta = nullptr;
   if ((fdiag & 0x400) && !fcta) cudaMalloc(&fcta, 3 * 4096 * sizeof(long long));
   a.cta = fcta;
@@ -1374,6 +1401,10 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
     attn_fwd_kernel<2, 0, 1, 1><<<grid, FwdCfg<2>::kThreads + 128, FwdCfg<2>::kSmem, st>>>(m, a);
   } else if (p_tmem && nq == 2 && poly == 0) {
     attn_fwd_kernel<2, 0, 1><<<grid, FwdCfg<2>::kThreads, FwdCfg<2>::kSmem, st>>>(m, a);
+  } else if (p_tmem && nq == 2 && poly == 1) {
+    attn_fwd_kernel<2, 1, 1><<<grid, FwdCfg<2>::kThreads, FwdCfg<2>::kSmem, st>>>(m, a);
+  } else if (p_tmem && nq == 2 && poly == 2) {
+    attn_fwd_kernel<2, 2, 1><<<grid, FwdCfg<2>::kThreads, FwdCfg<2>::kSmem, st>>>(m, a);
   } else if (nq == 4 && p_tmem) {
     attn_fwd_kernel<4, 0, 1><<<grid, FwdCfg<4>::kThreads, FwdCfg<4>::kSmem, st>>>(m, a);
   } else if (nq == 4) {
@@ -1388,6 +1419,19 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
   if (fdiag & 0x400) {
     g_nqb = T / AT; g_Z = b * H; g_G = grid;
     cta_summary("attn_fwd", fcta, grid, fwd_blocks, st);
+  }
+  if (fdiag & 0x200) {
+    static int fdumped = 0;
+    long long hb[64 * 16];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(hb, ftrace, sizeof(hb), cudaMemcpyDeviceToHost);
+    if (fdumped++ == 2) {
+      for (int g = 0; g < 32; ++g) {
+        fprintf(stderr, "fwd g %2d", g);
+        for (int e = 0; e < 9; ++e) fprintf(stderr, " %7lld", hb[g * 16 + e] - hb[0]);
+        fprintf(stderr, "\n");
+      }
+    }
   }
   if (pb) {
     double fl = 4.0 * (double)T * T * AT * b * H * 0.5;  // algorithmic: QK^T + PV, causal half (R28)
