@@ -55,8 +55,8 @@ def parse():
     ap.add_argument("--d", type=int, default=2048)
     ap.add_argument("--heads", type=int, default=16)
     ap.add_argument("--T", type=int, default=2048)
-    ap.add_argument("--S", type=int, default=0, help="stages (default 4 on 1 GPU, 8 on 2+ GPUs)")
-    ap.add_argument("--N", type=int, default=0, help="microbatches (default 16, or 32 with S=8)")
+    ap.add_argument("--S", type=int, default=0, help="stages (default 8 at every GPU count)")
+    ap.add_argument("--N", type=int, default=0, help="microbatches (default 32)")
     ap.add_argument("--arms", default="adaptive,zb,1f1b,zb-inorder")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
