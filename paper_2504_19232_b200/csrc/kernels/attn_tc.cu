@@ -185,7 +185,14 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
   // S buffers in TMEM: with P in TMEM a buffer is busy until its P V is done,
   // so S(g + 1) with two buffers would wait for P V(g - 1) to drain the tensor
   // pipe; three keep it fed (O then sits at column 384; QT needs 384+ for Q)
-  constexpr int NS = (PT && !QT) ? 3 : 2;
+  // PT = 2 (with QT): one S buffer, released as soon as the softmax has
+  // loaded it, and P in two separate 64-column buffers -- S(g + 1) then
+  // overlaps the softmax of block g, S reads only K from shared memory (Q
+  // is in TMEM) and nothing waits for a P V to drain.  TMEM: S [0, 128),
+  // O [128, 256), P [256, 384), Q [384, 512).
+  constexpr bool SEP = PT == 2;
+  static_assert(!SEP || QT, "PT = 2 needs Q in TMEM");
+  constexpr int NS = SEP ? 1 : ((PT && !QT) ? 3 : 2);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;  // no static shared memory: the window starts 1024-aligned (checked)
   if (threadIdx.x == 0 && (smem_u32(smem) & 1023)) __trap();
@@ -200,8 +207,8 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
   uint64_t* s_full = t_empty + kFwdRing;    // [NS]
   uint64_t* s_empty = s_full + NS;          // [NS]
   uint64_t* p_full = s_empty + NS;
-  uint64_t* p_empty = p_full + 1;
-  uint64_t* o_full = p_empty + 1;
+  uint64_t* p_empty = p_full + 1;           // [2] (SEP: per P buffer; else [0] only)
+  uint64_t* o_full = p_empty + 2;
   uint64_t* q_empty = o_full + 1;           // the item's last S MMA read Q (QT: the copy warps read it)
   uint64_t* qt_full = q_empty + 1;          // QT: [2] Q of the item in TMEM buffer it & 1
   uint64_t* qt_empty = qt_full + 2;         // QT: [2] that item's last S MMA done
@@ -226,10 +233,11 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
     }
     for (int i = 0; i < NS; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], PT ? 1 : kSoftWarps);
+      mbar_init(&s_empty[i], PT == 1 ? 1 : kSoftWarps);
     }
     mbar_init(p_full, kSoftWarps);
-    mbar_init(p_empty, 1);
+    mbar_init(&p_empty[0], 1);
+    mbar_init(&p_empty[1], 1);
     mbar_init(o_full, 1);
     fence_barrier_init();
   }
@@ -238,7 +246,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tO = tmem + NS * 128;
+  const uint32_t tO = tmem + (SEP ? 128 : NS * 128);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -336,15 +344,18 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
           const uint32_t aV = smem_u32(sRing + vslot * TILE);
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks) {
-            if (PT)
+            if (SEP)
+              tc_mma_f16_ts(tO, tmem + 256 + (g & 1) * 64 + 8 * ks, desc_mnmajor(aV, ks), idesc(0, 1),
+                            (j > 0 || ks > 0) ? 1u : 0u);
+            else if (PT)
               tc_mma_f16_ts(tO, tmem + (g % NS) * 128 + 16 * ks, desc_mnmajor(aV, ks), idesc(0, 1),
                             (j > 0 || ks > 0) ? 1u : 0u);
             else
               tc_mma_f16(tO, desc_kmajor(aP, ks), desc_mnmajor(aV, ks), idesc(0, 1), (j > 0 || ks > 0) ? 1u : 0u);
           }
           tc_commit(&t_empty[vslot]);
-          tc_commit(p_empty);
-          if (PT) tc_commit(&s_empty[g % NS]);  // P (in the S buffer) consumed
+          tc_commit(&p_empty[SEP ? (g & 1) : 0]);
+          if (PT == 1) tc_commit(&s_empty[g % NS]);  // P (in the S buffer) consumed
         }
         FTRACE(trm, g, 2)
         __syncwarp();
@@ -428,7 +439,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
         FTRACE(trs, g, 4)
         tc_fence_before();
         __syncwarp();
-        if (!PT && lane == 0) mbar_arrive(&s_empty[tb]);
+        if (PT != 1 && lane == 0) mbar_arrive(&s_empty[tb]);
         if (j == qb) {
           const int lim = qi - (j * AT + qtr * CW);  // last visible column of this group
 #pragma unroll
@@ -475,7 +486,11 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
         // only a rescale of O has to wait -- the softmax of block g then
         // overlaps P V of block g - 1 instead of following it.
         const bool resc_o = j > 0 && __any_sync(0xffffffffu, resc);
-        if (!PT || resc_o) mbar_wait(p_empty, (g & 1) ^ 1);
+        if (SEP) {
+          if (resc_o) mbar_wait(&p_empty[(g - 1) & 1], ((g - 1) >> 1) & 1);  // P V(g - 1) done
+        } else if (!PT || resc_o) {
+          mbar_wait(&p_empty[0], (g & 1) ^ 1);
+        }
         if (resc_o) {
           tc_fence_after();
 #pragma unroll
@@ -490,7 +505,16 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
           tmem_st_wait();
         }
         FTRACE(trs, g, 7)
-        if (PT) {
+        if (SEP) {
+          // P buffer g & 1: P V(g - 2) has finished reading it; k-step ks of
+          // this thread's keys at columns [8 ks, 8 ks + 8)
+          mbar_wait(&p_empty[g & 1], ((g >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t pb = tmem + 256 + (g & 1) * 64 + ((uint32_t)(quad * 32) << 16) + qtr * (CW / 2);
+#pragma unroll
+          for (int c = 0; c < CW / 16; ++c) tmem_st8(pb + 8 * c, pk + 8 * c);
+          tmem_st_wait();
+        } else if (PT) {
 #pragma unroll
           for (int c = 0; c < CW / 16; ++c) tmem_st8(tmem + tb * 128 + lanes + 16 * c, pk + 8 * c);
           tmem_st_wait();
@@ -1356,6 +1380,7 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
     cudaFuncSetAttribute(attn_fwd_kernel<4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<4>::kSmem);
     cudaFuncSetAttribute(attn_fwd_kernel<2, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
     cudaFuncSetAttribute(attn_fwd_kernel<2, 0, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
+    cudaFuncSetAttribute(attn_fwd_kernel<2, 0, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
     cudaFuncSetAttribute(attn_fwd_kernel<4, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<4>::kSmem);
     cudaFuncSetAttribute(attn_fwd_kernel<2, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
     cudaFuncSetAttribute(attn_fwd_kernel<2, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
@@ -1394,9 +1419,13 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
   static const bool p_tmem = !(getenv("ADAPTRA_ATTN_FWD") && !strcmp(getenv("ADAPTRA_ATTN_FWD"), "smem"));
   // Q kept in TMEM as well ($ADAPTRA_ATTN_FWD=qtmem)
   static const bool q_tmem = getenv("ADAPTRA_ATTN_FWD") && !strcmp(getenv("ADAPTRA_ATTN_FWD"), "qtmem");
+  // one S buffer released at load, P in separate buffers, Q in TMEM ($ADAPTRA_ATTN_FWD=sep)
+  static const bool sep_p = getenv("ADAPTRA_ATTN_FWD") && !strcmp(getenv("ADAPTRA_ATTN_FWD"), "sep");
   if (pp_on && (T / AT) % 2 == 0 && !per_item) {
     const int pitems = b * H * (T / AT) / 2;
     attn_fwd_pp_kernel<<<std::min(pitems, n_use), kPPThreads, kPPSmem, st>>>(m, a);
+  } else if (sep_p && nq == 2 && poly == 0) {
+    attn_fwd_kernel<2, 0, 2, 1><<<grid, FwdCfg<2>::kThreads + 128, FwdCfg<2>::kSmem, st>>>(m, a);
   } else if (q_tmem && nq == 2 && poly == 0) {
     attn_fwd_kernel<2, 0, 1, 1><<<grid, FwdCfg<2>::kThreads + 128, FwdCfg<2>::kSmem, st>>>(m, a);
   } else if (p_tmem && nq == 2 && poly == 0) {
