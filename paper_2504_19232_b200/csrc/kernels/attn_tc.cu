@@ -178,8 +178,11 @@ __device__ __forceinline__ int fwd_item(int r, int c, int G) { return (r & 1) ? 
 // S MMAs read only K from shared memory.  Four more warps copy each item's Q
 // from its TMA tile into TMEM (thread = query row) once the item two back has
 // issued its last S; the Q tile in shared memory is free right after.
-template <int NQ, int POLY, int PT = 0, int QT = 0>
-__global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
+// S2 = 1 (with PT = 1, three S buffers): the S products are issued by a warp
+// of their own (warp 2 + kSoftWarps), so S(g + 1) no longer waits in one
+// issue stream behind P V(g - 1); each issuer commits its own MMAs.
+template <int NQ, int POLY, int PT = 0, int QT = 0, int S2 = 0>
+__global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0) + (S2 ? 32 : 0), 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const AttnArgs a) {
   constexpr int kFwdRing = FwdCfg<NQ>::kRing, kSoftWarps = FwdCfg<NQ>::kSoftWarps, CW = FwdCfg<NQ>::kCols;
   // S buffers in TMEM: with P in TMEM a buffer is busy until its P V is done,
@@ -193,6 +196,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
   constexpr bool SEP = PT == 2;
   static_assert(!SEP || QT, "PT = 2 needs Q in TMEM");
   constexpr int NS = SEP ? 1 : ((PT && !QT) ? 3 : 2);
+  static_assert(!S2 || (PT == 1 && !QT), "S2 needs P in TMEM with three S buffers");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;  // no static shared memory: the window starts 1024-aligned (checked)
   if (threadIdx.x == 0 && (smem_u32(smem) & 1023)) __trap();
@@ -273,7 +277,9 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 || (S2 && warp == 2 + kSoftWarps)) {
+    // S2: warp 1 issues the P V products, warp 2 + kSoftWarps the S products
+    const bool do_s = !S2 || warp != 1, do_pv = !S2 || warp == 1;
     // S of block j+1 is issued before waiting for P of block j, so the softmax
     // warps overlap the tensor pipe; across items, S of the next item's first
     // block follows this item's last P V.  Global block g: S buffer
@@ -312,7 +318,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
     int g0 = 0;  // global index of the item's first block
     int it = 0;
     int item = fwd_item(0, cta, G);
-    if (item < n_items) {
+    if (item < n_items && do_s) {
       wait_q(0);
       issue_s(0, 0);
     }
@@ -327,7 +333,8 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
       const int next = fwd_item(it + 1, cta, G);
       for (int j = 0; j < nb; ++j) {
         const int g = g0 + j;
-        if (j + 1 < nb) {
+        if (!do_s) {
+        } else if (j + 1 < nb) {
           issue_s(g + 1, it & 1);
           FTRACE(trm, g, 0)
         } else {
@@ -335,6 +342,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
           if (lane == 0) tc_commit(QT ? &qt_empty[it & 1] : q_empty);
           __syncwarp();
         }
+        if (!do_pv) continue;
         const int vslot = (2 * g + 1) % kFwdRing;
         mbar_wait(p_full, g & 1);
         FTRACE(trm, g, 1)
@@ -360,12 +368,12 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0), 1)
         FTRACE(trm, g, 2)
         __syncwarp();
       }
-      if (lane == 0) tc_commit(o_full);
+      if (do_pv && lane == 0) tc_commit(o_full);
       __syncwarp();
       // the next item's first S: its Q load started when this item's last S
       // finished, so it lands while the softmax warps run the last block and
       // the epilogue (waiting here before the last P V would put it on the path)
-      if (next < n_items) {
+      if (next < n_items && do_s) {
         wait_q(it + 1);
         issue_s(g0 + nb, (it + 1) & 1);
       }
@@ -1381,6 +1389,7 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
     cudaFuncSetAttribute(attn_fwd_kernel<2, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
     cudaFuncSetAttribute(attn_fwd_kernel<2, 0, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
     cudaFuncSetAttribute(attn_fwd_kernel<2, 0, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
+    cudaFuncSetAttribute(attn_fwd_kernel<2, 0, 1, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
     cudaFuncSetAttribute(attn_fwd_kernel<4, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<4>::kSmem);
     cudaFuncSetAttribute(attn_fwd_kernel<2, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
     cudaFuncSetAttribute(attn_fwd_kernel<2, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<2>::kSmem);
@@ -1421,9 +1430,13 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
   static const bool q_tmem = getenv("ADAPTRA_ATTN_FWD") && !strcmp(getenv("ADAPTRA_ATTN_FWD"), "qtmem");
   // one S buffer released at load, P in separate buffers, Q in TMEM ($ADAPTRA_ATTN_FWD=sep)
   static const bool sep_p = getenv("ADAPTRA_ATTN_FWD") && !strcmp(getenv("ADAPTRA_ATTN_FWD"), "sep");
+  // S and P V from two issuing warps ($ADAPTRA_ATTN_FWD=s2)
+  static const bool s2 = getenv("ADAPTRA_ATTN_FWD") && !strcmp(getenv("ADAPTRA_ATTN_FWD"), "s2");
   if (pp_on && (T / AT) % 2 == 0 && !per_item) {
     const int pitems = b * H * (T / AT) / 2;
     attn_fwd_pp_kernel<<<std::min(pitems, n_use), kPPThreads, kPPSmem, st>>>(m, a);
+  } else if (s2 && nq == 2 && poly == 0) {
+    attn_fwd_kernel<2, 0, 1, 0, 1><<<grid, FwdCfg<2>::kThreads + 32, FwdCfg<2>::kSmem, st>>>(m, a);
   } else if (sep_p && nq == 2 && poly == 0) {
     attn_fwd_kernel<2, 0, 2, 1><<<grid, FwdCfg<2>::kThreads + 128, FwdCfg<2>::kSmem, st>>>(m, a);
   } else if (q_tmem && nq == 2 && poly == 0) {

@@ -7,8 +7,8 @@ with the A tile multicast (opt-in), half of the attention forward's
 exponentials on the FMA pipe (ex2_poly), bias gradients by separate
 column-sum launches instead of inside the grouped dW launch, the attention
 forward with P through shared memory (the round-2 default before P stayed
-in TMEM), with Q in TMEM as well, and with one S buffer plus separate P
-buffers."""
+in TMEM), with Q in TMEM as well, with one S buffer plus separate P buffers, and
+with the S and P V products issued by two warps."""
 import os
 import subprocess
 import sys
@@ -30,7 +30,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
                                     {"ADAPTRA_DB_FUSED": "0"},
                                     {"ADAPTRA_ATTN_FWD": "smem"},
                                     {"ADAPTRA_ATTN_FWD": "qtmem"},
-                                    {"ADAPTRA_ATTN_FWD": "sep"}])
+                                    {"ADAPTRA_ATTN_FWD": "sep"},
+                                    {"ADAPTRA_ATTN_FWD": "s2"}])
 def test_stage_parity_under_toggle(toggle):
     env = dict(os.environ, **toggle)
     files = ["tests/test_gpu_stage.py", "tests/test_gpu_fullsize.py"]
