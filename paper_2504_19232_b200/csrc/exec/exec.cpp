@@ -5,8 +5,10 @@
 // only the ops after it in that stage's order and never another stage's
 // launches (no cross-stage head-of-line blocking).  Outputs are
 // handed to the outbox right after the producing op (adaptra_send, never
-// blocks).  ADAPTRA_EXEC_INORDER is the blocking baseline (N1).  Per-kind op
-// times feed the profiler (adaptra_exec_profile, a1).
+// blocks).  ADAPTRA_EXEC_INORDER (bounded send queue) and ADAPTRA_EXEC_NCCL
+// (NCCL send/recv in the compute sequence, receives posted per the R39 plan)
+// are the blocking baselines (N1).  Per-kind op times feed the profiler
+// (adaptra_exec_profile, a1).
 #include <cuda_runtime.h>
 
 #include <algorithm>
