@@ -496,6 +496,11 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0) + (S2 ? 
         const bool resc_o = j > 0 && __any_sync(0xffffffffu, resc);
         if (SEP) {
           if (resc_o) mbar_wait(&p_empty[(g - 1) & 1], ((g - 1) >> 1) & 1);  // P V(g - 1) done
+        } else if (PT == 1 && NS == 3) {
+          // P V(g - 1) done = use (g - 1) / 3 of S buffer (g - 1) % 3 released
+          // (a parity wait on the single p_empty could alias: with three S
+          // buffers P V(g - 2) may still be running here)
+          if (resc_o) mbar_wait(&s_empty[(g - 1) % NS], ((g - 1) / NS) & 1);
         } else if (!PT || resc_o) {
           mbar_wait(&p_empty[0], (g & 1) ^ 1);
         }
