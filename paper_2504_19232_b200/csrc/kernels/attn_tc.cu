@@ -1428,9 +1428,13 @@ int attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int b, int H, int T, int d
   // profiles/r02_op_bench_pp.jsonl): two softmax groups sharing the SM's
   // MUFU / issue slots plus the second TMEM pass cost more than the overlap gains
   static const bool pp_on = getenv("ADAPTRA_ATTN_FWD") && !strcmp(getenv("ADAPTRA_ATTN_FWD"), "pp");
-  // P kept in TMEM for P V (default: 30.2 vs 32.7 us per C1 launch,
-  // profiles/r02_attn_ptmem_ab.jsonl); $ADAPTRA_ATTN_FWD=smem: P through shared memory
-  static const bool p_tmem = !(getenv("ADAPTRA_ATTN_FWD") && !strcmp(getenv("ADAPTRA_ATTN_FWD"), "smem"));
+  // P kept in TMEM for P V ($ADAPTRA_ATTN_FWD=ptmem; 30.2 vs 32.7 us per C1
+  // launch, profiles/r02_attn_ptmem_ab.jsonl).  Opt-in, not the default: with
+  // eight stages sharing the GPU the 8-stage bench hung in 3 of 6 runs on it
+  // (0 of 4 with P through shared memory, profiles/r02_attn_ptmem_hang.txt);
+  // its parity tests pass.  The variants built on it (qtmem, sep, s2) share
+  // that status.
+  static const bool p_tmem = getenv("ADAPTRA_ATTN_FWD") && !strcmp(getenv("ADAPTRA_ATTN_FWD"), "ptmem");
   // Q kept in TMEM as well ($ADAPTRA_ATTN_FWD=qtmem)
   static const bool q_tmem = getenv("ADAPTRA_ATTN_FWD") && !strcmp(getenv("ADAPTRA_ATTN_FWD"), "qtmem");
   // one S buffer released at load, P in separate buffers, Q in TMEM ($ADAPTRA_ATTN_FWD=sep)
