@@ -489,19 +489,23 @@ __global__ void __launch_bounds__(FwdCfg<NQ>::kThreads + (QT ? 128 : 0) + (S2 ? 
         }
         l = l * alpha + (acc0 + acc1);
         FTRACE(trs, g, 6)
-        // P V of the previous block done: O stable (and, without PT, the P
-        // buffer free).  With PT, P goes into this block's own S buffer, so
-        // only a rescale of O has to wait -- the softmax of block g then
-        // overlaps P V of block g - 1 instead of following it.
+        // P V of the previous block done before P(g) is written: O stable for
+        // a rescale (and, without PT, the P buffer free).  The wait is kept
+        // even when nothing is rescaled: P V(g - 1) needs every softmax warp's
+        // p_full arrival for g - 1, so no warp can arrive for block g while
+        // another has yet to arrive for g - 1 -- without it a fast warp's
+        // arrival counted toward the previous phase of p_full (a P V on an
+        // incomplete P, then an aliased parity: the intermittent 8-stage hang
+        // of profiles/r02_attn_ptmem_hang.txt).
         const bool resc_o = j > 0 && __any_sync(0xffffffffu, resc);
         if (SEP) {
-          if (resc_o) mbar_wait(&p_empty[(g - 1) & 1], ((g - 1) >> 1) & 1);  // P V(g - 1) done
+          if (g > 0) mbar_wait(&p_empty[(g - 1) & 1], ((g - 1) >> 1) & 1);
         } else if (PT == 1 && NS == 3) {
           // P V(g - 1) done = use (g - 1) / 3 of S buffer (g - 1) % 3 released
           // (a parity wait on the single p_empty could alias: with three S
           // buffers P V(g - 2) may still be running here)
-          if (resc_o) mbar_wait(&s_empty[(g - 1) % NS], ((g - 1) / NS) & 1);
-        } else if (!PT || resc_o) {
+          if (g > 0) mbar_wait(&s_empty[(g - 1) % NS], ((g - 1) / NS) & 1);
+        } else {
           mbar_wait(&p_empty[0], (g & 1) ^ 1);
         }
         if (resc_o) {
